@@ -1,0 +1,121 @@
+// Winograd-domain channel contraction (reference: _kernels.py:94-105 `_hadamard_accumulate_nb`,
+// called from pipeline.py:143-145) as 36 batched int8 tensor-core GEMMs on sm_100a:
+//
+//     I[xi][t][o] = sum_c V[xi][t][c] * U[xi][o][c]        xi in 0..35, exact int32
+//
+// V (input-transform codes) and U (weight-transform codes) are int8, K-major ([rows][Cpad]).
+// One CTA computes a 128 x BN tile of one xi with tcgen05.mma kind::i8 (M=128, N=BN, K=32 per
+// instruction), operands staged by TMA into 128/64/32-byte-swizzled shared memory through a
+// STAGES-deep mbarrier ring, accumulator in TMEM.  Warp roles: w0 TMA producer, w1 TMEM owner +
+// single-thread MMA issuer, w2..w5 epilogue (tcgen05.ld 32 lanes each).  The epilogue is a
+// template functor so the same mainloop serves the max pass and the requantisation pass.
+#pragma once
+#include "wl_ptx.cuh"
+
+namespace wl {
+
+constexpr int kGemmThreads = 192;
+
+template <int BN, int SW, int STAGES>
+struct GemmSmem {
+  static constexpr int kA = 128 * SW;
+  static constexpr int kB = BN * SW;
+  static constexpr int kBytes = 1024 + STAGES * (kA + kB) + 256;
+};
+
+// Epilogue contract: Epi::apply(row, col0, vals[16], nvalid) per thread for 16 consecutive columns
+// of one row, then Epi::finish() once per epilogue thread.
+template <int BN, int SW, int STAGES, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int T,
+                   int Kout, int Cpad, Epi epi) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using L = GemmSmem<BN, SW, STAGES>;
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * L::kA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * L::kB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN, xi = blockIdx.z;
+  const int kblocks = Cpad / SW;
+  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], L::kA + L::kB);
+        tma_load_3d(sA + s * L::kA, &tmA, &full[s], kb * SW, m0, xi);
+        tma_load_3d(sB + s * L::kB, &tmB, &full[s], kb * SW, n0, xi);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_i8(128, BN);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < SW / 32; ++k) {
+          const uint64_t ad = smem_desc_kmajor(sA + s * L::kA + k * 32, SW);
+          const uint64_t bd = smem_desc_kmajor(sB + s * L::kB + k * 32, SW);
+          umma_i8(tmem_base, ad, bd, idesc, (kb | k) != 0);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(accfull);
+    }
+    __syncwarp();
+  } else {
+    mbar_wait(accfull, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int row = m0 + 32 * q + lane;
+    const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16);
+    epi.begin(xi, row, row < T);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t r[16];
+      tmem_ld16(taddr + c, r);
+      tmem_ld_wait();
+      const int col = n0 + c;
+      int nvalid = Kout - col;
+      nvalid = nvalid > 16 ? 16 : nvalid;
+      if (row < T && nvalid > 0) epi.apply(xi, row, col, reinterpret_cast<int32_t*>(r), nvalid);
+    }
+    epi.finish(xi, row, row < T);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace wl
