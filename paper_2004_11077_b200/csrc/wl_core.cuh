@@ -1,0 +1,192 @@
+// Device helpers shared by the transform, GEMM-epilogue and output kernels.
+//
+// Integer-exact stage rule: if a stage tensor equals f * T with T integer and
+// f > 0, the reference's codes rint(t / (max|t| / qmax)) (quantize.py:118-119) equal
+// rhe(qmax * T / max|T|) except where that ratio is an exact half-integer ("tie").  At ties the
+// fp64 reference resolves by rounding noise, so those elements — and the elements that attain the
+// stage maximum, whose fp64 value IS max_abs (quantize.py:141) — are re-evaluated ("replayed") in
+// fp64 with the reference's exact operation order: sandwich tmp = X.R then L.tmp with l ascending
+// (_kernels.py:69-92), Hadamard sum over c ascending from 0.0 (_kernels.py:94-105), every product
+// and sum rounded separately (__dmul_rn/__dadd_rn, never fused).
+#pragma once
+#include <cstdint>
+#include "wl_tables.cuh"
+
+namespace wl {
+
+enum StageId { ST_INPUT = 0, ST_WEIGHTS, ST_WT, ST_WBC, ST_IBC, ST_IT, ST_HAD, ST_OBC, ST_OUT, ST_COUNT };
+
+// Per (group, stage) reduction slot: M = max |T| (integer stages) or fp32 bits of max |x| (input /
+// weights); F = fp64 bits of the reference's max_abs (positive doubles order like uint64).
+struct Acc {
+  unsigned long long M;
+  unsigned long long F;
+};
+
+struct StageQ {
+  long long M;
+  double maxabs, scale;
+  float rcp;
+  int qmax;
+};
+
+__device__ __forceinline__ StageQ load_int_stage(const Acc& a, int qmax) {
+  StageQ s;
+  s.M = (long long)a.M;
+  s.maxabs = __longlong_as_double((long long)a.F);
+  s.qmax = qmax;
+  s.scale = s.maxabs > 0.0 ? s.maxabs / (double)qmax : 1.0;  // quantize.py:107-108
+  s.rcp = s.M ? (float)qmax / (float)s.M : 0.f;
+  return s;
+}
+// Input / weight stage: M holds the fp32 bits of max|v|, exact in fp64.
+__device__ __forceinline__ StageQ load_float_stage(const Acc& a, int qmax) {
+  StageQ s;
+  s.M = 0;
+  s.maxabs = (double)__uint_as_float((unsigned)a.M);
+  s.qmax = qmax;
+  s.scale = s.maxabs > 0.0 ? s.maxabs / (double)qmax : 1.0;
+  s.rcp = s.maxabs > 0.0 ? (float)((double)qmax / s.maxabs) : 0.f;
+  return s;
+}
+
+// Dequantised value of a code as the reference holds it after fake_quant (quantize.py:120-125).
+__device__ __forceinline__ double deq(int c, int qmax, double maxabs, double scale) {
+  return c == qmax ? maxabs : (c == -qmax ? -maxabs : (double)c * scale);
+}
+
+// rhe(qmax * |T| / M) with exact tie detection.  Fast path in fp32 (error < 5e-5 code units);
+// within 2e-4 of a half-integer the decision is redone exactly in int64.  On an exact tie `tie`
+// is set and floor is returned; the caller replays the element in fp64.
+__device__ __forceinline__ int rq(long long T, const StageQ& q, bool& tie) {
+  if (T == 0 || q.M == 0) return 0;
+  const long long a = T < 0 ? -T : T;
+  const float x = __fmul_rn((float)a, q.rcp);
+  const float k = floorf(x);
+  const float fr = x - k;
+  int c = (int)k;
+  if (fabsf(fr - 0.5f) > 2e-4f) {
+    c += fr > 0.5f;
+  } else {
+    const long long n2 = 2LL * q.qmax * a;
+    const long long rhs = (2LL * c + 1) * q.M;
+    if (n2 > rhs)
+      c += 1;
+    else if (n2 == rhs)
+      tie = true;
+  }
+  return T < 0 ? -c : c;
+}
+
+// Reference code of a replayed fp64 stage value (quantize.py:118-119).
+__device__ __forceinline__ int code_of(double t, const StageQ& q) {
+  double c = rint(t / q.scale);
+  c = c > q.qmax ? q.qmax : c;
+  c = c < -q.qmax ? -q.qmax : c;
+  return (int)c;
+}
+
+// Input / weight codes from fp32 values: rint(fp64(v) / scale) exactly as the reference, with an
+// fp32 fast path that is only trusted away from half-integers.
+__device__ __forceinline__ int quant_float(float v, const StageQ& q) {
+  if (q.maxabs == 0.0) return 0;
+  const float x = __fmul_rn(fabsf(v), q.rcp);
+  const float k = floorf(x);
+  const float fr = x - k;
+  int c;
+  if (fabsf(fr - 0.5f) > 1e-4f) {
+    c = (int)k + (fr > 0.5f);
+    c = c > q.qmax ? q.qmax : c;
+    return v < 0.f ? -c : c;
+  }
+  double d = rint((double)v / q.scale);
+  d = d > q.qmax ? q.qmax : d;
+  d = d < -q.qmax ? -q.qmax : d;
+  return (int)d;
+}
+
+// ---------------------------------------------------------------- fp64 replays (rare path)
+
+// out[i][j] of L . X . L^T, L is R x B (row-major fp64), X is B x B given as codes + dequant params.
+__device__ __noinline__ double replay_sandwich(const double* __restrict__ L, int R, int B, const int* codes, int qmax,
+                                               double maxabs, double scale, int i, int j) {
+  (void)R;
+  double tmp[6];
+  for (int l = 0; l < B; ++l) {
+    double s = 0.0;
+    for (int l2 = 0; l2 < B; ++l2) s = __dadd_rn(s, __dmul_rn(deq(codes[l * B + l2], qmax, maxabs, scale), L[j * B + l2]));
+    tmp[l] = s;
+  }
+  double out = 0.0;
+  for (int l = 0; l < B; ++l) out = __dadd_rn(out, __dmul_rn(L[i * B + l], tmp[l]));
+  return out;
+}
+
+// Hadamard element: sum_c deq(u_c) * deq(v_c), c ascending from 0.0 (_kernels.py:99-104).
+__device__ __noinline__ double replay_hadamard(const int8_t* __restrict__ u, const int8_t* __restrict__ v, int C,
+                                               StageQ qu, StageQ qv) {
+  double acc = 0.0;
+  for (int c = 0; c < C; ++c)
+    acc = __dadd_rn(acc, __dmul_rn(deq(u[c], qu.qmax, qu.maxabs, qu.scale), deq(v[c], qv.qmax, qv.maxabs, qv.scale)));
+  return acc;
+}
+
+__device__ __forceinline__ unsigned long long dbits(double d) { return (unsigned long long)__double_as_longlong(d); }
+
+// Decide whether this lane must replay its local-argmax elements: only lanes holding the maximum
+// of their warp (when the warp shares one group), and only while that maximum can still be the
+// group's global maximum.  Any element equal to the final maximum passes this test because the
+// global value only grows.  fp64 magnitudes are ordered like the integers (gap >= 1/M relative,
+// fp64 noise < 1e-13), so an atomicMax over replayed values yields the exact max_abs.
+__device__ __forceinline__ bool replay_gate(long long m, int g, const Acc* acc, int stride, bool& uniform,
+                                            long long& wmax) {
+  const unsigned full = 0xffffffffu;
+  const int g0 = __shfl_sync(full, g, 0);
+  uniform = __all_sync(full, g == g0);
+  wmax = m;
+  if (uniform) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      long long other = __shfl_xor_sync(full, wmax, o);
+      wmax = other > wmax ? other : wmax;
+    }
+  }
+  if (m <= 0 || g < 0) return false;
+  if (uniform && m != wmax) return false;
+  const long long cur = (long long)(*(volatile const unsigned long long*)&acc[(size_t)g * stride].M);
+  return m >= cur;
+}
+
+__device__ __forceinline__ void publish_max(long long m, int g, Acc* acc, int stride, bool uniform, long long wmax) {
+  if (uniform) {
+    if ((threadIdx.x & 31) == 0 && wmax > 0 && g >= 0) atomicMax(&acc[(size_t)g * stride].M, (unsigned long long)wmax);
+  } else if (m > 0 && g >= 0) {
+    atomicMax(&acc[(size_t)g * stride].M, (unsigned long long)m);
+  }
+}
+
+// Compile-time sandwich out = L . X . L^T with L a tab:: matrix (R x C), X (C x C).
+template <class L, typename TO>
+__device__ __forceinline__ void sandwich(const int (&X)[L::C][L::C], TO (&out)[L::R][L::R]) {
+  int tmp[L::C][L::R];
+#pragma unroll
+  for (int i = 0; i < L::C; ++i)
+#pragma unroll
+    for (int j = 0; j < L::R; ++j) {
+      int s = 0;
+#pragma unroll
+      for (int l = 0; l < L::C; ++l) s += X[i][l] * L::e(j, l);
+      tmp[i][j] = s;
+    }
+#pragma unroll
+  for (int i = 0; i < L::R; ++i)
+#pragma unroll
+    for (int j = 0; j < L::R; ++j) {
+      TO s = 0;
+#pragma unroll
+      for (int l = 0; l < L::C; ++l) s += (TO)L::e(i, l) * (TO)tmp[l][j];
+      out[i][j] = s;
+    }
+}
+
+}  // namespace wl

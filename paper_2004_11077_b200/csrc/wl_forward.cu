@@ -1,0 +1,599 @@
+// C-ABI entry points of libwinoleg_b200.so (include/winoleg_b200.h) and the host orchestration of
+// the forward dependency chain.  See wl_kernels.cuh for the data layout and DESIGN.md for the
+// pass structure and rooflines.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <vector>
+#include <cstring>
+#include <string>
+
+#include "../../include/winoleg_b200.h"
+#include "gemm_i8.cuh"
+#include "wl_kernels.cuh"
+#include "wl_tmap.h"
+
+using namespace wl;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define WL_CUDA(expr)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (expr);                                                                   \
+    if (e_ != cudaSuccess) return fail(WL_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+struct wl_plan {
+  int mode;
+  PlanF64* d_pf;
+};
+
+// ------------------------------------------------------------------ stage-width plumbing
+
+static int check_bits(const wl_qcfg* q) {
+  if (!q) return fail(WL_ERR_ARG, "qcfg is NULL");
+  const int v[7] = {q->input_bits,       q->weight_bits,   q->input_transform_bits, q->weight_transform_bits,
+                    q->base_change_bits, q->hadamard_bits, q->output_transform_bits};
+  for (int i = 0; i < 7; ++i)
+    if (v[i] < 2) return fail(WL_ERR_BITS, "stage widths must be >= 2 (quantize.py:52-55)");
+  if (q->input_bits > 8 || q->weight_bits > 8 || q->input_transform_bits > 8 || q->weight_transform_bits > 8 ||
+      q->base_change_bits > 8)
+    return fail(WL_ERR_BITS, "input/weight/transform/base-change widths must be <= 8 (int8 tensor-core operands)");
+  if (q->hadamard_bits > 9) return fail(WL_ERR_BITS, "hadamard_bits must be <= 9");
+  if (q->output_transform_bits > 16) return fail(WL_ERR_BITS, "output_transform_bits must be <= 16");
+  return WL_OK;
+}
+
+static Bits make_bits(const wl_qcfg* q) {
+  auto qm = [](int b) { return (1 << (b - 1)) - 1; };
+  Bits b;
+  b.q[ST_INPUT] = qm(q->input_bits);
+  b.q[ST_WEIGHTS] = qm(q->weight_bits);
+  b.q[ST_WT] = qm(q->weight_transform_bits);
+  b.q[ST_WBC] = qm(q->base_change_bits);
+  b.q[ST_IBC] = qm(q->base_change_bits);
+  b.q[ST_IT] = qm(q->input_transform_bits);
+  b.q[ST_HAD] = qm(q->hadamard_bits);
+  b.q[ST_OBC] = qm(q->base_change_bits);
+  b.q[ST_OUT] = qm(q->output_transform_bits);
+  return b;
+}
+
+static int stage_bits(const wl_qcfg* q, int st) {
+  switch (st) {
+    case ST_INPUT: return q->input_bits;
+    case ST_WEIGHTS: return q->weight_bits;
+    case ST_WT: return q->weight_transform_bits;
+    case ST_IT: return q->input_transform_bits;
+    case ST_HAD: return q->hadamard_bits;
+    case ST_OUT: return q->output_transform_bits;
+    default: return q->base_change_bits;
+  }
+}
+
+static const int kCanonOrder[6] = {ST_INPUT, ST_WEIGHTS, ST_WT, ST_IT, ST_HAD, ST_OUT};
+static const int kLegOrder[9] = {ST_INPUT, ST_WEIGHTS, ST_WT, ST_WBC, ST_IBC, ST_IT, ST_HAD, ST_OBC, ST_OUT};
+
+// ------------------------------------------------------------------ geometry / workspace
+
+struct Layout {
+  Geo g;
+  size_t off_acc, off_c0, off_v, off_h, total;
+  int groups, hbytes;
+};
+
+static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
+  if (!s) return fail(WL_ERR_ARG, "shape is NULL");
+  if (s->n < 1 || s->c_in < 1 || s->c_out < 1 || s->pad < 0)
+    return fail(WL_ERR_ARG, "bad shape n=%d c_in=%d c_out=%d pad=%d", s->n, s->c_in, s->c_out, s->pad);
+  const int Hp = s->h + 2 * s->pad, Wp = s->w + 2 * s->pad;
+  if (Hp < 3 || Wp < 3) return fail(WL_ERR_ARG, "input %dx%d is smaller than the 3x3 kernel", Hp, Wp);
+  if (s->images_per_group < 1 || s->n % s->images_per_group)
+    return fail(WL_ERR_ARG, "images_per_group=%d must divide n=%d", s->images_per_group, s->n);
+  Geo& g = L->g;
+  g.N = s->n;
+  g.C = s->c_in;
+  g.K = s->c_out;
+  g.H = s->h;
+  g.W = s->w;
+  g.pad = s->pad;
+  g.Ho = Hp - 2;
+  g.Wo = Wp - 2;
+  g.th = (g.Ho + 3) / 4;
+  g.tw = (g.Wo + 3) / 4;
+  g.TP = g.th * g.tw;
+  g.T = g.N * g.TP;
+  g.Cp = round_up(g.C, 32);
+  g.Kp = g.K <= 64 ? 64 : (g.K <= 128 ? 128 : round_up(g.K, 256));
+  g.ipg = s->images_per_group;
+  if ((long long)g.T * g.Cp * 36 > (1LL << 40)) return fail(WL_ERR_ARG, "problem too large");
+  L->groups = g.N / g.ipg;
+  L->hbytes = q->hadamard_bits > 8 ? 2 : 1;
+  size_t o = 0;
+  L->off_acc = o;
+  o = align256(o + sizeof(Acc) * ST_COUNT * L->groups);
+  L->off_c0 = o;
+  o = align256(o + (size_t)g.N * g.H * g.W * g.Cp);
+  L->off_v = o;
+  o = align256(o + (size_t)36 * g.T * g.Cp);
+  L->off_h = o;
+  o = align256(o + (size_t)36 * g.T * g.Kp * L->hbytes);
+  L->total = o;
+  return WL_OK;
+}
+
+struct WeightHeader {
+  Acc wacc[ST_COUNT];
+  int K, C, Kp, Cp, mode, wstage;
+  wl_qcfg q;
+};
+
+static size_t weight_cache_bytes(int K, int C, int* Kp, int* Cp) {
+  *Cp = round_up(C, 32);
+  *Kp = K <= 64 ? 64 : (K <= 128 ? 128 : round_up(K, 256));
+  return align256(sizeof(WeightHeader)) + (size_t)36 * (*Kp) * (*Cp);
+}
+
+// ------------------------------------------------------------------ GEMM epilogues
+
+struct EpiHadMax {
+  Acc* acc;
+  const Acc* wacc;
+  const int8_t* U;
+  const int8_t* V;
+  Geo g;
+  int wstage, qmax_u, qmax_v;
+  long long m;
+  int cnt, grp;
+  int pos[4];
+  __device__ void begin(int, int row, bool valid) {
+    m = 0;
+    cnt = 0;
+    grp = valid ? (row / g.TP) / g.ipg : -1;
+  }
+  __device__ void apply(int, int, int col, const int32_t* v, int n) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j >= n) break;
+      long long a = v[j] < 0 ? -(long long)v[j] : (long long)v[j];
+      if (a > m) {
+        m = a;
+        cnt = 0;
+      }
+      if (a == m) {
+        if (cnt < 4) pos[cnt] = col + j;
+        ++cnt;
+      }
+    }
+  }
+  __device__ void finish(int xi, int row, bool) {
+    bool uniform;
+    long long wmax;
+    Acc* a = acc + ST_HAD;
+    if (replay_gate(m, grp, a, ST_COUNT, uniform, wmax)) {
+      const StageQ qu = load_int_stage(wacc[wstage], qmax_u);
+      const StageQ qv = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_IT], qmax_v);
+      const int8_t* vrow = V + ((size_t)xi * g.T + row) * g.Cp;
+      double f = 0.0;
+      if (cnt <= 4) {
+        for (int p = 0; p < cnt; ++p)
+          f = fmax(f, fabs(replay_hadamard(U + ((size_t)xi * g.Kp + pos[p]) * g.Cp, vrow, g.C, qu, qv)));
+      } else {  // many equal maxima in this row: find them all on CUDA cores
+        for (int k = 0; k < g.K; ++k) {
+          const int8_t* urow = U + ((size_t)xi * g.Kp + k) * g.Cp;
+          long long s = 0;
+          for (int c = 0; c < g.C; ++c) s += (int)urow[c] * (int)vrow[c];
+          if ((s < 0 ? -s : s) == m) f = fmax(f, fabs(replay_hadamard(urow, vrow, g.C, qu, qv)));
+        }
+      }
+      atomicMax(&a[(size_t)grp * ST_COUNT].F, dbits(f));
+    }
+    publish_max(m, grp, a, ST_COUNT, uniform, wmax);
+  }
+};
+
+template <typename HT>
+struct EpiHadRq {
+  Acc* acc;
+  const Acc* wacc;
+  const int8_t* U;
+  const int8_t* V;
+  HT* h;
+  Geo g;
+  int wstage, qmax_u, qmax_v, qmax_h;
+  StageQ q;
+  int grp;
+  __device__ void begin(int, int row, bool valid) {
+    grp = valid ? (row / g.TP) / g.ipg : 0;
+    q = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h);
+  }
+  __device__ void apply(int xi, int row, int col, const int32_t* v, int n) {
+    HT out[16];
+    bool any = false;
+    bool tie[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      bool t = false;
+      out[j] = (HT)rq(v[j], q, t);
+      tie[j] = t && j < n;
+      any |= tie[j];
+    }
+    if (any) {
+      const StageQ qu = load_int_stage(wacc[wstage], qmax_u);
+      const StageQ qv = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_IT], qmax_v);
+      const int8_t* vrow = V + ((size_t)xi * g.T + row) * g.Cp;
+      for (int j = 0; j < 16; ++j)
+        if (tie[j])
+          out[j] = (HT)code_of(replay_hadamard(U + ((size_t)xi * g.Kp + col + j) * g.Cp, vrow, g.C, qu, qv), q);
+    }
+    HT* dst = h + ((size_t)xi * g.T + row) * g.Kp + col;
+    if (sizeof(HT) == 1) {
+      *reinterpret_cast<int4*>(dst) = *reinterpret_cast<const int4*>(out);
+    } else {
+      reinterpret_cast<int4*>(dst)[0] = reinterpret_cast<const int4*>(out)[0];
+      reinterpret_cast<int4*>(dst)[1] = reinterpret_cast<const int4*>(out)[1];
+    }
+  }
+  __device__ void finish(int, int, bool) {}
+};
+
+template <int BN, int SW, class Epi>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo& g, const Epi& e, cudaStream_t st) {
+  constexpr int STAGES = 4;
+  using L = GemmSmem<BN, SW, STAGES>;
+  auto kern = gemm_i8_kernel<BN, SW, STAGES, Epi>;
+  static bool attr_set = false;  // per instantiation; idempotent
+  if (!attr_set) {
+    WL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes));
+    attr_set = true;
+  }
+  dim3 grid((g.T + 127) / 128, g.Kp / BN, 36);
+  kern<<<grid, kGemmThreads, L::kBytes, st>>>(ta, tb, g.T, g.K, g.Cp, e);
+  WL_CUDA(cudaGetLastError());
+  return WL_OK;
+}
+
+template <class Epi>
+static int dispatch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo& g, int bn, int sw, const Epi& e,
+                         cudaStream_t st) {
+#define WL_G(BN_, SW_) \
+  if (bn == BN_ && sw == SW_) return launch_gemm<BN_, SW_, Epi>(ta, tb, g, e, st);
+  WL_G(64, 32) WL_G(64, 64) WL_G(64, 128) WL_G(128, 32) WL_G(128, 64) WL_G(128, 128) WL_G(256, 32) WL_G(256, 64)
+  WL_G(256, 128)
+#undef WL_G
+  return fail(WL_ERR_ARG, "no GEMM tile for BN=%d SW=%d", bn, sw);
+}
+
+static void gemm_tiles(const Geo& g, int* bn, int* sw) {
+  *bn = g.Kp >= 256 ? 256 : g.Kp;
+  *sw = g.Cp % 128 == 0 ? 128 : (g.Cp % 64 == 0 ? 64 : 32);
+}
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+const char* wl_last_error(void) { return g_err.c_str(); }
+
+int wl_plan_create(int o, int k, int mode, const int64_t* int_mats, const double* f64_mats, wl_plan** out) {
+  if (!out || !int_mats || !f64_mats) return fail(WL_ERR_ARG, "NULL argument");
+  if (o != 4 || k != 3) return fail(WL_ERR_PLAN, "only F(4,3) is compiled for sm_100a (got F(%d,%d))", o, k);
+  if (mode != WL_CANONICAL && mode != WL_LEGENDRE) return fail(WL_ERR_ARG, "unknown mode %d", mode);
+  // verify the host construction against the compiled tables
+  int bad = 0;
+  const int64_t* p = int_mats;
+  auto check = [&](auto tag, int R, int C) {
+    using M = decltype(tag);
+    for (int i = 0; i < R; ++i)
+      for (int j = 0; j < C; ++j)
+        if (*p++ != M::e(i, j)) ++bad;
+  };
+  PlanF64 pf;
+  memset(&pf, 0, sizeof(pf));
+  const double* f = f64_mats;
+  if (mode == WL_CANONICAL) {
+    check(tab::Can_WT{}, 6, 3);
+    check(tab::Can_IT{}, 6, 6);
+    check(tab::Can_OT{}, 4, 6);
+    memcpy(pf.wt, f, 18 * 8);
+    memcpy(pf.it, f + 18, 36 * 8);
+    memcpy(pf.ot, f + 54, 24 * 8);
+  } else {
+    check(tab::Leg_WT{}, 6, 3);
+    check(tab::Leg_WBC{}, 6, 6);
+    check(tab::Leg_IBC{}, 6, 6);
+    check(tab::Leg_IT{}, 6, 6);
+    check(tab::Leg_OBC{}, 6, 6);
+    check(tab::Leg_OT{}, 4, 6);
+    memcpy(pf.wt, f, 18 * 8);
+    memcpy(pf.wbc, f + 18, 36 * 8);
+    memcpy(pf.ibc, f + 54, 36 * 8);
+    memcpy(pf.it, f + 90, 36 * 8);
+    memcpy(pf.obc, f + 126, 36 * 8);
+    memcpy(pf.ot, f + 162, 24 * 8);
+  }
+  if (bad)
+    return fail(WL_ERR_PLAN, "plan differs from the compiled default-point F(4,3) tables in %d entries", bad);
+  wl_plan* pl = new wl_plan;
+  pl->mode = mode;
+  cudaError_t e = cudaMalloc(&pl->d_pf, sizeof(PlanF64));
+  if (e == cudaSuccess) e = cudaMemcpy(pl->d_pf, &pf, sizeof(PlanF64), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    delete pl;
+    return fail(WL_ERR_CUDA, "plan upload: %s", cudaGetErrorString(e));
+  }
+  *out = pl;
+  return WL_OK;
+}
+
+int wl_plan_destroy(wl_plan* plan) {
+  if (!plan) return WL_OK;
+  cudaFree(plan->d_pf);
+  delete plan;
+  return WL_OK;
+}
+
+int wl_plan_mode(const wl_plan* plan) { return plan ? plan->mode : WL_ERR_ARG; }
+
+int wl_num_stages(const wl_plan* plan) { return plan ? (plan->mode == WL_LEGENDRE ? 9 : 6) : WL_ERR_ARG; }
+
+int wl_weight_cache_size(const wl_plan* plan, int c_out, int c_in, size_t* bytes) {
+  if (!plan || !bytes || c_out < 1 || c_in < 1) return fail(WL_ERR_ARG, "bad weight-cache query");
+  int Kp, Cp;
+  *bytes = weight_cache_bytes(c_out, c_in, &Kp, &Cp);
+  return WL_OK;
+}
+
+int wl_weight_transform(const wl_plan* plan, const wl_qcfg* q, const float* w, int c_out, int c_in, void* cache,
+                        size_t cache_bytes, void* stream) {
+  if (!plan || !w || !cache) return fail(WL_ERR_ARG, "NULL argument");
+  int rc = check_bits(q);
+  if (rc) return rc;
+  int Kp, Cp;
+  const size_t need = weight_cache_bytes(c_out, c_in, &Kp, &Cp);
+  if (cache_bytes < need) return fail(WL_ERR_WORKSPACE, "weight cache needs %zu bytes", need);
+  cudaStream_t st = (cudaStream_t)stream;
+  WeightHeader hdr;
+  memset(&hdr, 0, sizeof(hdr));
+  hdr.K = c_out;
+  hdr.C = c_in;
+  hdr.Kp = Kp;
+  hdr.Cp = Cp;
+  hdr.mode = plan->mode;
+  hdr.wstage = plan->mode == WL_LEGENDRE ? ST_WBC : ST_WT;
+  hdr.q = *q;
+  WeightHeader* dh = reinterpret_cast<WeightHeader*>(cache);
+  int8_t* U = reinterpret_cast<int8_t*>(cache) + align256(sizeof(WeightHeader));
+  WL_CUDA(cudaMemcpyAsync(dh, &hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
+  WL_CUDA(cudaMemsetAsync(U, 0, (size_t)36 * Kp * Cp, st));
+  const Bits b = make_bits(q);
+  const long long nw = (long long)c_out * c_in * 9;
+  absmax_weights_kernel<<<(int)std::min<long long>((nw + 255) / 256, 1024), 256, 0, st>>>(w, nw, dh->wacc);
+  // "weights" stage max_abs is exact: F = fp64(max |w|) is filled by the readers from M.
+  const int threads = 256, blocks = (c_out * c_in + threads - 1) / threads;
+  if (plan->mode == WL_CANONICAL) {
+    weight_stage_kernel<0, 0><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+    weight_stage_kernel<0, 2><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+  } else {
+    weight_stage_kernel<1, 0><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+    weight_stage_kernel<1, 1><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+    weight_stage_kernel<1, 2><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+  }
+  WL_CUDA(cudaGetLastError());
+  return WL_OK;
+}
+
+int wl_workspace_size(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* bytes) {
+  if (!plan || !bytes) return fail(WL_ERR_ARG, "NULL argument");
+  int rc = check_bits(q);
+  if (rc) return rc;
+  Layout L;
+  rc = make_layout(s, q, &L);
+  if (rc) return rc;
+  *bytes = L.total;
+  return WL_OK;
+}
+
+int wl_debug_layout(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* off, int* dims) {
+  if (!plan || !off || !dims) return fail(WL_ERR_ARG, "NULL argument");
+  int rc = check_bits(q);
+  if (rc) return rc;
+  Layout L;
+  rc = make_layout(s, q, &L);
+  if (rc) return rc;
+  off[0] = L.off_c0;
+  off[1] = L.off_v;
+  off[2] = L.off_h;
+  off[3] = L.off_acc;
+  dims[0] = L.g.Cp;
+  dims[1] = L.g.Kp;
+  dims[2] = L.g.T;
+  dims[3] = L.g.TP;
+  return WL_OK;
+}
+
+int wl_forward_launches(const wl_plan* plan, const wl_shape*, const wl_qcfg*) {
+  if (!plan) return WL_ERR_ARG;
+  // absmax, quant, input passes (2|3), gemm max, gemm requant, output passes (2|3)
+  return plan->mode == WL_LEGENDRE ? 10 : 8;
+}
+
+int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
+               const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!plan || !x || !cache || !y || !workspace) return fail(WL_ERR_ARG, "NULL argument");
+  int rc = check_bits(q);
+  if (rc) return rc;
+  Layout L;
+  rc = make_layout(s, q, &L);
+  if (rc) return rc;
+  if (workspace_bytes < L.total) return fail(WL_ERR_WORKSPACE, "workspace needs %zu bytes", L.total);
+  const Geo& g = L.g;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  Acc* acc = reinterpret_cast<Acc*>(ws + L.off_acc);
+  int8_t* c0 = reinterpret_cast<int8_t*>(ws + L.off_c0);
+  int8_t* V = reinterpret_cast<int8_t*>(ws + L.off_v);
+  void* h = ws + L.off_h;
+  const WeightHeader* wh = reinterpret_cast<const WeightHeader*>(cache);
+  const int8_t* U = reinterpret_cast<const int8_t*>(cache) + align256(sizeof(WeightHeader));
+  const Bits b = make_bits(q);
+  const bool leg = plan->mode == WL_LEGENDRE;
+
+  WL_CUDA(cudaMemsetAsync(acc, 0, sizeof(Acc) * ST_COUNT * L.groups, st));
+  {
+    const long long per_image = (long long)g.C * g.H * g.W;
+    int bx = (int)std::min<long long>((per_image / 4 + 255) / 256, 64);
+    absmax_f32_kernel<<<dim3(std::max(bx, 1), g.N), 256, 0, st>>>(x, per_image, g.ipg, acc);
+    quant_input_kernel<<<dim3(g.Cp / 32, g.H, g.N), 256, 0, st>>>(x, c0, g, b, acc);
+  }
+  const long long tc = (long long)g.T * g.C;
+  const int tb = 256;
+  const unsigned tgrid = (unsigned)((tc + tb - 1) / tb);
+  if (!leg) {
+    input_stage_kernel<0, 0><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    input_stage_kernel<0, 2><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+  } else {
+    input_stage_kernel<1, 0><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    input_stage_kernel<1, 1><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    input_stage_kernel<1, 2><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+  }
+  WL_CUDA(cudaGetLastError());
+  // padded channels of V must be zero for the GEMM: the stage kernels only write c < C
+  // (zeroed once per call when C is not a multiple of 32)
+  if (g.Cp != g.C) {
+    // write zeros for the padding columns through a 2-D memset
+    WL_CUDA(cudaMemset2DAsync(V + g.C, g.Cp, 0, g.Cp - g.C, (size_t)36 * g.T, st));
+  }
+
+  int bn, sw;
+  gemm_tiles(g, &bn, &sw);
+  CUtensorMap ta, tbm;
+  if (!make_tmap_i8_3d(&ta, V, g.Cp, g.T, 36, sw, 128) || !make_tmap_i8_3d(&tbm, U, g.Cp, g.Kp, 36, sw, bn))
+    return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  const int qu = b.q[wh ? (leg ? ST_WBC : ST_WT) : ST_WT];
+  {
+    EpiHadMax e;
+    e.acc = acc;
+    e.wacc = wh->wacc;
+    e.U = U;
+    e.V = V;
+    e.g = g;
+    e.wstage = leg ? ST_WBC : ST_WT;
+    e.qmax_u = qu;
+    e.qmax_v = b.q[ST_IT];
+    rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
+    if (rc) return rc;
+  }
+  if (L.hbytes == 1) {
+    EpiHadRq<int8_t> e;
+    e.acc = acc;
+    e.wacc = wh->wacc;
+    e.U = U;
+    e.V = V;
+    e.h = reinterpret_cast<int8_t*>(h);
+    e.g = g;
+    e.wstage = leg ? ST_WBC : ST_WT;
+    e.qmax_u = qu;
+    e.qmax_v = b.q[ST_IT];
+    e.qmax_h = b.q[ST_HAD];
+    rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
+  } else {
+    EpiHadRq<int16_t> e;
+    e.acc = acc;
+    e.wacc = wh->wacc;
+    e.U = U;
+    e.V = V;
+    e.h = reinterpret_cast<int16_t*>(h);
+    e.g = g;
+    e.wstage = leg ? ST_WBC : ST_WT;
+    e.qmax_u = qu;
+    e.qmax_v = b.q[ST_IT];
+    e.qmax_h = b.q[ST_HAD];
+    rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
+  }
+  if (rc) return rc;
+
+  const long long oc = (long long)g.T * g.K;
+  const unsigned ogrid = (unsigned)((oc + tb - 1) / tb);
+#define WL_OUT(HT)                                                                                             \
+  if (!leg) {                                                                                                  \
+    output_stage_kernel<0, 0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+    output_stage_kernel<0, 2, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+  } else {                                                                                                     \
+    output_stage_kernel<1, 0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+    output_stage_kernel<1, 1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+    output_stage_kernel<1, 2, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+  }
+  if (L.hbytes == 1) {
+    WL_OUT(int8_t)
+  } else {
+    WL_OUT(int16_t)
+  }
+#undef WL_OUT
+  WL_CUDA(cudaGetLastError());
+  return WL_OK;
+}
+
+int wl_read_stats(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, const void* cache, const void* workspace,
+                  wl_stage_stat* out, void* stream) {
+  if (!plan || !cache || !workspace || !out) return fail(WL_ERR_ARG, "NULL argument");
+  int rc = check_bits(q);
+  if (rc) return rc;
+  Layout L;
+  rc = make_layout(s, q, &L);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<Acc> acc((size_t)L.groups * ST_COUNT);
+  WeightHeader wh;
+  WL_CUDA(cudaMemcpyAsync(acc.data(), reinterpret_cast<const uint8_t*>(workspace) + L.off_acc,
+                          acc.size() * sizeof(Acc), cudaMemcpyDeviceToHost, st));
+  WL_CUDA(cudaMemcpyAsync(&wh, cache, sizeof(wh), cudaMemcpyDeviceToHost, st));
+  WL_CUDA(cudaStreamSynchronize(st));
+  const bool leg = plan->mode == WL_LEGENDRE;
+  const int ns = leg ? 9 : 6;
+  const int* order = leg ? kLegOrder : kCanonOrder;
+  for (int gi = 0; gi < L.groups; ++gi)
+    for (int i = 0; i < ns; ++i) {
+      const int stg = order[i];
+      const bool wside = stg == ST_WEIGHTS || stg == ST_WT || stg == ST_WBC;
+      const Acc& a = wside ? wh.wacc[stg] : acc[(size_t)gi * ST_COUNT + stg];
+      const int bits = wside ? stage_bits(&wh.q, stg) : stage_bits(q, stg);
+      double mx;
+      if (stg == ST_INPUT || stg == ST_WEIGHTS) {
+        unsigned u = (unsigned)a.M;
+        float fv;
+        memcpy(&fv, &u, 4);
+        mx = (double)fv;
+      } else {
+        long long fb = (long long)a.F;
+        memcpy(&mx, &fb, 8);
+      }
+      const int qmax = (1 << (bits - 1)) - 1;
+      wl_stage_stat& o = out[(size_t)gi * ns + i];
+      o.bits = bits;
+      o.max_abs = mx;
+      o.scale = mx > 0.0 ? mx / (double)qmax : 1.0;
+    }
+  return WL_OK;
+}
+
+}  // extern "C"

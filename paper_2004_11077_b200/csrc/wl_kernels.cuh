@@ -1,0 +1,447 @@
+// Forward-path kernels of the quantized Winograd F(4x4,3x3) layer (canonical or Legendre base).
+//
+// Reference dataflow (pipeline.py:106-158 with the cast hook of quantize.py:129-148):
+//   input -> [input_base_change] -> input_transform -> hadamard -> [output_base_change] -> output
+// Every stage is an integer sandwich D*L . codes . (D*L)^T of the previous stage's codes; each
+// stage needs its global max before its codes exist, so every kernel below is one pass of the
+// dependency chain: it recomputes what it needs from the last materialised codes, reduces the
+// current stage's max (and replays the argmax in fp64), or emits codes.
+//
+// Data layout in HBM (workspace):
+//   c0  int8 [N][H][W][Cp]     input codes, channel-last so (tile, channel) threads coalesce
+//   V   int8 [36][T][Cp]       input-transform codes, GEMM A operand (K-major)
+//   U   int8 [36][Kp][Cp]      weight-transform codes, GEMM B operand (K-major, cached)
+//   h   int8|int16 [36][T][Kp] hadamard codes
+//   acc Acc [groups][9]        per-group stage maxima
+// T = N * TP tiles, TP = ceil(Ho/4)*ceil(Wo/4); element xi = 6*i + j of a 6x6 tile.
+#pragma once
+#include "wl_core.cuh"
+
+namespace wl {
+
+struct Geo {
+  int N, C, K, H, W, pad, Ho, Wo, th, tw, TP, T, Cp, Kp, ipg;
+};
+
+struct Bits {
+  int q[ST_COUNT];  // qmax per stage id
+};
+
+struct PlanF64 {  // fp64 left matrices (nearest doubles of the exact rationals, construct.py:191-208)
+  double wt[6 * 3], wbc[36], ibc[36], it[36], obc[36], ot[4 * 6];
+};
+
+__device__ __forceinline__ int group_of_image(int n, const Geo& g) { return n / g.ipg; }
+
+// ---------------------------------------------------------------------------------- input side
+
+// max|x| per group (cast "input", quantize.py:141).  x is NCHW fp32; grid.y = image.
+__global__ void absmax_f32_kernel(const float* __restrict__ x, long long per_image, int ipg, Acc* acc) {
+  const int n = blockIdx.y;
+  const float* xi = x + (size_t)n * per_image;
+  unsigned m = 0;
+  const bool vec = (per_image % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  if (vec) {
+    const float4* x4 = reinterpret_cast<const float4*>(xi);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_image / 4;
+         i += (long long)gridDim.x * blockDim.x) {
+      float4 v = __ldg(&x4[i]);
+      m = max(m, __float_as_uint(fabsf(v.x)));
+      m = max(m, __float_as_uint(fabsf(v.y)));
+      m = max(m, __float_as_uint(fabsf(v.z)));
+      m = max(m, __float_as_uint(fabsf(v.w)));
+    }
+  } else {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_image;
+         i += (long long)gridDim.x * blockDim.x)
+      m = max(m, __float_as_uint(fabsf(__ldg(&xi[i]))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ unsigned sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0 && m) atomicMax(&acc[(size_t)(n / ipg) * ST_COUNT + ST_INPUT].M, (unsigned long long)m);
+  }
+}
+
+// c0 = rint(x / s0) (quantize.py:118-119), NCHW fp32 -> NHWC int8 through a shared-memory transpose.
+// Block = (image n, row h, 32-channel slab).
+__global__ void quant_input_kernel(const float* __restrict__ x, int8_t* __restrict__ c0, Geo g, Bits b,
+                                   const Acc* __restrict__ acc) {
+  __shared__ int8_t tile[32][257];
+  const int n = blockIdx.z, h = blockIdx.y, c_base = blockIdx.x * 32;
+  const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
+  for (int w0 = 0; w0 < g.W; w0 += 256) {
+    const int wn = min(256, g.W - w0);
+    for (int e = threadIdx.x; e < 32 * wn; e += blockDim.x) {
+      const int cc = e / wn, w = e % wn;
+      const int c = c_base + cc;
+      int code = 0;
+      if (c < g.C) code = quant_float(__ldg(&x[(((size_t)n * g.C + c) * g.H + h) * g.W + w0 + w]), q);
+      tile[cc][w] = (int8_t)code;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * wn; e += blockDim.x) {
+      const int w = e / 32, cc = e % 32;
+      const int c = c_base + cc;
+      if (c < g.Cp) c0[(((size_t)n * g.H + h) * g.W + w0 + w) * g.Cp + c] = tile[cc][w];
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void load_input_tile(const int8_t* __restrict__ c0, const Geo& g, int n, int tile, int c,
+                                                int (&X)[6][6]) {
+  const int ty = tile / g.tw, tx = tile % g.tw;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const int r = 4 * ty + i - g.pad;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      const int col = 4 * tx + j - g.pad;
+      X[i][j] = (r >= 0 && r < g.H && col >= 0 && col < g.W)
+                    ? (int)__ldg(&c0[(((size_t)n * g.H + r) * g.W + col) * g.Cp + c])
+                    : 0;
+    }
+  }
+}
+
+template <typename TT>
+__device__ __forceinline__ long long absmax36(const TT (&T)[6][6]) {
+  long long m = 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      long long a = (long long)T[i][j];
+      a = a < 0 ? -a : a;
+      m = a > m ? a : m;
+    }
+  return m;
+}
+
+// Requantise a 6x6 int32 stage tensor into codes; exact ties are replayed from the stage's own
+// input codes `Xin` (dequantised with `qin`) through the fp64 matrix `Lf`.
+template <typename TT>
+__device__ __forceinline__ void requant36(const TT (&T)[6][6], const StageQ& q, const int (&Xin)[6][6],
+                                          const StageQ& qin, const double* __restrict__ Lf, int (&out)[6][6]) {
+  bool any_tie = false;
+  bool tie[6][6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      bool t = false;
+      out[i][j] = rq((long long)T[i][j], q, t);
+      tie[i][j] = t;
+      any_tie |= t;
+    }
+  if (any_tie) {
+    int xc[36];
+#pragma unroll
+    for (int e = 0; e < 36; ++e) xc[e] = Xin[e / 6][e % 6];
+    for (int e = 0; e < 36; ++e)
+      if (tie[e / 6][e % 6])
+        out[e / 6][e % 6] =
+            code_of(replay_sandwich(Lf, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6), q);
+  }
+}
+
+// Reduce one thread's 6x6 stage tensor into the group max; replay the local argmax in fp64.
+template <typename TT>
+__device__ __forceinline__ void reduce36(const TT (&T)[6][6], int grp, bool active, Acc* acc, int stage,
+                                         const int (&Xin)[6][6], const StageQ& qin, const double* __restrict__ Lf,
+                                         int R) {
+  const long long m = active ? absmax36(T) : 0;
+  bool uniform;
+  long long wmax;
+  Acc* a = acc + stage;
+  if (replay_gate(m, active ? grp : -1, a, ST_COUNT, uniform, wmax)) {
+    int xc[36];
+#pragma unroll
+    for (int e = 0; e < 36; ++e) xc[e] = Xin[e / 6][e % 6];
+    double f = 0.0;
+    for (int e = 0; e < R * R; ++e) {
+      long long v = (long long)T[e / R][e % R];
+      if ((v < 0 ? -v : v) == m) f = fmax(f, fabs(replay_sandwich(Lf, R, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / R, e % R)));
+    }
+    atomicMax(&a[(size_t)grp * ST_COUNT].F, dbits(f));
+  }
+  publish_max(m, active ? grp : -1, a, ST_COUNT, uniform, wmax);
+}
+
+// Pass over (tile, channel) threads, channel fastest.  MODE 0 canonical / 1 Legendre.
+//   PASS 0: first input stage max (canonical input_transform | Legendre input_base_change)
+//   PASS 1: Legendre only — input_transform max from requantised base-change codes
+//   PASS 2: emit V codes
+template <int MODE, int PASS>
+__global__ void __launch_bounds__(256) input_stage_kernel(const int8_t* __restrict__ c0, int8_t* __restrict__ V, Geo g,
+                                                          Bits b, Acc* __restrict__ acc,
+                                                          const PlanF64* __restrict__ pf) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long total = (long long)g.T * g.C;
+  const bool active = idx < total;
+  const long long id = active ? idx : 0;
+  const int c = (int)(id % g.C);
+  const int t = (int)(id / g.C);
+  const int n = t / g.TP, tile = t % g.TP;
+  const int grp = group_of_image(n, g);
+  Acc* ga = acc + (size_t)grp * ST_COUNT;
+  int X[6][6];
+  load_input_tile(c0, g, n, tile, c, X);
+  const StageQ q0 = load_float_stage(ga[ST_INPUT], b.q[ST_INPUT]);
+  if constexpr (MODE == 0) {
+    int T1[6][6];
+    sandwich<tab::Can_IT>(X, T1);
+    if constexpr (PASS == 0) {
+      reduce36(T1, grp, active, acc, ST_IT, X, q0, pf->it, 6);
+    } else {
+      const StageQ q1 = load_int_stage(ga[ST_IT], b.q[ST_IT]);
+      int C1[6][6];
+      requant36(T1, q1, X, q0, pf->it, C1);
+      if (active)
+#pragma unroll
+        for (int e = 0; e < 36; ++e) V[((size_t)e * g.T + t) * g.Cp + c] = (int8_t)C1[e / 6][e % 6];
+    }
+  } else {
+    int T1[6][6];
+    sandwich<tab::Leg_IBC>(X, T1);
+    if constexpr (PASS == 0) {
+      reduce36(T1, grp, active, acc, ST_IBC, X, q0, pf->ibc, 6);
+    } else {
+      const StageQ q1 = load_int_stage(ga[ST_IBC], b.q[ST_IBC]);
+      int C1[6][6];
+      requant36(T1, q1, X, q0, pf->ibc, C1);
+      long long T2[6][6];
+      sandwich<tab::Leg_IT>(C1, T2);
+      if constexpr (PASS == 1) {
+        reduce36(T2, grp, active, acc, ST_IT, C1, q1, pf->it, 6);
+      } else {
+        const StageQ q2 = load_int_stage(ga[ST_IT], b.q[ST_IT]);
+        int C2[6][6];
+        requant36(T2, q2, C1, q1, pf->it, C2);
+        if (active)
+#pragma unroll
+          for (int e = 0; e < 36; ++e) V[((size_t)e * g.T + t) * g.Cp + c] = (int8_t)C2[e / 6][e % 6];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------- weight side
+
+// Thread per (out channel k, in channel c), c fastest.  PASS 0: weight_transform max; PASS 1
+// (Legendre): weight_base_change max; PASS 2: emit U codes [36][Kp][Cp].
+template <int MODE, int PASS>
+__global__ void __launch_bounds__(256) weight_stage_kernel(const float* __restrict__ w, int K, int C, int Kp, int Cp,
+                                                           int8_t* __restrict__ U, Bits b, Acc* __restrict__ wacc,
+                                                           const PlanF64* __restrict__ pf) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = idx < K * C;
+  const int id = active ? idx : 0;
+  const int c = id % C, k = id / C;
+  const StageQ qw = load_float_stage(wacc[ST_WEIGHTS], b.q[ST_WEIGHTS]);
+  int X[3][3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) X[i / 3][i % 3] = quant_float(__ldg(&w[(size_t)id * 9 + i]), qw);
+  int xc[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) xc[i] = X[i / 3][i % 3];
+  int U1[6][6];
+  const double* Lwt = pf->wt;
+  if constexpr (MODE == 0)
+    sandwich<tab::Can_WT>(X, U1);
+  else
+    sandwich<tab::Leg_WT>(X, U1);
+  if constexpr (PASS == 0) {
+    const long long m = active ? absmax36(U1) : 0;
+    bool uniform;
+    long long wmax;
+    if (replay_gate(m, active ? 0 : -1, wacc + ST_WT, ST_COUNT, uniform, wmax)) {
+      double f = 0.0;
+      for (int e = 0; e < 36; ++e) {
+        long long v = U1[e / 6][e % 6];
+        if ((v < 0 ? -v : v) == m)
+          f = fmax(f, fabs(replay_sandwich(Lwt, 6, 3, xc, qw.qmax, qw.maxabs, qw.scale, e / 6, e % 6)));
+      }
+      atomicMax(&wacc[ST_WT].F, dbits(f));
+    }
+    publish_max(m, active ? 0 : -1, wacc + ST_WT, ST_COUNT, uniform, wmax);
+    return;
+  }
+  const StageQ q1 = load_int_stage(wacc[ST_WT], b.q[ST_WT]);
+  int C1[6][6];
+  {
+    bool tie[36];
+    bool any = false;
+#pragma unroll
+    for (int e = 0; e < 36; ++e) {
+      bool t = false;
+      C1[e / 6][e % 6] = rq(U1[e / 6][e % 6], q1, t);
+      tie[e] = t;
+      any |= t;
+    }
+    if (any)
+      for (int e = 0; e < 36; ++e)
+        if (tie[e])
+          C1[e / 6][e % 6] = code_of(replay_sandwich(Lwt, 6, 3, xc, qw.qmax, qw.maxabs, qw.scale, e / 6, e % 6), q1);
+  }
+  if constexpr (MODE == 0) {
+    if (active)
+#pragma unroll
+      for (int e = 0; e < 36; ++e) U[((size_t)e * Kp + k) * Cp + c] = (int8_t)C1[e / 6][e % 6];
+  } else {
+    int U2[6][6];
+    sandwich<tab::Leg_WBC>(C1, U2);
+    if constexpr (PASS == 1) {
+      reduce36(U2, 0, active, wacc, ST_WBC, C1, q1, pf->wbc, 6);
+    } else {
+      const StageQ q2 = load_int_stage(wacc[ST_WBC], b.q[ST_WBC]);
+      int C2[6][6];
+      requant36(U2, q2, C1, q1, pf->wbc, C2);
+      if (active)
+#pragma unroll
+        for (int e = 0; e < 36; ++e) U[((size_t)e * Kp + k) * Cp + c] = (int8_t)C2[e / 6][e % 6];
+    }
+  }
+}
+
+__global__ void absmax_weights_kernel(const float* __restrict__ w, long long n, Acc* wacc) {
+  unsigned m = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(__ldg(&w[i]))));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(&wacc[ST_WEIGHTS].M, (unsigned long long)m);
+}
+
+// ---------------------------------------------------------------------------------- output side
+
+template <typename HT>
+__device__ __forceinline__ void load_h(const HT* __restrict__ h, const Geo& g, int t, int k, int (&X)[6][6]) {
+#pragma unroll
+  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = (int)h[((size_t)e * g.T + t) * g.Kp + k];
+}
+
+// 4x4 output tile, crop-aware reduction (pipeline.py:156-158: crop before the final cast).
+template <typename TT>
+__device__ __forceinline__ long long absmax_crop(const TT (&Y)[4][4], int ty, int tx, const Geo& g) {
+  long long m = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) {
+        long long a = (long long)Y[i][j];
+        a = a < 0 ? -a : a;
+        m = a > m ? a : m;
+      }
+    }
+  return m;
+}
+
+// Thread per (tile, out channel), channel fastest.
+//   canonical PASS 0: output max over Y = A^T h A (cropped); PASS 2: write y
+//   legendre  PASS 0: output_base_change max; PASS 1: output max; PASS 2: write y
+template <int MODE, int PASS, typename HT>
+__global__ void __launch_bounds__(256) output_stage_kernel(const HT* __restrict__ h, float* __restrict__ y,
+                                                           const float* __restrict__ bias, Geo g, Bits b,
+                                                           Acc* __restrict__ acc, const PlanF64* __restrict__ pf) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool active = idx < (long long)g.T * g.K;
+  const long long id = active ? idx : 0;
+  const int k = (int)(id % g.K);
+  const int t = (int)(id / g.K);
+  const int n = t / g.TP, tile = t % g.TP;
+  const int ty = tile / g.tw, tx = tile % g.tw;
+  const int grp = group_of_image(n, g);
+  Acc* ga = acc + (size_t)grp * ST_COUNT;
+  int H0[6][6];
+  load_h(h, g, t, k, H0);
+  const StageQ qh = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
+  int Cf[6][6];  // codes feeding the final A-transform
+  StageQ qf;
+  const double* Lot = pf->ot;
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int e = 0; e < 36; ++e) Cf[e / 6][e % 6] = H0[e / 6][e % 6];
+    qf = qh;
+  } else {
+    int T4[6][6];
+    sandwich<tab::Leg_OBC>(H0, T4);
+    if constexpr (PASS == 0) {
+      reduce36(T4, grp, active, acc, ST_OBC, H0, qh, pf->obc, 6);
+      return;
+    } else {
+      qf = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
+      requant36(T4, qf, H0, qh, pf->obc, Cf);
+    }
+  }
+  if constexpr (MODE == 1 && PASS == 0) return;
+  long long Y[4][4];
+  if constexpr (MODE == 0) {
+    int Yi[4][4];
+    sandwich<tab::Can_OT>(Cf, Yi);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) Y[e / 4][e % 4] = Yi[e / 4][e % 4];
+  } else {
+    sandwich<tab::Leg_OT>(Cf, Y);
+  }
+  constexpr bool kReduce = (MODE == 0 && PASS == 0) || (MODE == 1 && PASS == 1);
+  if constexpr (kReduce) {
+    const long long m = active ? absmax_crop(Y, ty, tx, g) : 0;
+    bool uniform;
+    long long wmax;
+    Acc* a = acc + ST_OUT;
+    if (replay_gate(m, active ? grp : -1, a, ST_COUNT, uniform, wmax)) {
+      int xc[36];
+#pragma unroll
+      for (int e = 0; e < 36; ++e) xc[e] = Cf[e / 6][e % 6];
+      double f = 0.0;
+      for (int e = 0; e < 16; ++e) {
+        const int i = e / 4, j = e % 4;
+        if (4 * ty + i >= g.Ho || 4 * tx + j >= g.Wo) continue;
+        long long v = Y[i][j];
+        if ((v < 0 ? -v : v) == m) f = fmax(f, fabs(replay_sandwich(Lot, 4, 6, xc, qf.qmax, qf.maxabs, qf.scale, i, j)));
+      }
+      atomicMax(&a[(size_t)grp * ST_COUNT].F, dbits(f));
+    }
+    publish_max(m, active ? grp : -1, a, ST_COUNT, uniform, wmax);
+  } else {
+    if (!active) return;
+    const StageQ qo = load_int_stage(ga[ST_OUT], b.q[ST_OUT]);
+    const float bk = bias ? __ldg(&bias[k]) : 0.f;
+    int xc[36];
+    bool have_xc = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = 4 * ty + i;
+      if (r >= g.Ho) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = 4 * tx + j;
+        if (col >= g.Wo) continue;
+        bool tie = false;
+        int code = rq(Y[i][j], qo, tie);
+        if (tie) {
+          if (!have_xc) {
+            for (int e = 0; e < 36; ++e) xc[e] = Cf[e / 6][e % 6];
+            have_xc = true;
+          }
+          code = code_of(replay_sandwich(Lot, 4, 6, xc, qf.qmax, qf.maxabs, qf.scale, i, j), qo);
+        }
+        const double v = deq(code, qo.qmax, qo.maxabs, qo.scale);
+        float out = (float)v;
+        if (bias) out += bk;
+        y[(((size_t)n * g.K + k) * g.Ho + r) * g.Wo + col] = out;
+      }
+    }
+  }
+}
+
+}  // namespace wl

@@ -1,0 +1,269 @@
+"""The quantized Winograd F(4x4,3x3) layer on B200: reference-shaped API over the C ABI.
+
+Drop-in for the reference entry point ``conv2d_winograd_quantized(x, w, plan, mode, qconfig)``
+(quantize.py:129-148), extended with a batch dimension, zero padding and bias:
+
+    y, stats = conv2d_winograd_quantized(x, w, plan, mode, qconfig, padding=0, bias=None,
+                                         scale_groups="image")
+
+* ``x`` [c_in,H,W] (reference shape) or [N,c_in,H,W]; torch CUDA tensor, or a numpy array (copied
+  to the current CUDA device; the result is then returned as float64 numpy like the reference).
+* ``scale_groups="image"``: every image gets its own stage scales, i.e. the batched call equals N
+  independent reference calls (bit-exact contract, tests/test_gpu_parity.py).  ``"batch"``: one
+  scale per stage over the whole batch (one cast over the [N,...] tensor).
+* ``stats``: list[StageStat] in reference order when there is one scale group, else a list of
+  such lists (one per group).
+* errors: DimensionError for shapes (reference.py:16-31), ValueError for mode / plan / widths
+  (pipeline.py:36-40, quantize.py:29-33, 52-55).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DimensionError
+from .plan import WinogradPlan, build_plan, stage_matrices
+from .quantize import STAGE_ORDER, QuantConfig, StageStat
+
+BASE_MODES = ("canonical", "legendre")
+_STAGE_NAMES = {"canonical": ("wt", "it", "ot"), "legendre": ("wt", "wbc", "ibc", "it", "obc", "ot")}
+
+
+def _require_mode(plan: WinogradPlan, mode: str) -> None:
+    if mode not in BASE_MODES:
+        raise ValueError(f"unknown base mode {mode!r}, expected one of {BASE_MODES}")
+    if mode == "legendre" and plan.base_change is None:
+        raise ValueError("legendre mode needs a plan built with use_legendre=True")
+
+
+class DevicePlan:
+    """wl_plan handle for (plan, mode, device); owns the device copy of the fp64 matrices."""
+
+    _cache: dict = {}
+    _lock = threading.Lock()
+
+    def __init__(self, plan: WinogradPlan, mode: str, device: torch.device):
+        _require_mode(plan, mode)
+        if not plan.is_exact:
+            raise ValueError("the B200 layer needs the exact plan from build_plan (not plan_to_float)")
+        if (plan.o, plan.k) != (4, 3):
+            raise ValueError(f"only F(4,3) is compiled for sm_100a, got F({plan.o},{plan.k})")
+        sm = stage_matrices(plan, mode)
+        names = _STAGE_NAMES[mode]
+        ints = np.ascontiguousarray(np.concatenate([sm[n].L_int.ravel() for n in names]), dtype=np.int64)
+        f64 = np.ascontiguousarray(np.concatenate([sm[n].L_f64.ravel() for n in names]), dtype=np.float64)
+        self.mode = mode
+        self.device = device
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _lib.check(_lib.lib().wl_plan_create(
+                4, 3, _lib.WL_LEGENDRE if mode == "legendre" else _lib.WL_CANONICAL,
+                ints.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                f64.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(handle)), "wl_plan_create")
+        self.handle = handle
+
+    @classmethod
+    def get(cls, plan: WinogradPlan, mode: str, device: torch.device) -> "DevicePlan":
+        key = (id(plan), mode, device.index)
+        with cls._lock:
+            dp = cls._cache.get(key)
+            if dp is None or dp._plan_ref is not plan:
+                dp = cls(plan, mode, device)
+                dp._plan_ref = plan
+                cls._cache[key] = dp
+            return dp
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                _lib.lib().wl_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def qcfg_struct(q: QuantConfig) -> _lib.wl_qcfg:
+    return _lib.wl_qcfg(*q.as_tuple())
+
+
+def _stream_ptr() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class WeightCache:
+    """Cached weight side (U codes + weight-stage stats), recomputed when the weight changes."""
+
+    def __init__(self):
+        self.key = None
+        self.buf = None
+
+    def get(self, dplan: DevicePlan, q: QuantConfig, w: torch.Tensor) -> torch.Tensor:
+        key = (id(dplan), q, w.data_ptr(), w._version, tuple(w.shape), w.device.index)
+        if self.key == key and self.buf is not None:
+            return self.buf
+        cout, cin = int(w.shape[0]), int(w.shape[1])
+        nbytes = ctypes.c_size_t()
+        _lib.check(_lib.lib().wl_weight_cache_size(dplan.handle, cout, cin, ctypes.byref(nbytes)),
+                   "wl_weight_cache_size")
+        if self.buf is None or self.buf.numel() < nbytes.value or self.buf.device != w.device:
+            self.buf = torch.empty(nbytes.value, dtype=torch.uint8, device=w.device)
+        qs = qcfg_struct(q)
+        _lib.check(_lib.lib().wl_weight_transform(
+            dplan.handle, ctypes.byref(qs), ctypes.c_void_p(w.data_ptr()), cout, cin,
+            ctypes.c_void_p(self.buf.data_ptr()), nbytes.value, _stream_ptr()), "wl_weight_transform")
+        self.key = key
+        return self.buf
+
+
+def _check_conv_args(x: torch.Tensor, w: torch.Tensor) -> None:
+    # reference.py:16-31 with a batch dimension
+    if x.dim() != 4:
+        raise DimensionError(f"input must be [N, c_in, H, W], got shape {tuple(x.shape)}")
+    if w.dim() != 4:
+        raise DimensionError(f"weights must be [c_out, c_in, k, k], got shape {tuple(w.shape)}")
+    c_out, c_in, k, k2 = w.shape
+    if k != k2:
+        raise DimensionError(f"kernel must be square, got {k}x{k2}")
+    if x.shape[1] != c_in:
+        raise DimensionError(f"channel mismatch: input has {x.shape[1]}, weights expect {c_in}")
+
+
+class QuantWinogradConv:
+    """Reusable forward runner: owns the device plan, the weight cache and the workspace."""
+
+    def __init__(self, plan: WinogradPlan, mode: str, qconfig: QuantConfig, device=None):
+        _require_mode(plan, mode)
+        self.plan, self.mode, self.qconfig = plan, mode, qconfig
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.dplan = DevicePlan.get(plan, mode, self.device)
+        self.wcache = WeightCache()
+        self.ws = None
+        self._last = None
+
+    def _shape(self, x, w, padding, groups):
+        n, cin, h, wd = (int(v) for v in x.shape)
+        if groups == "image":
+            ipg = 1
+        elif groups == "batch":
+            ipg = n
+        else:
+            raise ValueError(f"scale_groups must be 'image' or 'batch', got {groups!r}")
+        return _lib.wl_shape(n, cin, int(w.shape[0]), h, wd, int(padding), ipg)
+
+    def workspace_bytes(self, shape) -> int:
+        nbytes = ctypes.c_size_t()
+        qs = qcfg_struct(self.qconfig)
+        _lib.check(_lib.lib().wl_workspace_size(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs),
+                                                 ctypes.byref(nbytes)), "wl_workspace_size")
+        return nbytes.value
+
+    def forward(self, x: torch.Tensor, w: torch.Tensor, bias=None, padding: int = 0, scale_groups="image",
+                out: torch.Tensor | None = None) -> torch.Tensor:
+        _check_conv_args(x, w)
+        if w.shape[2] != 3:
+            raise DimensionError(f"plan is for k=3, weights have k={w.shape[2]}")
+        if not (x.is_cuda and w.is_cuda):
+            raise ValueError("x and w must be CUDA tensors")
+        x = x.contiguous().float()
+        w = w.contiguous().float()
+        shape = self._shape(x, w, padding, scale_groups)
+        ho, wo = shape.h + 2 * shape.pad - 2, shape.w + 2 * shape.pad - 2
+        if ho < 1 or wo < 1:
+            raise DimensionError(f"input {shape.h}x{shape.w} (pad {shape.pad}) is smaller than the 3x3 kernel")
+        cache = self.wcache.get(self.dplan, self.qconfig, w)
+        nbytes = self.workspace_bytes(shape)
+        if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
+            self.ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+        if out is None:
+            out = torch.empty((shape.n, shape.c_out, ho, wo), dtype=torch.float32, device=x.device)
+        if bias is not None:
+            bias = bias.contiguous().float()
+            if bias.shape != (shape.c_out,):
+                raise DimensionError(f"bias must be [{shape.c_out}], got {tuple(bias.shape)}")
+        qs = qcfg_struct(self.qconfig)
+        _lib.check(_lib.lib().wl_forward(
+            self.dplan.handle, ctypes.byref(qs), ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()),
+            ctypes.c_void_p(cache.data_ptr()), ctypes.c_void_p(bias.data_ptr() if bias is not None else 0),
+            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+            _stream_ptr()), "wl_forward")
+        self._last = (shape, cache)
+        return out
+
+    def stats(self):
+        """StageStat rows of the last forward (synchronises the stream)."""
+        shape, cache = self._last
+        ns = _lib.lib().wl_num_stages(self.dplan.handle)
+        groups = shape.n // shape.images_per_group
+        arr = (_lib.wl_stage_stat * (groups * ns))()
+        qs = qcfg_struct(self.qconfig)
+        _lib.check(_lib.lib().wl_read_stats(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs),
+                                            ctypes.c_void_p(cache.data_ptr()),
+                                            ctypes.c_void_p(self.ws.data_ptr()), arr, _stream_ptr()),
+                   "wl_read_stats")
+        names = STAGE_ORDER[self.mode]
+        return [[StageStat(names[i], arr[g * ns + i].bits, arr[g * ns + i].max_abs, arr[g * ns + i].scale)
+                 for i in range(ns)] for g in range(groups)]
+
+    def launches(self) -> int:
+        shape, _ = self._last
+        qs = qcfg_struct(self.qconfig)
+        return int(_lib.lib().wl_forward_launches(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs)))
+
+    def debug_views(self):
+        """Views of the materialised codes of the last call: c0 [N,H,W,Cp], V [36,T,Cp], h [36,T,Kp]."""
+        shape, cache = self._last
+        off = (ctypes.c_size_t * 4)()
+        dims = (ctypes.c_int * 4)()
+        qs = qcfg_struct(self.qconfig)
+        _lib.check(_lib.lib().wl_debug_layout(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs), off, dims),
+                   "wl_debug_layout")
+        Cp, Kp, T, _ = dims[0], dims[1], dims[2], dims[3]
+        ws = self.ws
+        c0 = ws[off[0]: off[0] + shape.n * shape.h * shape.w * Cp].view(torch.int8).view(shape.n, shape.h, shape.w, Cp)
+        V = ws[off[1]: off[1] + 36 * T * Cp].view(torch.int8).view(36, T, Cp)
+        hb = 2 if self.qconfig.hadamard_bits > 8 else 1
+        hraw = ws[off[2]: off[2] + 36 * T * Kp * hb]
+        h = (hraw.view(torch.int16) if hb == 2 else hraw.view(torch.int8)).view(36, T, Kp)
+        cin, cout = shape.c_in, shape.c_out
+        ucodes = cache[cache.numel() - 36 * Kp * Cp:].view(torch.int8).view(36, Kp, Cp)
+        return {"c0": c0[..., :cin], "V": V[..., :cin], "h": h[..., :cout], "U": ucodes[:, :cout, :cin]}
+
+
+_runners: dict = {}
+
+
+def conv2d_winograd_quantized(x, w, plan: WinogradPlan, mode: str, qconfig: QuantConfig, padding: int = 0,
+                              bias=None, scale_groups: str = "image"):
+    """Reference-compatible entry point (quantize.py:129-148) running on the GPU."""
+    _require_mode(plan, mode)
+    as_numpy = isinstance(x, np.ndarray) or isinstance(w, np.ndarray)
+    if as_numpy:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        x = torch.as_tensor(np.asarray(x, dtype=np.float32), device=dev)
+        w = torch.as_tensor(np.asarray(w, dtype=np.float32), device=dev)
+        if bias is not None:
+            bias = torch.as_tensor(np.asarray(bias, dtype=np.float32), device=dev)
+    single = x.dim() == 3
+    if single:
+        x = x.unsqueeze(0)
+    key = (id(plan), mode, qconfig, x.device.index)
+    r = _runners.get(key)
+    if r is None or r.plan is not plan:
+        r = QuantWinogradConv(plan, mode, qconfig, x.device)
+        _runners[key] = r
+    y = r.forward(x, w, bias=bias, padding=padding, scale_groups=scale_groups)
+    st = r.stats()
+    stats = st[0] if len(st) == 1 else st
+    if single:
+        y = y[0]
+    if as_numpy:
+        y = y.double().cpu().numpy()
+    return y, stats
+
+
+def default_plan(use_legendre: bool = True) -> WinogradPlan:
+    return build_plan(4, 3, use_legendre=use_legendre)

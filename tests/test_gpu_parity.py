@@ -1,0 +1,195 @@
+"""GPU parity: the sm_100a layer (through the C ABI) against the reference's golden fixtures and the
+pinned CPU oracle.  Contract: integer codes of every materialised stage and the StageStat rows are
+bit-exact; the fp32 output equals the reference's fp64 output rounded to fp32 (bias = 0)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_case
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2004_11077_b200 as W  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+PLAN = W.build_plan(4, 3, use_legendre=True)
+
+
+def qc_from_bits(bits):
+    return W.QuantConfig(**bits)
+
+
+def run_gpu(x, w, mode, qc, pad, groups="image", bias=None):
+    r = W.QuantWinogradConv(PLAN, mode, qc)
+    xt = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32), device="cuda")
+    wt = torch.as_tensor(np.ascontiguousarray(w, dtype=np.float32), device="cuda")
+    bt = None if bias is None else torch.as_tensor(bias, dtype=torch.float32, device="cuda")
+    y = r.forward(xt, wt, bias=bt, padding=pad, scale_groups=groups)
+    torch.cuda.synchronize()
+    return r, y
+
+
+def stats_tuples(stats):
+    return [(s.stage, s.bits, s.max_abs, s.scale) for s in stats]
+
+
+@pytest.mark.parametrize("path", golden_cases(), ids=lambda p: os.path.basename(p)[5:-4])
+def test_golden_case_bit_exact(path):
+    c = load_case(path)
+    meta = c["meta"]
+    qc = qc_from_bits(meta["bits"])
+    pad = meta["pad"]
+    x = c["x"][None]
+    r, y = run_gpu(x, c["w"], meta["mode"], qc, pad)
+    st = r.stats()[0]
+    want = list(zip(meta["stages"], c["stat_bits"].tolist(), c["stat_max_abs"].tolist(), c["stat_scale"].tolist()))
+    assert stats_tuples(st) == want
+    assert np.array_equal(y[0].cpu().numpy(), c["y"].astype(np.float32))
+    v = r.debug_views()
+    cin, cout = c["w"].shape[1], c["w"].shape[0]
+    H, Wd = c["x"].shape[1:]
+    ci = c["codes_input"]
+    if pad:
+        ci = ci[:, pad:pad + H, pad:pad + Wd]
+    assert np.array_equal(v["c0"][0].permute(2, 0, 1).cpu().numpy(), ci)
+    T = v["V"].shape[1]
+    vt = c["codes_input_transform"].reshape(cin, T, 36)
+    assert np.array_equal(v["V"].permute(2, 1, 0).cpu().numpy(), vt)
+    ht = c["codes_hadamard"].reshape(cout, T, 36)
+    assert np.array_equal(v["h"].permute(2, 1, 0).cpu().numpy().astype(np.int32), ht.astype(np.int32))
+    wkey = "codes_weight_base_change" if meta["mode"] == "legendre" else "codes_weight_transform"
+    if wkey in c:
+        assert np.array_equal(v["U"].permute(1, 2, 0).cpu().numpy(), c[wkey].reshape(cout, cin, 36))
+
+
+def _kaiming(rng, cout, cin):
+    return (rng.standard_normal((cout, cin, 3, 3)) * np.sqrt(2.0 / (9 * cin))).astype(np.float32)
+
+
+def _compare_with_oracle(x, w, mode, qc, pad, groups, sample=None):
+    r, y = run_gpu(x, w, mode, qc, pad, groups)
+    n = x.shape[0]
+    idx = np.arange(n) if sample is None else np.asarray(sample)
+    ipg = 1 if groups == "image" else n
+    xs = x[idx] if groups == "image" else x
+    yo, so, _ = O.quant_conv_batch(xs.astype(np.float64), w.astype(np.float64), mode,
+                                   {f: getattr(qc, f) for f in O.BIT_FIELDS}, padding=pad,
+                                   images_per_group=ipg)
+    yg = y.cpu().numpy()
+    yg = yg[idx] if groups == "image" else yg
+    assert np.array_equal(yg, yo.astype(np.float32))
+    st = r.stats()
+    if groups == "image":
+        for j, i in enumerate(idx):
+            assert stats_tuples(st[i]) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[j]]
+    else:
+        assert stats_tuples(st[0]) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[0]]
+    return r, y
+
+
+def test_config1_full_batch_both_granularities():
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((8, 64, 32, 32)).astype(np.float32)
+    w = _kaiming(rng, 64, 64)
+    for groups in ("image", "batch"):
+        _compare_with_oracle(x, w, "legendre", W.QuantConfig.uniform(8), 1, groups)
+
+
+@pytest.mark.parametrize("mode", ["legendre", "canonical"])
+@pytest.mark.parametrize("qname", ["8b", "8b+9b"])
+def test_config2(mode, qname):
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((128, 128, 16, 16)).astype(np.float32)
+    w = _kaiming(rng, 128, 128)
+    _compare_with_oracle(x, w, mode, W.QuantConfig.from_name(qname), 1, "image", sample=range(0, 128, 9))
+
+
+@pytest.mark.parametrize("c,hw", [(64, 32), (128, 16), (256, 8), (512, 4)])
+def test_config3_shapes(c, hw):
+    rng = np.random.default_rng(3)
+    x = np.maximum(rng.standard_normal((256, c, hw, hw)), 0).astype(np.float32)
+    w = _kaiming(rng, c, c)
+    _compare_with_oracle(x, w, "legendre", W.QuantConfig.uniform(8), 1, "image", sample=[0, 1, 77, 255])
+
+
+def test_config4_sampled_images():
+    rng = np.random.default_rng(0)
+    n = 64  # full config-4 shape per image; per-image scales make sampled parity exact
+    x = rng.standard_normal((n, 256, 56, 56)).astype(np.float32)
+    w = _kaiming(rng, 256, 256)
+    _compare_with_oracle(x, w, "legendre", W.QuantConfig.uniform(8), 1, "image", sample=[0, 31, 63])
+
+
+@pytest.mark.parametrize("cin,cout,h,w,pad", [(3, 64, 32, 32, 1), (5, 10, 13, 14, 0), (33, 70, 9, 7, 1),
+                                               (96, 200, 6, 11, 1), (1, 1, 3, 3, 0)])
+@pytest.mark.parametrize("mode", ["legendre", "canonical"])
+def test_ragged_shapes(cin, cout, h, w, pad, mode):
+    rng = np.random.default_rng(cin * 131 + cout)
+    x = rng.standard_normal((3, cin, h, w)).astype(np.float32)
+    wt = rng.standard_normal((cout, cin, 3, 3)).astype(np.float32)
+    _compare_with_oracle(x, wt, mode, W.QuantConfig.uniform(8, hadamard_bits=9), pad, "image")
+    _compare_with_oracle(x, wt, mode, W.QuantConfig.uniform(8), pad, "batch")
+
+
+def test_degenerate_inputs_ties_and_equal_maxima():
+    rng = np.random.default_rng(5)
+    cases = [np.zeros((2, 8, 8, 8)), np.ones((2, 8, 8, 8)), rng.integers(-2, 3, (2, 8, 8, 8)),
+             np.broadcast_to(rng.standard_normal((1, 8, 1, 1)), (2, 8, 8, 8))]
+    w = rng.integers(-1, 2, (16, 8, 3, 3)).astype(np.float32)
+    for x in cases:
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        for mode in ("canonical", "legendre"):
+            _compare_with_oracle(x, w, mode, W.QuantConfig.uniform(8), 1, "image")
+
+
+def test_bias_added_after_dequant():
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((2, 16, 12, 12)).astype(np.float32)
+    w = _kaiming(rng, 24, 16)
+    b = rng.standard_normal(24).astype(np.float32)
+    _, y0 = run_gpu(x, w, "legendre", W.QuantConfig.uniform(8), 1)
+    _, y1 = run_gpu(x, w, "legendre", W.QuantConfig.uniform(8), 1, bias=b)
+    assert torch.equal(y1, y0 + torch.as_tensor(b, device="cuda")[None, :, None, None])
+
+
+def test_reference_shaped_numpy_call():
+    c = load_case(golden_cases()[0])
+    meta = c["meta"]
+    x = c["x"].astype(np.float64)
+    if meta["pad"]:
+        x = np.pad(x, ((0, 0), (1, 1), (1, 1)))
+    y, st = W.conv2d_winograd_quantized(x, c["w"].astype(np.float64), PLAN, meta["mode"],
+                                        W.QuantConfig(**meta["bits"]))
+    assert y.dtype == np.float64 and y.shape == c["y"].shape
+    assert np.array_equal(y, c["y"].astype(np.float32).astype(np.float64))
+    assert [s.stage for s in st] == meta["stages"]
+
+
+def test_determinism_bit_identical():
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((4, 32, 20, 20)).astype(np.float32)
+    w = _kaiming(rng, 48, 32)
+    for mode in ("canonical", "legendre"):
+        _, a = run_gpu(x, w, mode, W.QuantConfig.uniform(8, hadamard_bits=9), 1)
+        _, b = run_gpu(x, w, mode, W.QuantConfig.uniform(8, hadamard_bits=9), 1)
+        assert torch.equal(a, b)
+
+
+def test_identity_free_errors():
+    r = W.QuantWinogradConv(PLAN, "legendre", W.QuantConfig.uniform(8))
+    x = torch.zeros((1, 4, 8, 8), device="cuda")
+    with pytest.raises(W.DimensionError):
+        r.forward(x, torch.zeros((2, 3, 3, 3), device="cuda"))
+    with pytest.raises(W.DimensionError):
+        r.forward(x[0], torch.zeros((2, 4, 3, 3), device="cuda"))
+    with pytest.raises(ValueError):
+        W.QuantWinogradConv(PLAN, "legendre", W.QuantConfig.uniform(10)).forward(
+            x, torch.zeros((2, 4, 3, 3), device="cuda"))
+    with pytest.raises(ValueError):
+        W.QuantWinogradConv(W.build_plan(4, 3), "legendre", W.QuantConfig.uniform(8))
