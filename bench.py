@@ -1,0 +1,353 @@
+"""Benchmark of the B200 quantized Legendre-Winograd F(4,3) layer (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3], the largest single-GPU configuration): per GPU N=1024 images,
+Cin=Cout=256, 56x56, pad 1, 8-bit Legendre F(4,3) forward, x ~ N(0,1) fp32, Kaiming-normal weights,
+bias 0, no collective.  Stage scales are per image ("image" groups: every image is quantized exactly
+as one reference call on that image).  A step is one forward over the 1024 images; the weight
+transform is cached (computed once before timing, as the north star's "amortised" weight kernel).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line on rank 0 (see README/DESIGN for every key).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "quantized Legendre-Winograd F(4,3) conv: effective TOPS & images/s"
+CFG = dict(n=1024, c=256, hw=56, pad=1, mode="legendre", qconfig="8b")
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def layer_units(n, c, k, hw, pad):
+    ho = hw + 2 * pad - 2
+    T = n * (-(-ho // 4)) ** 2
+    bytes_ = 4 * n * c * hw * hw + 4 * n * k * ho * ho + 36 * c * k + 4 * k
+    i8ops = 2 * 36 * T * c * k
+    eff_ops = 2 * 9 * n * ho * ho * c * k
+    return bytes_, i8ops, eff_ops, T
+
+
+def kernel_units(name, n, c, k, hw, pad, hbytes=1):
+    """Algorithmic (compulsory) bytes and int8 ops of one launch of each forward kernel."""
+    ho = hw + 2 * pad - 2
+    T = n * (-(-ho // 4)) ** 2
+    cp, kp = -(-c // 32) * 32, (64 if k <= 64 else 128 if k <= 128 else -(-k // 256) * 256)
+    x, c0, V, U, h, y = 4 * n * c * hw * hw, n * hw * hw * cp, 36 * T * cp, 36 * kp * cp, 36 * T * kp * hbytes, 4 * n * k * ho * ho
+    table = {
+        "absmax_input": (x, 0), "quant_input": (x + c0, 0),
+        "input_base_change_max": (c0, 0), "input_transform_max": (c0, 0), "input_transform_codes": (c0 + V, 0),
+        "gemm_hadamard_max": (V + U, 2 * 36 * T * cp * kp), "gemm_hadamard_codes": (V + U + h, 2 * 36 * T * cp * kp),
+        "output_base_change_max": (h, 0), "output_max": (h, 0), "output_write": (h + y, 0),
+    }
+    return table.get(name, (0, 0))
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index, self.proc, self.path = index, None, None
+
+    def start(self):
+        try:
+            self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_baseline(seconds_target=12.0, mode="legendre"):
+    """The CPU port of the reference path (oracle/, bit-identical to the reference's numba backend),
+    on all host threads, per-image calls on a bounded sample of config-4 images."""
+    from oracle import oracle as O
+
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    rng = np.random.default_rng(0)
+    k = CFG["c"]
+    w = (rng.standard_normal((k, k, 3, 3)) * np.sqrt(2.0 / (9 * k))).astype(np.float32).astype(np.float64)
+    x1 = rng.standard_normal((threads, CFG["c"], CFG["hw"], CFG["hw"])).astype(np.float32).astype(np.float64)
+    bits = O.uniform_bits(8)
+    O.quant_conv_batch(x1[:1, :, :8, :8], w, mode, bits, padding=1, nthreads=1)  # load / warm
+    t0 = time.perf_counter()
+    O.quant_conv_batch(x1, w, mode, bits, padding=1, images_per_group=1, nthreads=threads)
+    dt = time.perf_counter() - t0
+    reps = max(1, int(seconds_target / max(dt, 1e-3)))
+    times = [dt]
+    for _ in range(min(reps, 5) - 1):
+        t0 = time.perf_counter()
+        O.quant_conv_batch(x1, w, mode, bits, padding=1, images_per_group=1, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": threads / best, "unit": "images/s", "cores": threads, "kind": "port",
+            "sample": f"{threads} config-4 images (256ch 56x56 pad1, Legendre 8b, per-image calls), "
+                      f"best of {len(times)} runs, oracle/winoleg_oracle.c fp64 port of the reference path"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (C port, bit-identical to the numba backend) on the
+    host cores; rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    rng = np.random.default_rng(0)
+    k = CFG["c"]
+    w = (rng.standard_normal((k, k, 3, 3)) * np.sqrt(2.0 / (9 * k))).astype(np.float32).astype(np.float64)
+    x = rng.standard_normal((threads, CFG["c"], CFG["hw"], CFG["hw"])).astype(np.float32).astype(np.float64)
+    bits = O.uniform_bits(8)
+    for _ in range(args.warmup):
+        O.quant_conv_batch(x, w, CFG["mode"], bits, padding=1, images_per_group=1, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.quant_conv_batch(x, w, CFG["mode"], bits, padding=1, images_per_group=1, nthreads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    _, _, eff, _ = layer_units(threads, CFG["c"], CFG["c"], CFG["hw"], CFG["pad"])
+    val = threads / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config4: N=1024/GPU Cin=Cout=256 56x56 pad1 Legendre 8b fwd (sampled)",
+                   "sample_images_per_step": threads, "scale_groups": "image"},
+        "effective_tops": eff / dt / 1e12,
+        "cpu_baseline": {"value": val, "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{threads} images per step (one per host thread), per-image reference calls"},
+        "e2e": {"value": val, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def measure_int8_peak(torch):
+    try:
+        a = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+        b = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e9
+        for _ in range(5):
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2004_11077_b200 as W
+    from paper_2004_11077_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n, c, hw, pad = CFG["n"], CFG["c"], CFG["hw"], CFG["pad"]
+    k = c
+    qc = W.QuantConfig.from_name(CFG["qconfig"])
+    plan = W.build_plan(4, 3, use_legendre=True)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    x = torch.randn((n, c, hw, hw), generator=gen, device=dev, dtype=torch.float32)
+    gw = torch.Generator(device=dev)
+    gw.manual_seed(0)
+    w = torch.randn((k, c, 3, 3), generator=gw, device=dev) * float(np.sqrt(2.0 / (9 * c)))
+    y = torch.empty((n, k, hw + 2 * pad - 2, hw + 2 * pad - 2), device=dev)
+    r = W.QuantWinogradConv(plan, CFG["mode"], qc, dev)
+    r.forward(x, w, padding=pad, out=y)  # builds the weight cache + workspace
+    torch.cuda.synchronize()
+    launches = r.launches()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        r.forward(x, w, padding=pad, out=y)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local_rank)
+    if rank == 0:
+        clocks.start()
+    _lib.profile_enable(True)
+    _lib.profile_read()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        r.forward(x, w, padding=pad, out=y)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    kern, calls = _lib.profile_read()
+    _lib.profile_enable(False)
+    clk = clocks.stop() if rank == 0 else None
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # end to end through the public API with host buffers: pinned x -> device, forward, y -> pinned host
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        yh = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+        xd = torch.empty_like(x)
+        for _ in range(1):
+            xd.copy_(xh, non_blocking=True)
+            r.forward(xd, w, padding=pad, out=y)
+            yh.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        ke = max(1, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(ke):
+            xd.copy_(xh, non_blocking=True)
+            r.forward(xd, w, padding=pad, out=y)
+            yh.copy_(y, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        me = e0.elapsed_time(e1) / ke
+        if world > 1:
+            t = torch.tensor([me], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            me = float(t.item())
+        e2e = {"value": world * n / (me * 1e-3), "unit": "images/s",
+               "h2d_bytes_per_step": int(x.numel() * 4), "d2h_bytes_per_step": int(y.numel() * 4),
+               "ms_per_step": me, "path": "QuantWinogradConv.forward (C ABI wl_forward) with pinned host x/y"}
+        del xh, yh, xd
+
+    if rank != 0:
+        return
+    hbm, bf16, peak_kind = _peaks()
+    i8_peak = measure_int8_peak(torch)
+    bytes_, i8ops, eff, T = layer_units(n, c, k, hw, pad)
+    t_roof = max(bytes_ / (hbm * 1e9), i8ops / ((i8_peak or 2 * bf16) * 1e12))
+    per_kernel = {name: v / max(calls, 1) for name, v in kern.items()}
+    dom = max(per_kernel, key=per_kernel.get)
+    kb, kops = kernel_units(dom, n, c, k, hw, pad)
+    dom_ms = per_kernel[dom]
+    t_hbm, t_tc = kb / (hbm * 1e9), (kops / ((i8_peak or 2 * bf16) * 1e12) if kops else 0.0)
+    if t_tc > t_hbm:
+        roof = {"kernel": dom, "bound": "tensor", "achieved": kops / (dom_ms * 1e-3) / 1e12,
+                "peak": i8_peak or 2 * bf16, "unit": "TOPS(int8)"}
+    else:
+        roof = {"kernel": dom, "bound": "hbm", "achieved": kb / (dom_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["algorithmic_bytes_per_launch"] = kb
+    roof["ms_per_launch"] = dom_ms
+    roof["peak_source"] = peak_kind if roof["bound"] == "hbm" else ("torch._int_mm 8192^3 measured live" if i8_peak else "2x bf16 planning")
+    value = world * n / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8", "data": "synthetic (torch.randn on device, seeded per rank)",
+        "config": {"workload": "config4: N=1024/GPU Cin=Cout=256 56x56 pad1 Legendre F(4,3) 8b fwd",
+                   "scale_groups": "image", "l2": "inputs (3.29 GB) larger than L2", "global_batch": world * n,
+                   "parallelism": f"batch-sharded x{world}, no collective"},
+        "effective_tops": world * eff / (ms * 1e-3) / 1e12,
+        "layer_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms * 1e-3), "hbm_bytes": bytes_,
+                           "int8_ops": i8ops, "int8_peak_tops": i8_peak, "hbm_gbs": hbm},
+        "roofline": roof,
+        "kernel_ms": {kname: round(v, 4) for kname, v in per_kernel.items()},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

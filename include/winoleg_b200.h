@@ -89,6 +89,12 @@ int wl_debug_layout(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, si
 /* Number of kernels wl_forward launches for this shape (reported by bench.py as gpu_launches). */
 int wl_forward_launches(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q);
 
+/* Optional per-kernel CUDA-event timing of wl_forward (measurement only, not thread safe):
+ * wl_profile_read synchronises the device and returns, per kernel slot, the summed milliseconds
+ * over every wl_forward issued since the previous read. */
+int wl_profile_enable(int on);
+int wl_profile_read(const char** names_out, double* ms_out, int max, int* n_out, int* calls_out);
+
 const char* wl_last_error(void);
 
 #ifdef __cplusplus

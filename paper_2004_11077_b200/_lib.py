@@ -37,7 +37,7 @@ _lib = None
 
 EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_mode", "wl_weight_cache_size", "wl_weight_transform",
            "wl_workspace_size", "wl_forward", "wl_num_stages", "wl_read_stats", "wl_debug_layout",
-           "wl_forward_launches", "wl_last_error")
+           "wl_forward_launches", "wl_profile_enable", "wl_profile_read", "wl_last_error")
 
 
 def lib():
@@ -62,6 +62,8 @@ def lib():
     L.wl_read_stats.argtypes = [VP, P(wl_shape), P(wl_qcfg), VP, VP, P(wl_stage_stat), VP]
     L.wl_debug_layout.argtypes = [VP, P(wl_shape), P(wl_qcfg), P(S), P(I)]
     L.wl_forward_launches.argtypes = [VP, P(wl_shape), P(wl_qcfg)]
+    L.wl_profile_enable.argtypes = [I]
+    L.wl_profile_read.argtypes = [P(ctypes.c_char_p), P(ctypes.c_double), I, P(I), P(I)]
     L.wl_last_error.restype = ctypes.c_char_p
     L.wl_last_error.argtypes = []
     _lib = L
@@ -77,3 +79,16 @@ def check(rc: int, what: str) -> None:
     if rc in (WL_ERR_BITS, WL_ERR_PLAN):
         raise ValueError(f"{what}: {msg}")
     raise CudaLayerError(f"{what} failed ({rc}): {msg}")
+
+
+def profile_enable(on: bool) -> None:
+    check(lib().wl_profile_enable(int(on)), "wl_profile_enable")
+
+
+def profile_read() -> tuple[dict, int]:
+    """{kernel name: summed ms} over the wl_forward calls since the last read, and the call count."""
+    names = (ctypes.c_char_p * 32)()
+    ms = (ctypes.c_double * 32)()
+    n, calls = ctypes.c_int(), ctypes.c_int()
+    check(lib().wl_profile_read(names, ms, 32, ctypes.byref(n), ctypes.byref(calls)), "wl_profile_read")
+    return {names[i].decode(): ms[i] for i in range(min(n.value, 32))}, calls.value

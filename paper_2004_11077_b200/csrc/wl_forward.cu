@@ -47,6 +47,35 @@ struct wl_plan {
   PlanF64* d_pf;
 };
 
+// ------------------------------------------------------------------ optional per-kernel event timing
+// (bench.py: kernel share of the step and the dominant kernel's roofline).  Process global, meant
+// for single-threaded measurement only.
+namespace {
+struct ProfCall {
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> names;
+};
+struct Prof {
+  bool on = false;
+  std::vector<ProfCall> calls;
+  ProfCall* cur = nullptr;
+} g_prof;
+
+void prof_begin() {
+  if (!g_prof.on) return;
+  g_prof.calls.emplace_back();
+  g_prof.cur = &g_prof.calls.back();
+}
+void prof_mark(const char* name, cudaStream_t st) {
+  if (!g_prof.on || !g_prof.cur) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_prof.cur->ev.push_back(e);
+  g_prof.cur->names.push_back(name);
+}
+}  // namespace
+
 // ------------------------------------------------------------------ stage-width plumbing
 
 static int check_bits(const wl_qcfg* q) {
@@ -294,6 +323,42 @@ extern "C" {
 
 const char* wl_last_error(void) { return g_err.c_str(); }
 
+int wl_profile_enable(int on) {
+  g_prof.on = on != 0;
+  return WL_OK;
+}
+
+// Sums the per-kernel event intervals of every wl_forward since the last read (synchronising).
+// names_out receives up to `max` kernel names (static strings), ms_out their summed milliseconds.
+int wl_profile_read(const char** names_out, double* ms_out, int max, int* n_out, int* calls_out) {
+  WL_CUDA(cudaDeviceSynchronize());
+  int n = 0;
+  std::vector<double> acc;
+  std::vector<const char*> names;
+  for (auto& c : g_prof.calls) {
+    for (size_t i = 1; i < c.ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c.ev[i - 1], c.ev[i]);
+      if (acc.size() < i) {
+        acc.push_back(0.0);
+        names.push_back(c.names[i]);
+      }
+      acc[i - 1] += ms;
+    }
+    for (auto e : c.ev) cudaEventDestroy(e);
+  }
+  n = (int)acc.size();
+  for (int i = 0; i < n && i < max; ++i) {
+    if (names_out) names_out[i] = names[i];
+    if (ms_out) ms_out[i] = acc[i];
+  }
+  if (n_out) *n_out = n;
+  if (calls_out) *calls_out = (int)g_prof.calls.size();
+  g_prof.calls.clear();
+  g_prof.cur = nullptr;
+  return WL_OK;
+}
+
 int wl_plan_create(int o, int k, int mode, const int64_t* int_mats, const double* f64_mats, wl_plan** out) {
   if (!out || !int_mats || !f64_mats) return fail(WL_ERR_ARG, "NULL argument");
   if (o != 4 || k != 3) return fail(WL_ERR_PLAN, "only F(4,3) is compiled for sm_100a (got F(%d,%d))", o, k);
@@ -458,23 +523,32 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
   const Bits b = make_bits(q);
   const bool leg = plan->mode == WL_LEGENDRE;
 
+  prof_begin();
   WL_CUDA(cudaMemsetAsync(acc, 0, sizeof(Acc) * ST_COUNT * L.groups, st));
+  prof_mark("begin", st);
   {
     const long long per_image = (long long)g.C * g.H * g.W;
     int bx = (int)std::min<long long>((per_image / 4 + 255) / 256, 64);
     absmax_f32_kernel<<<dim3(std::max(bx, 1), g.N), 256, 0, st>>>(x, per_image, g.ipg, acc);
+    prof_mark("absmax_input", st);
     quant_input_kernel<<<dim3(g.Cp / 32, g.H, g.N), 256, 0, st>>>(x, c0, g, b, acc);
+    prof_mark("quant_input", st);
   }
   const long long tc = (long long)g.T * g.C;
   const int tb = 256;
   const unsigned tgrid = (unsigned)((tc + tb - 1) / tb);
   if (!leg) {
     input_stage_kernel<0, 0><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    prof_mark("input_transform_max", st);
     input_stage_kernel<0, 2><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    prof_mark("input_transform_codes", st);
   } else {
     input_stage_kernel<1, 0><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    prof_mark("input_base_change_max", st);
     input_stage_kernel<1, 1><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    prof_mark("input_transform_max", st);
     input_stage_kernel<1, 2><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    prof_mark("input_transform_codes", st);
   }
   WL_CUDA(cudaGetLastError());
   // padded channels of V must be zero for the GEMM: the stage kernels only write c < C
@@ -502,6 +576,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     e.qmax_v = b.q[ST_IT];
     rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
     if (rc) return rc;
+    prof_mark("gemm_hadamard_max", st);
   }
   if (L.hbytes == 1) {
     EpiHadRq<int8_t> e;
@@ -531,17 +606,23 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
   }
   if (rc) return rc;
+  prof_mark("gemm_hadamard_codes", st);
 
   const long long oc = (long long)g.T * g.K;
   const unsigned ogrid = (unsigned)((oc + tb - 1) / tb);
 #define WL_OUT(HT)                                                                                             \
   if (!leg) {                                                                                                  \
     output_stage_kernel<0, 0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+    prof_mark("output_max", st);                                                                               \
     output_stage_kernel<0, 2, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+    prof_mark("output_write", st);                                                                             \
   } else {                                                                                                     \
     output_stage_kernel<1, 0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+    prof_mark("output_base_change_max", st);                                                                   \
     output_stage_kernel<1, 1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+    prof_mark("output_max", st);                                                                               \
     output_stage_kernel<1, 2, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
+    prof_mark("output_write", st);                                                                             \
   }
   if (L.hbytes == 1) {
     WL_OUT(int8_t)
