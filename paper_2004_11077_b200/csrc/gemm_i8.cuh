@@ -23,8 +23,9 @@ struct GemmSmem {
   static constexpr int kBytes = 1024 + STAGES * (kA + kB) + 256;
 };
 
-// Epilogue contract: Epi::apply(row, col0, vals[16], nvalid) per thread for 16 consecutive columns
-// of one row, then Epi::finish() once per epilogue thread.
+// Epilogue contract: Epi::begin(xi, row, valid), then Epi::apply(xi, row, col0, vals[16], nvalid) per
+// thread for 16 consecutive columns of one row, then Epi::finish(xi, row, valid) once per thread
+// (all 32 lanes of each epilogue warp reach finish, so it may use warp collectives).
 template <int BN, int SW, int STAGES, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int T,
@@ -99,14 +100,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16);
     epi.begin(xi, row, row < T);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t r[16];
-      tmem_ld16(taddr + c, r);
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r0[16], r1[16];
+      tmem_ld16(taddr + c, r0);
+      tmem_ld16(taddr + c + 16, r1);
       tmem_ld_wait();
       const int col = n0 + c;
-      int nvalid = Kout - col;
-      nvalid = nvalid > 16 ? 16 : nvalid;
-      if (row < T && nvalid > 0) epi.apply(xi, row, col, reinterpret_cast<int32_t*>(r), nvalid);
+      const int nv0 = Kout - col, nv1 = Kout - col - 16;
+      if (row < T && nv0 > 0) epi.apply(xi, row, col, r0, nv0 > 16 ? 16 : nv0);
+      if (row < T && nv1 > 0) epi.apply(xi, row, col + 16, r1, nv1 > 16 ? 16 : nv1);
     }
     epi.finish(xi, row, row < T);
   }

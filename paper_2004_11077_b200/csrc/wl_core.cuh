@@ -19,10 +19,16 @@ enum StageId { ST_INPUT = 0, ST_WEIGHTS, ST_WT, ST_WBC, ST_IBC, ST_IT, ST_HAD, S
 // Per (group, stage) reduction slot: M = max |T| (integer stages) or fp32 bits of max |x| (input /
 // weights); F = fp64 bits of the reference's max_abs (positive doubles order like uint64).
 struct Acc {
-  unsigned long long M;
-  unsigned long long F;
+  unsigned long long M;   // exact integer max |T| (fp32 bits of max|x| for input / weights)
+  unsigned long long F;   // fp64 bits of the reference max_abs
+  unsigned int MF;        // fp32 bits of the running max of the fp32 fast-path values (candidate gate)
+  unsigned int pad_;
 };
 
+// Max tables: every hot pass writes the maximum of each 32-unit entry (fp32 bits for the transform
+// stages, exact int for the Hadamard row chunks).  A finalize kernel scans the table, recomputes
+// exactly only the entries that can hold the group's argmax, and replays that argmax in fp64.
+// Deterministic, no capacity limit.
 struct StageQ {
   long long M;
   double maxabs, scale;
@@ -163,6 +169,86 @@ __device__ __forceinline__ void publish_max(long long m, int g, Acc* acc, int st
   } else if (m > 0 && g >= 0) {
     atomicMax(&acc[(size_t)g * stride].M, (unsigned long long)m);
   }
+}
+
+// ---------------------------------------------------------------- fp32 fast path
+
+// Parameters of one integer stage for the fp32 fast path: x = T_f * r, rounded half-even by the
+// magic-number add; elements whose x lies within `band` of a half-integer take the exact path.
+struct StageF {
+  float r, band;
+  int qmax;
+};
+__device__ __forceinline__ StageF load_stage_f(const Acc& a, int qmax, float E) {
+  StageF s;
+  const float M = (float)(long long)a.M;
+  s.qmax = qmax;
+  s.r = a.M ? (float)qmax / M : 0.f;
+  s.band = a.M ? (float)qmax * (E / M) + 1e-4f : 0.f;
+  return s;
+}
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x half-even to an integer
+__device__ __forceinline__ int rq_fast(float T, const StageF& s, float& dmax) {
+  const float x = T * s.r;
+  const float y = x + kMagic;
+  const float k = y - kMagic;
+  dmax = fmaxf(dmax, fabsf(x - k));
+  return __float_as_int(y) - 0x4B400000;
+}
+
+// Record the fp32 maximum `m` of this lane's unit into the entry (t, c/32) of the stage's max table
+// and into the group's running fp32 maximum.  When the warp is exactly one entry (channel-aligned),
+// lane 0 stores; otherwise lanes atomically max into their entries.
+__device__ __forceinline__ void record_max(float m, int g, unsigned* table_entry, bool aligned, Acc* acc_stage,
+                                          bool& uniform, float& wmax) {
+  const unsigned full = 0xffffffffu;
+  const int g0 = __shfl_sync(full, g, 0);
+  uniform = __all_sync(full, g == g0) && aligned;
+  wmax = m;
+  if (uniform) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(full, wmax, o));
+    if ((threadIdx.x & 31) == 0 && g >= 0) *table_entry = __float_as_uint(wmax);
+  } else if (g >= 0) {
+    atomicMax(table_entry, __float_as_uint(m));
+  }
+}
+
+__device__ __forceinline__ void publish_mf(float m, int g, Acc* acc_stage, bool uniform, float wmax) {
+  if (uniform) {
+    if ((threadIdx.x & 31) == 0 && wmax > 0.f && g >= 0)
+      atomicMax(&acc_stage[(size_t)g * ST_COUNT].MF, __float_as_uint(wmax));
+  } else if (m > 0.f && g >= 0) {
+    atomicMax(&acc_stage[(size_t)g * ST_COUNT].MF, __float_as_uint(m));
+  }
+}
+
+// fp32 sandwich out = L . X . L^T with compile-time integer L (R x C).  The first half X . L^T is
+// exact (|partial sums| <= qmax_in * rowsum(L) < 2^24); the second half rounds once per fma, so
+// |out - exact| <= 8 * 2^-24 * rowsum(L)^2 * qmax_in (the per-stage E passed to the kernels).
+template <class L>
+__device__ __forceinline__ void sandwich_f(const float (&X)[L::C][L::C], float (&out)[L::R][L::R]) {
+  float tmp[L::C][L::R];
+#pragma unroll
+  for (int i = 0; i < L::C; ++i)
+#pragma unroll
+    for (int j = 0; j < L::R; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int l = 0; l < L::C; ++l)
+        if (L::e(j, l) != 0) s = fmaf(X[i][l], (float)L::e(j, l), s);
+      tmp[i][j] = s;
+    }
+#pragma unroll
+  for (int i = 0; i < L::R; ++i)
+#pragma unroll
+    for (int j = 0; j < L::R; ++j) {
+      float s = 0.f;
+#pragma unroll
+      for (int l = 0; l < L::C; ++l)
+        if (L::e(i, l) != 0) s = fmaf((float)L::e(i, l), tmp[l][j], s);
+      out[i][j] = s;
+    }
 }
 
 // Compile-time sandwich out = L . X . L^T with L a tab:: matrix (R x C), X (C x C).

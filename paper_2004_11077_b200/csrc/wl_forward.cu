@@ -7,12 +7,13 @@
 #include <cstdarg>
 #include <cstdio>
 #include <vector>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
 #include "../../include/winoleg_b200.h"
 #include "gemm_i8.cuh"
-#include "wl_kernels.cuh"
+#include "wl_kernels2.cuh"
 #include "wl_tmap.h"
 
 using namespace wl;
@@ -124,10 +125,13 @@ static const int kLegOrder[9] = {ST_INPUT, ST_WEIGHTS, ST_WT, ST_WBC, ST_IBC, ST
 
 // ------------------------------------------------------------------ geometry / workspace
 
+constexpr int kNumTables = 5;  // IBC, IT, HAD, OBC, OUT
+static const int kTableStage[kNumTables] = {ST_IBC, ST_IT, ST_HAD, ST_OBC, ST_OUT};
+
 struct Layout {
   Geo g;
-  size_t off_acc, off_c0, off_v, off_h, total;
-  int groups, hbytes;
+  size_t off_acc, off_c0, off_v, off_h, off_c1, off_c4, off_tab[kNumTables], tab_bytes[kNumTables], total;
+  int groups, hbytes, bn;
 };
 
 static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
@@ -166,6 +170,18 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   o = align256(o + (size_t)36 * g.T * g.Cp);
   L->off_h = o;
   o = align256(o + (size_t)36 * g.T * g.Kp * L->hbytes);
+  L->off_c1 = o;
+  o = align256(o + (size_t)36 * g.T * g.Cp);
+  L->off_c4 = o;
+  o = align256(o + (size_t)36 * g.T * g.Kp);
+  L->bn = g.Kp >= 128 ? 128 : g.Kp;
+  const size_t CB = (g.C + 31) / 32, KB = (g.K + 31) / 32;
+  const size_t ents[kNumTables] = {g.T * CB, g.T * CB, (size_t)36 * g.T * (g.Kp / L->bn), g.T * KB, g.T * KB};
+  for (int i = 0; i < kNumTables; ++i) {
+    L->off_tab[i] = o;
+    L->tab_bytes[i] = ents[i] * sizeof(unsigned);
+    o = align256(o + L->tab_bytes[i]);
+  }
   L->total = o;
   return WL_OK;
 }
@@ -184,62 +200,44 @@ static size_t weight_cache_bytes(int K, int C, int* Kp, int* Cp) {
 
 // ------------------------------------------------------------------ GEMM epilogues
 
+// Max pass: exact int32 accumulators; per-thread maximum over its row chunk; the group maximum M is
+// reduced in place (atomicMax) and units that may hold the argmax are pushed as candidates for the
+// fp64 replay in finalize_hadamard_kernel.
 struct EpiHadMax {
   Acc* acc;
-  const Acc* wacc;
-  const int8_t* U;
-  const int8_t* V;
+  unsigned* table;
   Geo g;
-  int wstage, qmax_u, qmax_v;
+  int nchunk;
   long long m;
-  int cnt, grp;
-  int pos[4];
-  __device__ void begin(int, int row, bool valid) {
+  int grp;
+  __device__ __forceinline__ void begin(int, int row, bool valid) {
     m = 0;
-    cnt = 0;
     grp = valid ? (row / g.TP) / g.ipg : -1;
   }
-  __device__ void apply(int, int, int col, const int32_t* v, int n) {
+  __device__ __forceinline__ void apply(int, int, int, const uint32_t* v, int n) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      if (j >= n) break;
-      long long a = v[j] < 0 ? -(long long)v[j] : (long long)v[j];
-      if (a > m) {
-        m = a;
-        cnt = 0;
-      }
-      if (a == m) {
-        if (cnt < 4) pos[cnt] = col + j;
-        ++cnt;
+      if (j < n) {
+        const int x = (int)v[j];
+        const long long a = x < 0 ? -(long long)x : (long long)x;
+        m = a > m ? a : m;
       }
     }
   }
-  __device__ void finish(int xi, int row, bool) {
+  __device__ __forceinline__ void finish(int xi, int row, bool valid) {
+    if (valid) table[((size_t)xi * g.T + row) * nchunk + blockIdx.y] = (unsigned)m;
     bool uniform;
     long long wmax;
     Acc* a = acc + ST_HAD;
-    if (replay_gate(m, grp, a, ST_COUNT, uniform, wmax)) {
-      const StageQ qu = load_int_stage(wacc[wstage], qmax_u);
-      const StageQ qv = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_IT], qmax_v);
-      const int8_t* vrow = V + ((size_t)xi * g.T + row) * g.Cp;
-      double f = 0.0;
-      if (cnt <= 4) {
-        for (int p = 0; p < cnt; ++p)
-          f = fmax(f, fabs(replay_hadamard(U + ((size_t)xi * g.Kp + pos[p]) * g.Cp, vrow, g.C, qu, qv)));
-      } else {  // many equal maxima in this row: find them all on CUDA cores
-        for (int k = 0; k < g.K; ++k) {
-          const int8_t* urow = U + ((size_t)xi * g.Kp + k) * g.Cp;
-          long long s = 0;
-          for (int c = 0; c < g.C; ++c) s += (int)urow[c] * (int)vrow[c];
-          if ((s < 0 ? -s : s) == m) f = fmax(f, fabs(replay_hadamard(urow, vrow, g.C, qu, qv)));
-        }
-      }
-      atomicMax(&a[(size_t)grp * ST_COUNT].F, dbits(f));
-    }
+    // (replay_gate only computes the warp reduction here; the replay itself runs in finalize)
+    replay_gate(m, grp, a, ST_COUNT, uniform, wmax);
     publish_max(m, grp, a, ST_COUNT, uniform, wmax);
   }
 };
 
+// Requantisation pass: h = rhe(qmax_h * I / M) with the fp32 magic-number fast path (I is exact and
+// |I| < 2^24, so the only inexactness is the product by qmax/M); near half-integers the exact int64
+// decision, and exact ties are replayed in fp64 from the U and V codes.
 template <typename HT>
 struct EpiHadRq {
   Acc* acc;
@@ -249,30 +247,30 @@ struct EpiHadRq {
   HT* h;
   Geo g;
   int wstage, qmax_u, qmax_v, qmax_h;
-  StageQ q;
+  StageF s;
   int grp;
-  __device__ void begin(int, int row, bool valid) {
+  __device__ __forceinline__ void begin(int, int row, bool valid) {
     grp = valid ? (row / g.TP) / g.ipg : 0;
-    q = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h);
+    s = load_stage_f(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h, 0.f);
   }
-  __device__ void apply(int xi, int row, int col, const int32_t* v, int n) {
+  __device__ __forceinline__ void apply(int xi, int row, int col, const uint32_t* v, int n) {
     HT out[16];
-    bool any = false;
-    bool tie[16];
+    float dmax = 0.f;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      bool t = false;
-      out[j] = (HT)rq(v[j], q, t);
-      tie[j] = t && j < n;
-      any |= tie[j];
-    }
-    if (any) {
-      const StageQ qu = load_int_stage(wacc[wstage], qmax_u);
-      const StageQ qv = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_IT], qmax_v);
-      const int8_t* vrow = V + ((size_t)xi * g.T + row) * g.Cp;
-      for (int j = 0; j < 16; ++j)
-        if (tie[j])
-          out[j] = (HT)code_of(replay_hadamard(U + ((size_t)xi * g.Kp + col + j) * g.Cp, vrow, g.C, qu, qv), q);
+    for (int j = 0; j < 16; ++j) out[j] = (HT)rq_fast((float)(int)v[j], s, dmax);
+    if (dmax > 0.5f - s.band) {
+      const StageQ q = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h);
+      for (int j = 0; j < 16; ++j) {
+        bool tie = false;
+        int code = rq((long long)(int)v[j], q, tie);
+        if (tie && j < n) {
+          const StageQ qu = load_int_stage(wacc[wstage], qmax_u);
+          const StageQ qv = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_IT], qmax_v);
+          code = code_of(replay_hadamard(U + ((size_t)xi * g.Kp + col + j) * g.Cp,
+                                         V + ((size_t)xi * g.T + row) * g.Cp, g.C, qu, qv), q);
+        }
+        out[j] = (HT)code;
+      }
     }
     HT* dst = h + ((size_t)xi * g.T + row) * g.Kp + col;
     if (sizeof(HT) == 1) {
@@ -282,12 +280,12 @@ struct EpiHadRq {
       reinterpret_cast<int4*>(dst)[1] = reinterpret_cast<const int4*>(out)[1];
     }
   }
-  __device__ void finish(int, int, bool) {}
+  __device__ __forceinline__ void finish(int, int, bool) {}
 };
 
 template <int BN, int SW, class Epi>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo& g, const Epi& e, cudaStream_t st) {
-  constexpr int STAGES = 4;
+  constexpr int STAGES = 3;
   using L = GemmSmem<BN, SW, STAGES>;
   auto kern = gemm_i8_kernel<BN, SW, STAGES, Epi>;
   static bool attr_set = false;  // per instantiation; idempotent
@@ -306,15 +304,43 @@ static int dispatch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo
                          cudaStream_t st) {
 #define WL_G(BN_, SW_) \
   if (bn == BN_ && sw == SW_) return launch_gemm<BN_, SW_, Epi>(ta, tb, g, e, st);
-  WL_G(64, 32) WL_G(64, 64) WL_G(64, 128) WL_G(128, 32) WL_G(128, 64) WL_G(128, 128) WL_G(256, 32) WL_G(256, 64)
-  WL_G(256, 128)
+  WL_G(64, 32) WL_G(64, 64) WL_G(64, 128) WL_G(128, 32) WL_G(128, 64) WL_G(128, 128)
 #undef WL_G
   return fail(WL_ERR_ARG, "no GEMM tile for BN=%d SW=%d", bn, sw);
 }
 
 static void gemm_tiles(const Geo& g, int* bn, int* sw) {
-  *bn = g.Kp >= 256 ? 256 : g.Kp;
+  *bn = g.Kp >= 128 ? 128 : g.Kp;  // must match Layout::bn
   *sw = g.Cp % 128 == 0 ? 128 : (g.Cp % 64 == 0 ? 64 : 32);
+}
+
+// Certified fp32 error bound of each stage's fast path (integer units): the first sandwich half is
+// exact, the second rounds once per fma (<= 6 of them) on partial sums bounded by
+// rowsum(L)^2 * qmax_in, so |T_f - T| <= 6 * 2^-24 * rowsum^2 * qmax_in; 8 is used for margin.
+static StageE stage_errors(int mode, const Bits& b) {
+  auto rowsum = [](auto tag, int R, int C) {
+    using M = decltype(tag);
+    long long best = 0;
+    for (int i = 0; i < R; ++i) {
+      long long s = 0;
+      for (int j = 0; j < C; ++j) s += std::abs(M::e(i, j));
+      best = std::max(best, s);
+    }
+    return (double)best;
+  };
+  auto bound = [](double rs, int qin) { return (float)(8.0 * rs * rs * qin / 16777216.0); };
+  StageE E;
+  for (int i = 0; i < ST_COUNT; ++i) E.e[i] = 0.f;
+  if (mode == WL_CANONICAL) {
+    E.e[ST_IT] = bound(rowsum(tab::Can_IT{}, 6, 6), b.q[ST_INPUT]);
+    E.e[ST_OUT] = bound(rowsum(tab::Can_OT{}, 4, 6), b.q[ST_HAD]);
+  } else {
+    E.e[ST_IBC] = bound(rowsum(tab::Leg_IBC{}, 6, 6), b.q[ST_INPUT]);
+    E.e[ST_IT] = bound(rowsum(tab::Leg_IT{}, 6, 6), b.q[ST_IBC]);
+    E.e[ST_OBC] = bound(rowsum(tab::Leg_OBC{}, 6, 6), b.q[ST_HAD]);
+    E.e[ST_OUT] = bound(rowsum(tab::Leg_OT{}, 4, 6), b.q[ST_OBC]);
+  }
+  return E;
 }
 
 // ------------------------------------------------------------------ C ABI
@@ -499,7 +525,9 @@ int wl_debug_layout(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, si
 int wl_forward_launches(const wl_plan* plan, const wl_shape*, const wl_qcfg*) {
   if (!plan) return WL_ERR_ARG;
   // absmax, quant, input passes (2|3), gemm max, gemm requant, output passes (2|3)
-  return plan->mode == WL_LEGENDRE ? 10 : 8;
+  // absmax, quant, then (Legendre) in_a + fin, in_b + fin, in_c, gemm + fin, gemm, out_a + fin, out_b + fin,
+  // out_c  | (canonical) in_a + fin, in_c, gemm + fin, gemm, out_a + fin, out_c
+  return plan->mode == WL_LEGENDRE ? 17 : 12;
 }
 
 int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
@@ -534,48 +562,57 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     quant_input_kernel<<<dim3(g.Cp / 32, g.H, g.N), 256, 0, st>>>(x, c0, g, b, acc);
     prof_mark("quant_input", st);
   }
+  int8_t* c1 = reinterpret_cast<int8_t*>(ws + L.off_c1);
+  int8_t* c4 = reinterpret_cast<int8_t*>(ws + L.off_c4);
+  Tables tabs;
+  for (int i = 0; i < ST_COUNT; ++i) tabs.t[i] = nullptr;
+  for (int i = 0; i < kNumTables; ++i) {
+    tabs.t[kTableStage[i]] = reinterpret_cast<unsigned*>(ws + L.off_tab[i]);
+    if (kTableStage[i] != ST_HAD) WL_CUDA(cudaMemsetAsync(ws + L.off_tab[i], 0, L.tab_bytes[i], st));
+  }
+  const StageE E = stage_errors(plan->mode, b);
+
   const long long tc = (long long)g.T * g.C;
   const int tb = 256;
   const unsigned tgrid = (unsigned)((tc + tb - 1) / tb);
+  const int fin_blocks = 4 * 148;
   if (!leg) {
-    input_stage_kernel<0, 0><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    in_a_kernel<0><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
+    finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
     prof_mark("input_transform_max", st);
-    input_stage_kernel<0, 2><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    in_c_kernel<0><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, E);
     prof_mark("input_transform_codes", st);
   } else {
-    input_stage_kernel<1, 0><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    in_a_kernel<1><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
+    finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
     prof_mark("input_base_change_max", st);
-    input_stage_kernel<1, 1><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    in_b_kernel<<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs, E);
+    finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
     prof_mark("input_transform_max", st);
-    input_stage_kernel<1, 2><<<tgrid, tb, 0, st>>>(c0, V, g, b, acc, plan->d_pf);
+    in_c_kernel<1><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, E);
     prof_mark("input_transform_codes", st);
   }
   WL_CUDA(cudaGetLastError());
   // padded channels of V must be zero for the GEMM: the stage kernels only write c < C
-  // (zeroed once per call when C is not a multiple of 32)
-  if (g.Cp != g.C) {
-    // write zeros for the padding columns through a 2-D memset
-    WL_CUDA(cudaMemset2DAsync(V + g.C, g.Cp, 0, g.Cp - g.C, (size_t)36 * g.T, st));
-  }
+  if (g.Cp != g.C) WL_CUDA(cudaMemset2DAsync(V + g.C, g.Cp, 0, g.Cp - g.C, (size_t)36 * g.T, st));
 
   int bn, sw;
   gemm_tiles(g, &bn, &sw);
   CUtensorMap ta, tbm;
   if (!make_tmap_i8_3d(&ta, V, g.Cp, g.T, 36, sw, 128) || !make_tmap_i8_3d(&tbm, U, g.Cp, g.Kp, 36, sw, bn))
     return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  const int qu = b.q[wh ? (leg ? ST_WBC : ST_WT) : ST_WT];
+  const int wstage = leg ? ST_WBC : ST_WT;
+  const int qu = b.q[wstage];
   {
     EpiHadMax e;
     e.acc = acc;
-    e.wacc = wh->wacc;
-    e.U = U;
-    e.V = V;
+    e.table = tabs.t[ST_HAD];
     e.g = g;
-    e.wstage = leg ? ST_WBC : ST_WT;
-    e.qmax_u = qu;
-    e.qmax_v = b.q[ST_IT];
+    e.nchunk = g.Kp / bn;
     rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
     if (rc) return rc;
+    finalize_hadamard_kernel<<<fin_blocks, 256, 0, st>>>(U, V, g, acc, wh->wacc, wstage, qu, b.q[ST_IT],
+                                                         tabs.t[ST_HAD], bn);
     prof_mark("gemm_hadamard_max", st);
   }
   if (L.hbytes == 1) {
@@ -586,7 +623,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     e.V = V;
     e.h = reinterpret_cast<int8_t*>(h);
     e.g = g;
-    e.wstage = leg ? ST_WBC : ST_WT;
+    e.wstage = wstage;
     e.qmax_u = qu;
     e.qmax_v = b.q[ST_IT];
     e.qmax_h = b.q[ST_HAD];
@@ -599,7 +636,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     e.V = V;
     e.h = reinterpret_cast<int16_t*>(h);
     e.g = g;
-    e.wstage = leg ? ST_WBC : ST_WT;
+    e.wstage = wstage;
     e.qmax_u = qu;
     e.qmax_v = b.q[ST_IT];
     e.qmax_h = b.q[ST_HAD];
@@ -610,19 +647,25 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
 
   const long long oc = (long long)g.T * g.K;
   const unsigned ogrid = (unsigned)((oc + tb - 1) / tb);
-#define WL_OUT(HT)                                                                                             \
-  if (!leg) {                                                                                                  \
-    output_stage_kernel<0, 0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
-    prof_mark("output_max", st);                                                                               \
-    output_stage_kernel<0, 2, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
-    prof_mark("output_write", st);                                                                             \
-  } else {                                                                                                     \
-    output_stage_kernel<1, 0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
-    prof_mark("output_base_change_max", st);                                                                   \
-    output_stage_kernel<1, 1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
-    prof_mark("output_max", st);                                                                               \
-    output_stage_kernel<1, 2, HT><<<ogrid, tb, 0, st>>>((const HT*)h, y, bias, g, b, acc, plan->d_pf);         \
-    prof_mark("output_write", st);                                                                             \
+#define WL_OUT(HT)                                                                                              \
+  if (!leg) {                                                                                                   \
+    out_a_kernel<0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, g, acc, tabs);                                  \
+    finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
+        tabs.t[ST_OUT], E.e[ST_OUT]);                        \
+    prof_mark("output_max", st);                                                                                \
+    out_c_kernel<0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, y, bias, g, b, acc, plan->d_pf, E);             \
+    prof_mark("output_write", st);                                                                              \
+  } else {                                                                                                      \
+    out_a_kernel<1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, g, acc, tabs);                                  \
+    finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
+        tabs.t[ST_OBC], E.e[ST_OBC]);                        \
+    prof_mark("output_base_change_max", st);                                                                    \
+    out_b_kernel<HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf, tabs, E);                  \
+    finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
+        tabs.t[ST_OUT], E.e[ST_OUT]);                        \
+    prof_mark("output_max", st);                                                                                \
+    out_c_kernel<1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, y, bias, g, b, acc, plan->d_pf, E);             \
+    prof_mark("output_write", st);                                                                              \
   }
   if (L.hbytes == 1) {
     WL_OUT(int8_t)
