@@ -21,8 +21,11 @@ enum StageId { ST_INPUT = 0, ST_WEIGHTS, ST_WT, ST_WBC, ST_IBC, ST_IT, ST_HAD, S
 struct Acc {
   unsigned long long M;   // exact integer max |T| (fp32 bits of max|x| for input / weights)
   unsigned long long F;   // fp64 bits of the reference max_abs
-  unsigned int MF;        // fp32 bits of the running max of the fp32 fast-path values (candidate gate)
-  unsigned int pad_;
+  unsigned int MF;        // fp32 bits of the running max of the fp32 fast-path values
+  float thr;              // fast path: 0.5 - band (set by stage_params_kernel once M is final)
+  float r;                // fast path: qmax / M
+  unsigned int TM;        // fp32 bits of max |first-half value| over the group (error bound input)
+  double scale;           // reference scale max_abs / qmax (1.0 when max_abs == 0)
 };
 
 // Max tables: every hot pass writes the maximum of each 32-unit entry (fp32 bits for the transform
@@ -184,15 +187,23 @@ __device__ __forceinline__ StageF load_stage_f(const Acc& a, int qmax, float E) 
   const float M = (float)(long long)a.M;
   s.qmax = qmax;
   s.r = a.M ? (float)qmax / M : 0.f;
-  s.band = a.M ? (float)qmax * (E / M) + 1e-4f : 0.f;
+  // slack: T_f error E, r = fl(qmax/M) relative 2^-24 (<= 1.6e-5 code units at qmax 255), fma rounding
+  s.band = a.M ? (float)qmax * (E / M) + 3e-5f : 0.f;
   return s;
 }
-constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x half-even to an integer
-__device__ __forceinline__ int rq_fast(float T, const StageF& s, float& dmax) {
-  const float x = T * s.r;
-  const float y = x + kMagic;
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: fma(T, r, kMagic) rounds T*r half-even to an integer
+// One requantisation: y = fl(T*r + kMagic) holds rhe(T*r) in its low mantissa bits (single
+// rounding of the exact product); d = fl(T*r - k) measures the distance to that integer.
+// Returns the code as float (exact); `y` bits carry the two's-complement code in their low byte.
+__device__ __forceinline__ float rq_fast_f(float T, const StageF& s, float& dmax, float& y) {
+  y = fmaf(T, s.r, kMagic);
   const float k = y - kMagic;
-  dmax = fmaxf(dmax, fabsf(x - k));
+  dmax = fmaxf(dmax, fabsf(fmaf(T, s.r, -k)));
+  return k;
+}
+__device__ __forceinline__ int rq_fast(float T, const StageF& s, float& dmax) {
+  float y;
+  rq_fast_f(T, s, dmax, y);
   return __float_as_int(y) - 0x4B400000;
 }
 
@@ -227,8 +238,8 @@ __device__ __forceinline__ void publish_mf(float m, int g, Acc* acc_stage, bool 
 // exact (|partial sums| <= qmax_in * rowsum(L) < 2^24); the second half rounds once per fma, so
 // |out - exact| <= 8 * 2^-24 * rowsum(L)^2 * qmax_in (the per-stage E passed to the kernels).
 template <class L>
-__device__ __forceinline__ void sandwich_f(const float (&X)[L::C][L::C], float (&out)[L::R][L::R]) {
-  float tmp[L::C][L::R];
+__device__ __forceinline__ void sandwich_f(const float (&X)[L::C][L::C], float (&tmp)[L::C][L::R],
+                                           float (&out)[L::R][L::R]) {
 #pragma unroll
   for (int i = 0; i < L::C; ++i)
 #pragma unroll
@@ -249,6 +260,59 @@ __device__ __forceinline__ void sandwich_f(const float (&X)[L::C][L::C], float (
         if (L::e(i, l) != 0) s = fmaf((float)L::e(i, l), tmp[l][j], s);
       out[i][j] = s;
     }
+}
+
+template <class L>
+__device__ __forceinline__ void sandwich_f(const float (&X)[L::C][L::C], float (&out)[L::R][L::R]) {
+  float tmp[L::C][L::R];
+  sandwich_f<L>(X, tmp, out);
+}
+
+// Column-streaming fp32 sandwich: for each output column j, tc = X . L[j]^T (exact) and
+// col = L . tc; f(j, col) consumes the column before the next is formed, so only X and one column
+// are live (same operation count and error bound as sandwich_f).
+template <class L, class F>
+__device__ __forceinline__ void sandwich_cols(const float (&X)[L::C][L::C], F&& f, float* tmax = nullptr) {
+#pragma unroll
+  for (int j = 0; j < L::R; ++j) {
+    float tc[L::C];
+#pragma unroll
+    for (int l = 0; l < L::C; ++l) {
+      float s = 0.f;
+#pragma unroll
+      for (int l2 = 0; l2 < L::C; ++l2)
+        if (L::e(j, l2) != 0) s = fmaf(X[l][l2], (float)L::e(j, l2), s);
+      tc[l] = s;
+      if (tmax) *tmax = fmaxf(*tmax, fabsf(s));
+    }
+    float col[L::R];
+#pragma unroll
+    for (int i = 0; i < L::R; ++i) {
+      float s = 0.f;
+#pragma unroll
+      for (int l = 0; l < L::C; ++l)
+        if (L::e(i, l) != 0) s = fmaf((float)L::e(i, l), tc[l], s);
+      col[i] = s;
+    }
+    f(j, col);
+  }
+}
+
+// Fast-path code of one element: y = fl(T*r + magic) (single rounding of the exact product);
+// when |T*r - k| is within the certified band of a half-integer, `exact()` recomputes the element
+// in integers (out of line, reloading its inputs from global memory).
+template <class Exact>
+__device__ __forceinline__ int rq_elem(float T, float r, float thr, Exact&& exact, float& kf) {
+  const float y = fmaf(T, r, kMagic);
+  const float k = y - kMagic;
+  int code = __float_as_int(y) - 0x4B400000;
+  if (fabsf(fmaf(T, r, -k)) > thr) {
+    code = exact();
+    kf = (float)code;
+  } else {
+    kf = k;
+  }
+  return code;
 }
 
 // Compile-time sandwich out = L . X . L^T with L a tab:: matrix (R x C), X (C x C).

@@ -158,7 +158,10 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   g.Cp = round_up(g.C, 32);
   g.Kp = g.K <= 64 ? 64 : (g.K <= 128 ? 128 : round_up(g.K, 256));
   g.ipg = s->images_per_group;
-  if ((long long)g.T * g.Cp * 36 > (1LL << 40)) return fail(WL_ERR_ARG, "problem too large");
+  if ((unsigned long long)g.T * std::max(g.Cp, g.Kp) * 36 >= (1ULL << 32) ||
+      (unsigned long long)g.N * g.H * g.W * g.Cp >= (1ULL << 32) || g.Cp > 4096 || g.Kp > 4096)
+    return fail(WL_ERR_ARG, "problem too large for one call (split the batch; per-image scale groups are "
+                            "independent)");
   L->groups = g.N / g.ipg;
   L->hbytes = q->hadamard_bits > 8 ? 2 : 1;
   size_t o = 0;
@@ -251,7 +254,10 @@ struct EpiHadRq {
   int grp;
   __device__ __forceinline__ void begin(int, int row, bool valid) {
     grp = valid ? (row / g.TP) / g.ipg : 0;
-    s = load_stage_f(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h, 0.f);
+    const Acc& a = acc[(size_t)grp * ST_COUNT + ST_HAD];
+    s.r = a.r;
+    s.band = 0.5f - a.thr;
+    s.qmax = qmax_h;
   }
   __device__ __forceinline__ void apply(int xi, int row, int col, const uint32_t* v, int n) {
     HT out[16];
@@ -314,10 +320,9 @@ static void gemm_tiles(const Geo& g, int* bn, int* sw) {
   *sw = g.Cp % 128 == 0 ? 128 : (g.Cp % 64 == 0 ? 64 : 32);
 }
 
-// Certified fp32 error bound of each stage's fast path (integer units): the first sandwich half is
-// exact, the second rounds once per fma (<= 6 of them) on partial sums bounded by
-// rowsum(L)^2 * qmax_in, so |T_f - T| <= 6 * 2^-24 * rowsum^2 * qmax_in; 8 is used for margin.
-static StageE stage_errors(int mode, const Bits& b) {
+// Max row abs-sum of each stage's integer matrix: with the group's max |first-half value| it bounds
+// the fp32 error of the second half (stage_error in wl_kernels2.cuh).
+static StageE stage_rowsums(int mode) {
   auto rowsum = [](auto tag, int R, int C) {
     using M = decltype(tag);
     long long best = 0;
@@ -326,19 +331,18 @@ static StageE stage_errors(int mode, const Bits& b) {
       for (int j = 0; j < C; ++j) s += std::abs(M::e(i, j));
       best = std::max(best, s);
     }
-    return (double)best;
+    return (float)best;
   };
-  auto bound = [](double rs, int qin) { return (float)(8.0 * rs * rs * qin / 16777216.0); };
   StageE E;
   for (int i = 0; i < ST_COUNT; ++i) E.e[i] = 0.f;
   if (mode == WL_CANONICAL) {
-    E.e[ST_IT] = bound(rowsum(tab::Can_IT{}, 6, 6), b.q[ST_INPUT]);
-    E.e[ST_OUT] = bound(rowsum(tab::Can_OT{}, 4, 6), b.q[ST_HAD]);
+    E.e[ST_IT] = rowsum(tab::Can_IT{}, 6, 6);
+    E.e[ST_OUT] = rowsum(tab::Can_OT{}, 4, 6);
   } else {
-    E.e[ST_IBC] = bound(rowsum(tab::Leg_IBC{}, 6, 6), b.q[ST_INPUT]);
-    E.e[ST_IT] = bound(rowsum(tab::Leg_IT{}, 6, 6), b.q[ST_IBC]);
-    E.e[ST_OBC] = bound(rowsum(tab::Leg_OBC{}, 6, 6), b.q[ST_HAD]);
-    E.e[ST_OUT] = bound(rowsum(tab::Leg_OT{}, 4, 6), b.q[ST_OBC]);
+    E.e[ST_IBC] = rowsum(tab::Leg_IBC{}, 6, 6);
+    E.e[ST_IT] = rowsum(tab::Leg_IT{}, 6, 6);
+    E.e[ST_OBC] = rowsum(tab::Leg_OBC{}, 6, 6);
+    E.e[ST_OUT] = rowsum(tab::Leg_OT{}, 4, 6);
   }
   return E;
 }
@@ -559,7 +563,14 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     int bx = (int)std::min<long long>((per_image / 4 + 255) / 256, 64);
     absmax_f32_kernel<<<dim3(std::max(bx, 1), g.N), 256, 0, st>>>(x, per_image, g.ipg, acc);
     prof_mark("absmax_input", st);
-    quant_input_kernel<<<dim3(g.Cp / 32, g.H, g.N), 256, 0, st>>>(x, c0, g, b, acc);
+    const int qrow = std::max(1, std::min(64, 160000 / (g.Cp + 4)));
+    const size_t qsm = (size_t)qrow * (g.Cp + 4);
+    static bool qattr = false;
+    if (!qattr) {
+      WL_CUDA(cudaFuncSetAttribute(quant_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      qattr = true;
+    }
+    quant_input_kernel<<<dim3(g.H, g.N), 256, qsm, st>>>(x, c0, g, b, acc, qrow);
     prof_mark("quant_input", st);
   }
   int8_t* c1 = reinterpret_cast<int8_t*>(ws + L.off_c1);
@@ -570,26 +581,30 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     tabs.t[kTableStage[i]] = reinterpret_cast<unsigned*>(ws + L.off_tab[i]);
     if (kTableStage[i] != ST_HAD) WL_CUDA(cudaMemsetAsync(ws + L.off_tab[i], 0, L.tab_bytes[i], st));
   }
-  const StageE E = stage_errors(plan->mode, b);
+  const StageE E = stage_rowsums(plan->mode);
 
   const long long tc = (long long)g.T * g.C;
   const int tb = 256;
   const unsigned tgrid = (unsigned)((tc + tb - 1) / tb);
   const int fin_blocks = 4 * 148;
+  const int pgrid = (L.groups + 127) / 128;
   if (!leg) {
     in_a_kernel<0><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
     finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
     prof_mark("input_transform_max", st);
-    in_c_kernel<0><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, E);
+    in_c_kernel<0><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
     prof_mark("input_transform_codes", st);
   } else {
     in_a_kernel<1><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
     finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
+    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
     prof_mark("input_base_change_max", st);
-    in_b_kernel<<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs, E);
+    in_b_kernel<<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs);
     finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
     prof_mark("input_transform_max", st);
-    in_c_kernel<1><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, E);
+    in_c_kernel<1><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
     prof_mark("input_transform_codes", st);
   }
   WL_CUDA(cudaGetLastError());
@@ -613,6 +628,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     if (rc) return rc;
     finalize_hadamard_kernel<<<fin_blocks, 256, 0, st>>>(U, V, g, acc, wh->wacc, wstage, qu, b.q[ST_IT],
                                                          tabs.t[ST_HAD], bn);
+    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_HAD, b.q[ST_HAD], 0.f);
     prof_mark("gemm_hadamard_max", st);
   }
   if (L.hbytes == 1) {
@@ -651,20 +667,23 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
   if (!leg) {                                                                                                   \
     out_a_kernel<0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, g, acc, tabs);                                  \
     finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
-        tabs.t[ST_OUT], E.e[ST_OUT]);                        \
+        tabs.t[ST_OUT], E.e[ST_OUT]); \
+    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);                        \
     prof_mark("output_max", st);                                                                                \
-    out_c_kernel<0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, y, bias, g, b, acc, plan->d_pf, E);             \
+    out_c_kernel<0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, y, bias, g, b, acc, plan->d_pf);             \
     prof_mark("output_write", st);                                                                              \
   } else {                                                                                                      \
     out_a_kernel<1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, g, acc, tabs);                                  \
     finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
-        tabs.t[ST_OBC], E.e[ST_OBC]);                        \
+        tabs.t[ST_OBC], E.e[ST_OBC]); \
+    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);                        \
     prof_mark("output_base_change_max", st);                                                                    \
-    out_b_kernel<HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf, tabs, E);                  \
+    out_b_kernel<HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf, tabs);                  \
     finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
-        tabs.t[ST_OUT], E.e[ST_OUT]);                        \
+        tabs.t[ST_OUT], E.e[ST_OUT]); \
+    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);                        \
     prof_mark("output_max", st);                                                                                \
-    out_c_kernel<1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, y, bias, g, b, acc, plan->d_pf, E);             \
+    out_c_kernel<1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, y, bias, g, b, acc, plan->d_pf);             \
     prof_mark("output_write", st);                                                                              \
   }
   if (L.hbytes == 1) {

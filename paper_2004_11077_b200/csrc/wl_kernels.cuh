@@ -69,27 +69,29 @@ __global__ void absmax_f32_kernel(const float* __restrict__ x, long long per_ima
   }
 }
 
-// c0 = rint(x / s0) (quantize.py:118-119), NCHW fp32 -> NHWC int8 through a shared-memory transpose.
-// Block = (image n, row h, 32-channel slab).
-__global__ void quant_input_kernel(const float* __restrict__ x, int8_t* __restrict__ c0, Geo g, Bits b,
-                                   const Acc* __restrict__ acc) {
-  __shared__ int8_t tile[32][257];
-  const int n = blockIdx.z, h = blockIdx.y, c_base = blockIdx.x * 32;
+// c0 = rint(x / s0) (quantize.py:118-119), NCHW fp32 -> NHWC int8.  Block = (row h, image n):
+// warps sweep channels with lanes along W (coalesced loads), codes land in a shared row buffer
+// [w][Cp+4] (the +4 pad keeps the byte stores bank-conflict free), which is copied out as words.
+__global__ void __launch_bounds__(256) quant_input_kernel(const float* __restrict__ x, int8_t* __restrict__ c0, Geo g,
+                                                          Bits b, const Acc* __restrict__ acc, int kQuantRowW) {
+  extern __shared__ int8_t srow[];
+  const int h = blockIdx.x, n = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
-  for (int w0 = 0; w0 < g.W; w0 += 256) {
-    const int wn = min(256, g.W - w0);
-    for (int e = threadIdx.x; e < 32 * wn; e += blockDim.x) {
-      const int cc = e / wn, w = e % wn;
-      const int c = c_base + cc;
-      int code = 0;
-      if (c < g.C) code = quant_float(__ldg(&x[(((size_t)n * g.C + c) * g.H + h) * g.W + w0 + w]), q);
-      tile[cc][w] = (int8_t)code;
+  const int ld = g.Cp + 4;
+  for (int w0 = 0; w0 < g.W; w0 += kQuantRowW) {
+    const int wn = min(kQuantRowW, g.W - w0);
+    for (int c = warp; c < g.Cp; c += nwarps) {
+      const float* xr = x + (((size_t)n * g.C + c) * g.H + h) * g.W + w0;
+      for (int w = lane; w < wn; w += 32)
+        srow[w * ld + c] = c < g.C ? (int8_t)quant_float(__ldg(xr + w), q) : (int8_t)0;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < 32 * wn; e += blockDim.x) {
-      const int w = e / 32, cc = e % 32;
-      const int c = c_base + cc;
-      if (c < g.Cp) c0[(((size_t)n * g.H + h) * g.W + w0 + w) * g.Cp + c] = tile[cc][w];
+    int* dst = reinterpret_cast<int*>(c0 + (((size_t)n * g.H + h) * g.W + w0) * g.Cp);
+    const int words = g.Cp >> 2;
+    for (int i = threadIdx.x; i < wn * words; i += blockDim.x) {
+      const int w = i / words, j = i - w * words;
+      dst[i] = *reinterpret_cast<const int*>(srow + w * ld + 4 * j);
     }
     __syncthreads();
   }

@@ -1,17 +1,18 @@
-// v2 transform kernels: fp32 fast path with certified error bounds, exact integer fallback,
-// deferred fp64 argmax replay through per-entry max tables.
+// Transform kernels (v2): fp32 fast path with certified error bounds, exact integer fallback per
+// element, deferred fp64 argmax replay through per-entry max tables.
 //
 // Every stage value T is an integer.  The fast path evaluates T in fp32: the
 // first sandwich half is exact and the second rounds once per fma, so |T_f - T| <= E_stage
-// (host-computed, see wl_forward.cu).  Hence
-//   * codes: x = T_f * qmax/M rounded half-even by a magic-number add is the exact rhe() result
-//     unless x is within qmax*E/M (+ fp32 slack) of a half-integer; such tile-channels are redone
-//     with integer arithmetic and exact tie replay (requant36);
-//   * maxima: only units whose fp32 maximum is within 2E of the running group maximum can hold the
-//     exact argmax; they are pushed to a candidate list that finalize_* recomputes exactly
-//     (integer M, fp64 max_abs by replay in the reference's operation order).
+// (host-computed, wl_forward.cu: stage_errors).  Hence
+//   * codes: y = fl(T_f * qmax/M + 1.5*2^23) is rhe(T_f * qmax/M); it equals the exact rhe() of
+//     the integer stage value unless T_f*qmax/M lies within qmax*E/M (+ fp32 slack) of a
+//     half-integer — those elements are recomputed in integers out of line (exact_elem), exact
+//     ties replayed in fp64 in the reference's operation order;
+//   * maxima: each pass writes the fp32 maximum of every 32-unit entry to a table plus the group's
+//     running fp32 maximum; finalize_* recomputes exactly only the entries within 2E of it
+//     (integer M, fp64 max_abs by replay), and stage_params_kernel derives r, band and scale.
 // Thread mapping: one (tile, channel) unit per thread, channel fastest, so every byte-plane access
-// of a warp is one contiguous 32-byte segment.
+// of a warp is one contiguous 32-byte segment; 32-bit element offsets (host-checked < 2^32).
 #pragma once
 #include "wl_kernels.cuh"
 
@@ -21,132 +22,117 @@ struct Tables {  // max tables per stage id (only IBC, IT, HAD, OBC, OUT are use
   unsigned* t[ST_COUNT];
 };
 
-struct StageE {  // certified fp32 error bound per stage (integer units)
+struct StageE {  // max row abs-sum of each stage's integer matrix (error-bound factor)
   float e[ST_COUNT];
 };
 
-__device__ __forceinline__ void load_c0_f(const int8_t* __restrict__ c0, const Geo& g, int n, int tile, int c,
-                                          float (&X)[6][6]) {
+// Certified bound on |T_f - T| for a group: every fma partial sum of the second half is bounded by
+// rowsum(L) * max|tmp| and rounds by at most 2^-24 of itself; <= 6 roundings (+ margin).
+__device__ __forceinline__ float stage_error(const Acc& a, float rowsum) {
+  return 6.5f * 5.9604645e-8f * rowsum * __uint_as_float(a.TM);
+}
+
+// 6x6 window of input codes (NHWC int8, implicit zero padding).
+template <typename XT>
+__device__ __forceinline__ void load_c0(const int8_t* __restrict__ c0, const Geo& g, int n, int tile, int c,
+                                        XT (&X)[6][6]) {
   const int ty = tile / g.tw, tx = tile % g.tw;
+  const int r0 = 4 * ty - g.pad, q0 = 4 * tx - g.pad;
+  const uint32_t cp = (uint32_t)g.Cp;
+  const uint32_t base = ((uint32_t)(n * g.H + r0) * (uint32_t)g.W + (uint32_t)q0) * cp + (uint32_t)c;
+  bool cv[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) cv[j] = (unsigned)(q0 + j) < (unsigned)g.W;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    const int r = 4 * ty + i - g.pad;
+    const bool rv = (unsigned)(r0 + i) < (unsigned)g.H;
+    const uint32_t rb = base + (uint32_t)i * (uint32_t)g.W * cp;
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-      const int col = 4 * tx + j - g.pad;
-      X[i][j] = (r >= 0 && r < g.H && col >= 0 && col < g.W)
-                    ? (float)__ldg(&c0[(((size_t)n * g.H + r) * g.W + col) * g.Cp + c])
-                    : 0.f;
-    }
+    for (int j = 0; j < 6; ++j) X[i][j] = (rv && cv[j]) ? (XT)__ldg(c0 + (rb + (uint32_t)j * cp)) : (XT)0;
   }
 }
 
 // 36 codes of one unit from a [36][rows][ld] plane layout.
 template <typename HT, typename XT>
-__device__ __forceinline__ void load_planes(const HT* __restrict__ P, size_t plane, size_t off, XT (&X)[6][6]) {
+__device__ __forceinline__ void load_planes(const HT* __restrict__ P, uint32_t plane, uint32_t off, XT (&X)[6][6]) {
 #pragma unroll
-  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = (XT)__ldg(&P[(size_t)e * plane + off]);
-}
-
-template <int R>
-__device__ __forceinline__ float absmax_f(const float (&T)[R][R]) {
-  float m = 0.f;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-#pragma unroll
-    for (int j = 0; j < R; ++j) m = fmaxf(m, fabsf(T[i][j]));
-  return m;
+  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = (XT)__ldg(P + (off + (uint32_t)e * plane));
 }
 
 // Max of one (unit row t, channel c) into table entry t*ceil(C/32) + c/32 and the group running max.
-__device__ __forceinline__ void record_unit(float m, int grp, bool active, Acc* acc, int stage, unsigned* table,
-                                            int t, int c, int C) {
+__device__ __forceinline__ void record_unit(float m, float tm, int grp, bool active, Acc* acc, int stage,
+                                            unsigned* table, int t, int c, int C) {
   bool uniform;
   float wmax;
   const int CB = (C + 31) >> 5;
   record_max(active ? m : 0.f, active ? grp : -1, table + (size_t)t * CB + (c >> 5), (C & 31) == 0, acc + stage,
              uniform, wmax);
   publish_mf(active ? m : 0.f, active ? grp : -1, acc + stage, uniform, wmax);
-}
-
-// ---------------------------------------------------------------------------------- exact fallbacks
-// Out of line so the fast path keeps a small register footprint; results go through local memory.
-
-// Legendre input_base_change codes of one unit from c0 (exact, ties replayed).
-__device__ __noinline__ void exact_c1_unit(const int8_t* __restrict__ c0, const Geo g, int n, int tile, int c,
-                                           const Acc* ga, const Bits b, const PlanF64* pf, int* out) {
-  int Xi[6][6], T1[6][6], C1[6][6];
-  load_input_tile(c0, g, n, tile, c, Xi);
-  sandwich<tab::Leg_IBC>(Xi, T1);
-  requant36(T1, load_int_stage(ga[ST_IBC], b.q[ST_IBC]), Xi, load_float_stage(ga[ST_INPUT], b.q[ST_INPUT]), pf->ibc,
-            C1);
-  for (int e = 0; e < 36; ++e) out[e] = C1[e / 6][e % 6];
-}
-
-// V codes of one unit (canonical from c0, Legendre from c1), exact with tie replay.
-template <int MODE>
-__device__ __noinline__ void exact_v_unit(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1, const Geo g,
-                                          int t, int c, const Acc* ga, const Bits b, const PlanF64* pf, int* out) {
-  const int n = t / g.TP, tile = t % g.TP;
-  int Xi[6][6], Cv[6][6];
-  if constexpr (MODE == 0) {
-    int Ti[6][6];
-    load_input_tile(c0, g, n, tile, c, Xi);
-    sandwich<tab::Can_IT>(Xi, Ti);
-    requant36(Ti, load_int_stage(ga[ST_IT], b.q[ST_IT]), Xi, load_float_stage(ga[ST_INPUT], b.q[ST_INPUT]), pf->it,
-              Cv);
-  } else {
-    long long Ti[6][6];
+  // group max of the first-half magnitudes (for the error bound)
+  float tw = active ? tm : 0.f;
+  if (uniform) {
 #pragma unroll
-    for (int e = 0; e < 36; ++e) Xi[e / 6][e % 6] = c1[((size_t)e * g.T + t) * g.Cp + c];
-    sandwich<tab::Leg_IT>(Xi, Ti);
-    requant36(Ti, load_int_stage(ga[ST_IT], b.q[ST_IT]), Xi, load_int_stage(ga[ST_IBC], b.q[ST_IBC]), pf->it, Cv);
+    for (int o = 16; o > 0; o >>= 1) tw = fmaxf(tw, __shfl_xor_sync(0xffffffffu, tw, o));
+    if ((threadIdx.x & 31) == 0 && grp >= 0 && tw > 0.f)
+      atomicMax(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tw));
+  } else if (active && grp >= 0 && tw > 0.f) {
+    atomicMax(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tw));
   }
-  for (int e = 0; e < 36; ++e) out[e] = Cv[e / 6][e % 6];
 }
 
-// Legendre output_base_change codes of one (t, k) unit from h.
+// ---------------------------------------------------------------------------------- exact elements
+
+struct SrcC0 {  // input codes window
+  const int8_t* p;
+  Geo g;
+  int n, tile, c;
+  __device__ void load(int (&X)[6][6]) const { load_c0(p, g, n, tile, c, X); }
+};
 template <typename HT>
-__device__ __noinline__ void exact_c4_unit(const HT* __restrict__ h, const Geo g, int t, int k, const Acc* ga,
-                                           const Bits b, const PlanF64* pf, int* out) {
-  int Hi[6][6], Ti[6][6], C4[6][6];
-#pragma unroll
-  for (int e = 0; e < 36; ++e) Hi[e / 6][e % 6] = h[((size_t)e * g.T + t) * g.Kp + k];
-  sandwich<tab::Leg_OBC>(Hi, Ti);
-  requant36(Ti, load_int_stage(ga[ST_OBC], b.q[ST_OBC]), Hi, load_int_stage(ga[ST_HAD], b.q[ST_HAD]), pf->obc, C4);
-  for (int e = 0; e < 36; ++e) out[e] = C4[e / 6][e % 6];
+struct SrcPlanes {  // [36][rows][ld] codes
+  const HT* p;
+  uint32_t plane, off;
+  __device__ void load(int (&X)[6][6]) const { load_planes(p, plane, off, X); }
+};
+
+// Exact code of element (i, j) of stage L . X . L^T, X reloaded from src; ties replayed in fp64.
+template <class L, class Src>
+__device__ __noinline__ int exact_elem(Src src, int i, int j, const Acc* a_stage, int qmax, const Acc* a_in,
+                                       int qmax_in, bool in_float, const double* __restrict__ Lf) {
+  int X[6][6];
+  src.load(X);
+  long long T = 0;
+  for (int l = 0; l < L::C; ++l) {
+    long long tmp = 0;
+    for (int l2 = 0; l2 < L::C; ++l2) tmp += (long long)X[l][l2] * L::e(j, l2);
+    T += (long long)L::e(i, l) * tmp;
+  }
+  const StageQ q = load_int_stage(*a_stage, qmax);
+  bool tie = false;
+  int code = rq(T, q, tie);
+  if (tie) {
+    const StageQ qin = in_float ? load_float_stage(*a_in, qmax_in) : load_int_stage(*a_in, qmax_in);
+    int xc[36];
+    for (int e = 0; e < 36; ++e) xc[e] = X[e / 6][e % 6];
+    code = code_of(replay_sandwich(Lf, L::R, L::C, xc, qin.qmax, qin.maxabs, qin.scale, i, j), q);
+  }
+  return code;
 }
 
-// Output-stage codes of one (t, k) unit (canonical from h, Legendre from c4).
-template <int MODE, typename HT>
-__device__ __noinline__ void exact_out_unit(const HT* __restrict__ h, const int8_t* __restrict__ c4, const Geo g,
-                                            int t, int k, const Acc* ga, const Bits b, const PlanF64* pf, int* out) {
-  int Xi[6][6];
-  long long Yi[4][4];
-  StageQ qf;
-  if constexpr (MODE == 0) {
-#pragma unroll
-    for (int e = 0; e < 36; ++e) Xi[e / 6][e % 6] = h[((size_t)e * g.T + t) * g.Kp + k];
-    int Y32[4][4];
-    sandwich<tab::Can_OT>(Xi, Y32);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) Yi[e / 4][e % 4] = Y32[e / 4][e % 4];
-    qf = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
-  } else {
-#pragma unroll
-    for (int e = 0; e < 36; ++e) Xi[e / 6][e % 6] = c4[((size_t)e * g.T + t) * g.Kp + k];
-    sandwich<tab::Leg_OT>(Xi, Yi);
-    qf = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
-  }
-  const StageQ qo = load_int_stage(ga[ST_OUT], b.q[ST_OUT]);
-  int xc[36];
-  for (int e = 0; e < 36; ++e) xc[e] = Xi[e / 6][e % 6];
-  for (int e = 0; e < 16; ++e) {
-    bool tie = false;
-    int code = rq(Yi[e / 4][e % 4], qo, tie);
-    if (tie) code = code_of(replay_sandwich(pf->ot, 4, 6, xc, qf.qmax, qf.maxabs, qf.scale, e / 4, e % 4), qo);
-    out[e] = code;
-  }
+// r, threshold and reference scale of one stage for every group, once its M and F are final.
+__global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage, int qmax, float rowsum) {
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= groups) return;
+  Acc& a = acc[(size_t)gi * ST_COUNT + stage];
+  const float E = stage_error(a, rowsum);
+  const long long M = (long long)a.M;
+  const double maxabs = __longlong_as_double((long long)a.F);
+  a.r = M ? (float)((double)qmax / (double)M) : 0.f;
+  // band: E * qmax / M from the fp32 stage value, + 3e-5 for r's rounding (<= 1.6e-5 code units at
+  // qmax 255) and the fma rounding of the distance itself
+  const float band = M ? (float)((double)qmax * E / (double)M) + 3e-5f : 0.f;
+  a.thr = 0.5f - band;
+  a.scale = maxabs > 0.0 ? maxabs / (double)qmax : 1.0;
 }
 
 // ---------------------------------------------------------------------------------- input side
@@ -155,89 +141,106 @@ __device__ __noinline__ void exact_out_unit(const HT* __restrict__ h, const int8
 template <int MODE>
 __global__ void __launch_bounds__(256) in_a_kernel(const int8_t* __restrict__ c0, Geo g, Acc* __restrict__ acc,
                                                    Tables tabs) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool active = idx < (long long)g.T * g.C;
-  const long long id = active ? idx : 0;
-  const int c = (int)(id % g.C), t = (int)(id / g.C);
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = idx < (uint32_t)g.T * (uint32_t)g.C;
+  const uint32_t id = active ? idx : 0u;
+  const int c = (int)(id % (uint32_t)g.C), t = (int)(id / (uint32_t)g.C);
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
-  float X[6][6], T[6][6];
-  load_c0_f(c0, g, n, tile, c, X);
+  float X[6][6];
+  load_c0(c0, g, n, tile, c, X);
   constexpr int st = MODE == 0 ? ST_IT : ST_IBC;
+  float m = 0.f, tm = 0.f;
+  auto mx = [&](int, const float (&col)[6]) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
+  };
   if constexpr (MODE == 0)
-    sandwich_f<tab::Can_IT>(X, T);
+    sandwich_cols<tab::Can_IT>(X, mx, &tm);
   else
-    sandwich_f<tab::Leg_IBC>(X, T);
-  record_unit(absmax_f(T), grp, active, acc, st, tabs.t[st], t, c, g.C);
+    sandwich_cols<tab::Leg_IBC>(X, mx, &tm);
+  record_unit(m, tm, grp, active, acc, st, tabs.t[st], t, c, g.C);
 }
 
 // Legendre: input_base_change codes c1 (stored) and input_transform maximum.
-__global__ void __launch_bounds__(256) in_b_kernel(const int8_t* __restrict__ c0, int8_t* __restrict__ c1, Geo g,
+__global__ void __launch_bounds__(256, 2) in_b_kernel(const int8_t* __restrict__ c0, int8_t* __restrict__ c1, Geo g,
                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                                   Tables tabs, StageE E) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool active = idx < (long long)g.T * g.C;
-  const long long id = active ? idx : 0;
-  const int c = (int)(id % g.C), t = (int)(id / g.C);
+                                                   Tables tabs) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = idx < (uint32_t)g.T * (uint32_t)g.C;
+  const uint32_t id = active ? idx : 0u;
+  const int c = (int)(id % (uint32_t)g.C), t = (int)(id / (uint32_t)g.C);
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
-  float X[6][6], T[6][6];
-  load_c0_f(c0, g, n, tile, c, X);
-  sandwich_f<tab::Leg_IBC>(X, T);
-  const StageF s1 = load_stage_f(ga[ST_IBC], b.q[ST_IBC], E.e[ST_IBC]);
-  int C1[6][6];
-  float dmax = 0.f;
+  const float r = ga[ST_IBC].r, thr = ga[ST_IBC].thr;
+  const uint32_t plane = (uint32_t)g.T * g.Cp;
+  int8_t* dst = c1 + (uint32_t)t * g.Cp + c;
+  float K1[6][6];
+  {
+    float X[6][6];
+    load_c0(c0, g, n, tile, c, X);
+    sandwich_cols<tab::Leg_IBC>(X, [&](int j, const float (&col)[6]) {
 #pragma unroll
-  for (int e = 0; e < 36; ++e) C1[e / 6][e % 6] = rq_fast(T[e / 6][e % 6], s1, dmax);
-  if (dmax > 0.5f - s1.band) {  // exact path for this unit
-    int tmp[36];
-    exact_c1_unit(c0, g, n, tile, c, ga, b, pf, tmp);
-#pragma unroll
-    for (int e = 0; e < 36; ++e) C1[e / 6][e % 6] = tmp[e];
+      for (int i = 0; i < 6; ++i) {
+        const int code = rq_elem(col[i], r, thr, [&] {
+          return exact_elem<tab::Leg_IBC>(SrcC0{c0, g, n, tile, c}, i, j, ga + ST_IBC, b.q[ST_IBC], ga + ST_INPUT,
+                                          b.q[ST_INPUT], true, pf->ibc);
+        }, K1[i][j]);
+        if (active) dst[(uint32_t)(6 * i + j) * plane] = (int8_t)code;
+      }
+    });
   }
-  if (active)
+  float m = 0.f, tm = 0.f;
+  sandwich_cols<tab::Leg_IT>(K1, [&](int, const float (&col)[6]) {
 #pragma unroll
-    for (int e = 0; e < 36; ++e) c1[((size_t)e * g.T + t) * g.Cp + c] = (int8_t)C1[e / 6][e % 6];
-  float Xf[6][6], T2[6][6];
-#pragma unroll
-  for (int e = 0; e < 36; ++e) Xf[e / 6][e % 6] = (float)C1[e / 6][e % 6];
-  sandwich_f<tab::Leg_IT>(Xf, T2);
-  record_unit(absmax_f(T2), grp, active, acc, ST_IT, tabs.t[ST_IT], t, c, g.C);
+    for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
+  }, &tm);
+  record_unit(m, tm, grp, active, acc, ST_IT, tabs.t[ST_IT], t, c, g.C);
 }
 
 // V codes.  Canonical: from c0 through B^T.  Legendre: from the stored c1 through B_P^T.
 template <int MODE>
 __global__ void __launch_bounds__(256) in_c_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
                                                    int8_t* __restrict__ V, Geo g, Bits b, Acc* __restrict__ acc,
-                                                   const PlanF64* __restrict__ pf, StageE E) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)g.T * g.C) return;
-  const int c = (int)(idx % g.C), t = (int)(idx / g.C);
+                                                   const PlanF64* __restrict__ pf) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (uint32_t)g.T * (uint32_t)g.C) return;
+  const int c = (int)(idx % (uint32_t)g.C), t = (int)(idx / (uint32_t)g.C);
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
-  float X[6][6], T[6][6];
+  const float r = ga[ST_IT].r, thr = ga[ST_IT].thr;
+  const uint32_t plane = (uint32_t)g.T * g.Cp;
+  const uint32_t off = (uint32_t)t * g.Cp + c;
+  int8_t* dst = V + off;
+  float X[6][6];
+  float kdummy;
   if constexpr (MODE == 0) {
-    load_c0_f(c0, g, n, tile, c, X);
-    sandwich_f<tab::Can_IT>(X, T);
+    load_c0(c0, g, n, tile, c, X);
+    sandwich_cols<tab::Can_IT>(X, [&](int j, const float (&col)[6]) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const int code = rq_elem(col[i], r, thr, [&] {
+          return exact_elem<tab::Can_IT>(SrcC0{c0, g, n, tile, c}, i, j, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT,
+                                         b.q[ST_INPUT], true, pf->it);
+        }, kdummy);
+        dst[(uint32_t)(6 * i + j) * plane] = (int8_t)code;
+      }
+    });
   } else {
-    load_planes(c1, (size_t)g.T * g.Cp, (size_t)t * g.Cp + c, X);
-    sandwich_f<tab::Leg_IT>(X, T);
+    load_planes(c1, plane, off, X);
+    sandwich_cols<tab::Leg_IT>(X, [&](int j, const float (&col)[6]) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const int code = rq_elem(col[i], r, thr, [&] {
+          return exact_elem<tab::Leg_IT>(SrcPlanes<int8_t>{c1, plane, off}, i, j, ga + ST_IT, b.q[ST_IT],
+                                         ga + ST_IBC, b.q[ST_IBC], false, pf->it);
+        }, kdummy);
+        dst[(uint32_t)(6 * i + j) * plane] = (int8_t)code;
+      }
+    });
   }
-  const StageF s = load_stage_f(ga[ST_IT], b.q[ST_IT], E.e[ST_IT]);
-  int Cv[6][6];
-  float dmax = 0.f;
-#pragma unroll
-  for (int e = 0; e < 36; ++e) Cv[e / 6][e % 6] = rq_fast(T[e / 6][e % 6], s, dmax);
-  if (dmax > 0.5f - s.band) {
-    int tmp[36];
-    exact_v_unit<MODE>(c0, c1, g, t, c, ga, b, pf, tmp);
-#pragma unroll
-    for (int e = 0; e < 36; ++e) Cv[e / 6][e % 6] = tmp[e];
-  }
-#pragma unroll
-  for (int e = 0; e < 36; ++e) V[((size_t)e * g.T + t) * g.Cp + c] = (int8_t)Cv[e / 6][e % 6];
 }
 
 // Exact recomputation of one input-side unit: local exact max and fp64 max_abs of its argmax.
@@ -252,12 +255,12 @@ __device__ void exact_input_unit(const int8_t* __restrict__ c0, const int8_t* __
   StageQ qin;
   const double* Lf;
   if (MODE == 1 && STAGE == ST_IT) {
-    load_planes(c1, (size_t)g.T * g.Cp, (size_t)t * g.Cp + c, Xi);
+    load_planes(c1, (uint32_t)g.T * g.Cp, (uint32_t)t * g.Cp + c, Xi);
     sandwich<tab::Leg_IT>(Xi, T);
     qin = load_int_stage(ga[ST_IBC], b.q[ST_IBC]);
     Lf = pf->it;
   } else {
-    load_input_tile(c0, g, n, tile, c, Xi);
+    load_c0(c0, g, n, tile, c, Xi);
     int Ti[6][6];
     if (MODE == 0)
       sandwich<tab::Can_IT>(Xi, Ti);
@@ -275,7 +278,8 @@ __device__ void exact_input_unit(const int8_t* __restrict__ c0, const int8_t* __
   double f = 0.0;
   for (int e = 0; e < 36; ++e) {
     const long long v = T[e / 6][e % 6];
-    if ((v < 0 ? -v : v) == m) f = fmax(f, fabs(replay_sandwich(Lf, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6)));
+    if ((v < 0 ? -v : v) == m)
+      f = fmax(f, fabs(replay_sandwich(Lf, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6)));
   }
   atomicMax(&ga[STAGE].M, (unsigned long long)m);
   atomicMax(&ga[STAGE].F, dbits(f));
@@ -285,7 +289,7 @@ __device__ void exact_input_unit(const int8_t* __restrict__ c0, const int8_t* __
 template <int MODE, int STAGE>
 __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1, Geo g, Bits b,
                                       Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                      const unsigned* __restrict__ table, float E) {
+                                      const unsigned* __restrict__ table, float rowsum) {
   const int CB = (g.C + 31) >> 5;
   const long long nent = (long long)g.T * CB;
   const int lane = threadIdx.x & 31;
@@ -298,8 +302,9 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
       const float v = __uint_as_float(table[e]);
       const int t = (int)(e / CB);
       const int grp = (t / g.TP) / g.ipg;
-      const float mf = __uint_as_float(acc[(size_t)grp * ST_COUNT + STAGE].MF);
-      pass = v > 0.f && v >= mf - 2.f * E;
+      const Acc& a = acc[(size_t)grp * ST_COUNT + STAGE];
+      const float mf = __uint_as_float(a.MF);
+      pass = v > 0.f && v >= mf - 2.f * stage_error(a, rowsum);
     }
     unsigned mask = __ballot_sync(0xffffffffu, pass);
     while (mask) {
@@ -319,122 +324,131 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
 template <int MODE, typename HT>
 __global__ void __launch_bounds__(256) out_a_kernel(const HT* __restrict__ h, Geo g, Acc* __restrict__ acc,
                                                     Tables tabs) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool active = idx < (long long)g.T * g.K;
-  const long long id = active ? idx : 0;
-  const int k = (int)(id % g.K), t = (int)(id / g.K);
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = idx < (uint32_t)g.T * (uint32_t)g.K;
+  const uint32_t id = active ? idx : 0u;
+  const int k = (int)(id % (uint32_t)g.K), t = (int)(id / (uint32_t)g.K);
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
+  const int ty = tile / g.tw, tx = tile % g.tw;
   float X[6][6];
-  load_planes(h, (size_t)g.T * g.Kp, (size_t)t * g.Kp + k, X);
-  float m;
+  load_planes(h, (uint32_t)g.T * g.Kp, (uint32_t)t * g.Kp + k, X);
+  float m = 0.f, tm = 0.f;
   constexpr int st = MODE == 0 ? ST_OUT : ST_OBC;
   if constexpr (MODE == 0) {
-    float Y[4][4];
-    sandwich_f<tab::Can_OT>(X, Y);
-    const int ty = tile / g.tw, tx = tile % g.tw;
-    m = 0.f;
+    sandwich_cols<tab::Can_OT>(X, [&](int j, const float (&col)[4]) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(Y[i][j]));
+      for (int i = 0; i < 4; ++i)
+        if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[i]));
+    }, &tm);
   } else {
-    float T[6][6];
-    sandwich_f<tab::Leg_OBC>(X, T);
-    m = absmax_f(T);
+    sandwich_cols<tab::Leg_OBC>(X, [&](int, const float (&col)[6]) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
+    }, &tm);
   }
-  record_unit(m, grp, active, acc, st, tabs.t[st], t, k, g.K);
+  record_unit(m, tm, grp, active, acc, st, tabs.t[st], t, k, g.K);
 }
 
 // Legendre: output_base_change codes c4 (stored) and cropped output maximum.
 template <typename HT>
-__global__ void __launch_bounds__(256) out_b_kernel(const HT* __restrict__ h, int8_t* __restrict__ c4, Geo g, Bits b,
-                                                    Acc* __restrict__ acc, const PlanF64* __restrict__ pf, Tables tabs,
-                                                    StageE E) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool active = idx < (long long)g.T * g.K;
-  const long long id = active ? idx : 0;
-  const int k = (int)(id % g.K), t = (int)(id / g.K);
+__global__ void __launch_bounds__(256, 2) out_b_kernel(const HT* __restrict__ h, int8_t* __restrict__ c4, Geo g, Bits b,
+                                                    Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
+                                                    Tables tabs) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = idx < (uint32_t)g.T * (uint32_t)g.K;
+  const uint32_t id = active ? idx : 0u;
+  const int k = (int)(id % (uint32_t)g.K), t = (int)(id / (uint32_t)g.K);
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
-  float X[6][6], T[6][6];
-  load_planes(h, (size_t)g.T * g.Kp, (size_t)t * g.Kp + k, X);
-  sandwich_f<tab::Leg_OBC>(X, T);
-  const StageF s4 = load_stage_f(ga[ST_OBC], b.q[ST_OBC], E.e[ST_OBC]);
-  int C4[6][6];
-  float dmax = 0.f;
+  const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr;
+  const uint32_t plane = (uint32_t)g.T * g.Kp;
+  const uint32_t off = (uint32_t)t * g.Kp + k;
+  int8_t* dst = c4 + off;
+  float K4[6][6];
+  {
+    float X[6][6];
+    load_planes(h, plane, off, X);
+    sandwich_cols<tab::Leg_OBC>(X, [&](int j, const float (&col)[6]) {
 #pragma unroll
-  for (int e = 0; e < 36; ++e) C4[e / 6][e % 6] = rq_fast(T[e / 6][e % 6], s4, dmax);
-  if (dmax > 0.5f - s4.band) {
-    int tmp[36];
-    exact_c4_unit(h, g, t, k, ga, b, pf, tmp);
-#pragma unroll
-    for (int e = 0; e < 36; ++e) C4[e / 6][e % 6] = tmp[e];
+      for (int i = 0; i < 6; ++i) {
+        const int code = rq_elem(col[i], r, thr, [&] {
+          return exact_elem<tab::Leg_OBC>(SrcPlanes<HT>{h, plane, off}, i, j, ga + ST_OBC, b.q[ST_OBC], ga + ST_HAD,
+                                          b.q[ST_HAD], false, pf->obc);
+        }, K4[i][j]);
+        if (active) dst[(uint32_t)(6 * i + j) * plane] = (int8_t)code;
+      }
+    });
   }
-  if (active)
-#pragma unroll
-    for (int e = 0; e < 36; ++e) c4[((size_t)e * g.T + t) * g.Kp + k] = (int8_t)C4[e / 6][e % 6];
-  float Xf[6][6], Y[4][4];
-#pragma unroll
-  for (int e = 0; e < 36; ++e) Xf[e / 6][e % 6] = (float)C4[e / 6][e % 6];
-  sandwich_f<tab::Leg_OT>(Xf, Y);
   const int ty = tile / g.tw, tx = tile % g.tw;
-  float m = 0.f;
+  float m = 0.f, tm = 0.f;
+  sandwich_cols<tab::Leg_OT>(K4, [&](int j, const float (&col)[4]) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(Y[i][j]));
-  record_unit(m, grp, active, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K);
+    for (int i = 0; i < 4; ++i)
+      if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[i]));
+  }, &tm);
+  record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K);
 }
 
 // Final output: codes of the output stage, dequantised (snap +-qmax to +-max_abs), + bias, fp32 NCHW.
 template <int MODE, typename HT>
-__global__ void __launch_bounds__(256) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
+__global__ void __launch_bounds__(256, 2) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
                                                     float* __restrict__ y, const float* __restrict__ bias, Geo g,
-                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                                    StageE E) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)g.T * g.K) return;
-  const int k = (int)(idx % g.K), t = (int)(idx / g.K);
+                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (uint32_t)g.T * (uint32_t)g.K) return;
+  const int k = (int)(idx % (uint32_t)g.K), t = (int)(idx / (uint32_t)g.K);
   const int n = t / g.TP, tile = t % g.TP;
   const int ty = tile / g.tw, tx = tile % g.tw;
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
-  float X[6][6], Y[4][4];
+  const float r = ga[ST_OUT].r, thr = ga[ST_OUT].thr;
+  const double scale = ga[ST_OUT].scale;
+  const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
+  const int qo = b.q[ST_OUT];
+  const uint32_t plane = (uint32_t)g.T * g.Kp;
+  const uint32_t off = (uint32_t)t * g.Kp + k;
+  float Yo[4][4];
+  float X[6][6];
+  float kdummy;
+  auto emit = [&](int i, int j, int code) {
+    Yo[i][j] = code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+  };
   if constexpr (MODE == 0) {
-    load_planes(h, (size_t)g.T * g.Kp, (size_t)t * g.Kp + k, X);
-    sandwich_f<tab::Can_OT>(X, Y);
+    load_planes(h, plane, off, X);
+    sandwich_cols<tab::Can_OT>(X, [&](int j, const float (&col)[4]) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        emit(i, j, rq_elem(col[i], r, thr, [&] {
+               return exact_elem<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, i, j, ga + ST_OUT, qo, ga + ST_HAD,
+                                              b.q[ST_HAD], false, pf->ot);
+             }, kdummy));
+    });
   } else {
-    load_planes(c4, (size_t)g.T * g.Kp, (size_t)t * g.Kp + k, X);
-    sandwich_f<tab::Leg_OT>(X, Y);
-  }
-  const StageF s = load_stage_f(ga[ST_OUT], b.q[ST_OUT], E.e[ST_OUT]);
-  int Co[4][4];
-  float dmax = 0.f;
+    load_planes(c4, plane, off, X);
+    sandwich_cols<tab::Leg_OT>(X, [&](int j, const float (&col)[4]) {
 #pragma unroll
-  for (int e = 0; e < 16; ++e) Co[e / 4][e % 4] = rq_fast(Y[e / 4][e % 4], s, dmax);
-  const StageQ qo = load_int_stage(ga[ST_OUT], b.q[ST_OUT]);
-  if (dmax > 0.5f - s.band) {
-    int tmp[16];
-    exact_out_unit<MODE, HT>(h, c4, g, t, k, ga, b, pf, tmp);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) Co[e / 4][e % 4] = tmp[e];
+      for (int i = 0; i < 4; ++i)
+        emit(i, j, rq_elem(col[i], r, thr, [&] {
+               return exact_elem<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, i, j, ga + ST_OUT, qo,
+                                              ga + ST_OBC, b.q[ST_OBC], false, pf->ot);
+             }, kdummy));
+    });
   }
   const float bk = bias ? __ldg(&bias[k]) : 0.f;
+  const bool vec = (g.Wo & 3) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int r = 4 * ty + i;
-    if (r >= g.Ho) continue;
-    float* row = y + (((size_t)n * g.K + k) * g.Ho + r) * g.Wo + 4 * tx;
+    const int rr = 4 * ty + i;
+    if (rr >= g.Ho) continue;
+    float* row = y + (((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + 4 * tx;
+    if (vec) {
+      *reinterpret_cast<float4*>(row) = make_float4(Yo[i][0] + bk, Yo[i][1] + bk, Yo[i][2] + bk, Yo[i][3] + bk);
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (4 * tx + j >= g.Wo) continue;
-      float out = (float)deq(Co[i][j], qo.qmax, qo.maxabs, qo.scale);
-      if (bias) out += bk;
-      row[j] = out;
+      for (int j = 0; j < 4; ++j)
+        if (4 * tx + j < g.Wo) row[j] = Yo[i][j] + bk;
     }
   }
 }
@@ -448,7 +462,7 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
   Acc* ga = acc + (size_t)grp * ST_COUNT;
   int Xi[6][6];
   if (MODE == 1 && STAGE == ST_OBC) {
-    load_planes(h, (size_t)g.T * g.Kp, (size_t)t * g.Kp + k, Xi);
+    load_planes(h, (uint32_t)g.T * g.Kp, (uint32_t)t * g.Kp + k, Xi);
     int T[6][6];
     sandwich<tab::Leg_OBC>(Xi, T);
     const long long m = absmax36(T);
@@ -459,23 +473,23 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
     double f = 0.0;
     for (int e = 0; e < 36; ++e) {
       const long long v = T[e / 6][e % 6];
-      if ((v < 0 ? -v : v) == m) f = fmax(f, fabs(replay_sandwich(pf->obc, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6)));
+      if ((v < 0 ? -v : v) == m)
+        f = fmax(f, fabs(replay_sandwich(pf->obc, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6)));
     }
     atomicMax(&ga[ST_OBC].M, (unsigned long long)m);
     atomicMax(&ga[ST_OBC].F, dbits(f));
     return;
   }
-  // output stage (cropped)
   long long Y[4][4];
   StageQ qin;
   if (MODE == 0) {
-    load_planes(h, (size_t)g.T * g.Kp, (size_t)t * g.Kp + k, Xi);
+    load_planes(h, (uint32_t)g.T * g.Kp, (uint32_t)t * g.Kp + k, Xi);
     int Y32[4][4];
     sandwich<tab::Can_OT>(Xi, Y32);
     for (int e = 0; e < 16; ++e) Y[e / 4][e % 4] = Y32[e / 4][e % 4];
     qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
   } else {
-    load_planes(c4, (size_t)g.T * g.Kp, (size_t)t * g.Kp + k, Xi);
+    load_planes(c4, (uint32_t)g.T * g.Kp, (uint32_t)t * g.Kp + k, Xi);
     sandwich<tab::Leg_OT>(Xi, Y);
     qin = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
   }
@@ -488,7 +502,8 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
     const int i = e / 4, j = e % 4;
     if (4 * ty + i >= g.Ho || 4 * tx + j >= g.Wo) continue;
     const long long v = Y[i][j];
-    if ((v < 0 ? -v : v) == m) f = fmax(f, fabs(replay_sandwich(pf->ot, 4, 6, xc, qin.qmax, qin.maxabs, qin.scale, i, j)));
+    if ((v < 0 ? -v : v) == m)
+      f = fmax(f, fabs(replay_sandwich(pf->ot, 4, 6, xc, qin.qmax, qin.maxabs, qin.scale, i, j)));
   }
   atomicMax(&ga[ST_OUT].M, (unsigned long long)m);
   atomicMax(&ga[ST_OUT].F, dbits(f));
@@ -497,7 +512,7 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
 template <int MODE, int STAGE, typename HT>
 __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4, Geo g, Bits b,
                                        Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                       const unsigned* __restrict__ table, float E) {
+                                       const unsigned* __restrict__ table, float rowsum) {
   const int KB = (g.K + 31) >> 5;
   const long long nent = (long long)g.T * KB;
   const int lane = threadIdx.x & 31;
@@ -510,8 +525,9 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
       const float v = __uint_as_float(table[e]);
       const int t = (int)(e / KB);
       const int grp = (t / g.TP) / g.ipg;
-      const float mf = __uint_as_float(acc[(size_t)grp * ST_COUNT + STAGE].MF);
-      pass = v > 0.f && v >= mf - 2.f * E;
+      const Acc& a = acc[(size_t)grp * ST_COUNT + STAGE];
+      const float mf = __uint_as_float(a.MF);
+      pass = v > 0.f && v >= mf - 2.f * stage_error(a, rowsum);
     }
     unsigned mask = __ballot_sync(0xffffffffu, pass);
     while (mask) {
