@@ -1,9 +1,10 @@
 // Winograd-domain channel contraction (reference: _kernels.py:94-105 `_hadamard_accumulate_nb`,
 // called from pipeline.py:143-145) as 36 batched int8 tensor-core GEMMs on sm_100a:
 //
-//     I[xi][t][o] = sum_c V[xi][t][c] * U[xi][o][c]        xi in 0..35, exact int32
+//     I[xi][t][o] = sum_c V[t][xi][c] * U[o][xi][c]        xi in 0..35, exact int32
 //
-// V (input-transform codes) and U (weight-transform codes) are int8, K-major ([rows][Cpad]).
+// V (input-transform codes, [T][36][Cp]) and U (weight-transform codes, [Kp][36][Cp]) are int8,
+// K-major; the TMA maps view them as 3-D {c, xi, row} with boxes {SW, 1, rows}.
 // One CTA computes a 128 x BN tile of one xi with tcgen05.mma kind::i8 (M=128, N=BN, K=32 per
 // instruction), operands staged by TMA into 128/64/32-byte-swizzled shared memory through a
 // STAGES-deep mbarrier ring, accumulator in TMEM.  Warp roles: w0 TMA producer, w1 TMEM owner +
@@ -68,8 +69,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t ph = (kb / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], L::kA + L::kB);
-        tma_load_3d(sA + s * L::kA, &tmA, &full[s], kb * SW, m0, xi);
-        tma_load_3d(sB + s * L::kB, &tmB, &full[s], kb * SW, n0, xi);
+        tma_load_3d(sA + s * L::kA, &tmA, &full[s], kb * SW, xi, m0);
+        tma_load_3d(sB + s * L::kB, &tmB, &full[s], kb * SW, xi, n0);
       }
     }
     __syncwarp();

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "../../include/winoleg_b200.h"
 #include "gemm_i8.cuh"
@@ -39,6 +40,11 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+int pow2_at_least(int v, int lo) {
+  int p = lo;
+  while (p < v) p <<= 1;
+  return p;
+}
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 }  // namespace
@@ -155,11 +161,11 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   g.tw = (g.Wo + 3) / 4;
   g.TP = g.th * g.tw;
   g.T = g.N * g.TP;
-  g.Cp = round_up(g.C, 32);
-  g.Kp = g.K <= 64 ? 64 : (g.K <= 128 ? 128 : round_up(g.K, 256));
+  g.Cp = pow2_at_least(g.C, 32);
+  g.Kp = pow2_at_least(g.K, 64);
   g.ipg = s->images_per_group;
   if ((unsigned long long)g.T * std::max(g.Cp, g.Kp) * 36 >= (1ULL << 32) ||
-      (unsigned long long)g.N * g.H * g.W * g.Cp >= (1ULL << 32) || g.Cp > 4096 || g.Kp > 4096)
+      (unsigned long long)g.N * g.H * g.W * g.Cp >= (1ULL << 32) || g.Cp > 512 || g.Kp > 512)
     return fail(WL_ERR_ARG, "problem too large for one call (split the batch; per-image scale groups are "
                             "independent)");
   L->groups = g.N / g.ipg;
@@ -196,9 +202,34 @@ struct WeightHeader {
 };
 
 static size_t weight_cache_bytes(int K, int C, int* Kp, int* Cp) {
-  *Cp = round_up(C, 32);
-  *Kp = K <= 64 ? 64 : (K <= 128 ? 128 : round_up(K, 256));
+  *Cp = pow2_at_least(C, 32);
+  *Kp = pow2_at_least(K, 64);
   return align256(sizeof(WeightHeader)) + (size_t)36 * (*Kp) * (*Cp);
+}
+
+// ------------------------------------------------------------------ compile-time strides
+template <int V>
+using IntC = std::integral_constant<int, V>;
+template <class F>
+static int dispatch_ld_in(int ld, F&& f) {
+  switch (ld) {
+    case 32: f(IntC<32>{}); return WL_OK;
+    case 64: f(IntC<64>{}); return WL_OK;
+    case 128: f(IntC<128>{}); return WL_OK;
+    case 256: f(IntC<256>{}); return WL_OK;
+    case 512: f(IntC<512>{}); return WL_OK;
+  }
+  return fail(WL_ERR_ARG, "unsupported padded channel count %d", ld);
+}
+template <class F>
+static int dispatch_ld_out(int ld, F&& f) {
+  switch (ld) {
+    case 64: f(IntC<64>{}); return WL_OK;
+    case 128: f(IntC<128>{}); return WL_OK;
+    case 256: f(IntC<256>{}); return WL_OK;
+    case 512: f(IntC<512>{}); return WL_OK;
+  }
+  return fail(WL_ERR_ARG, "unsupported padded output-channel count %d", ld);
 }
 
 // ------------------------------------------------------------------ GEMM epilogues
@@ -272,13 +303,13 @@ struct EpiHadRq {
         if (tie && j < n) {
           const StageQ qu = load_int_stage(wacc[wstage], qmax_u);
           const StageQ qv = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_IT], qmax_v);
-          code = code_of(replay_hadamard(U + ((size_t)xi * g.Kp + col + j) * g.Cp,
-                                         V + ((size_t)xi * g.T + row) * g.Cp, g.C, qu, qv), q);
+          code = code_of(replay_hadamard(U + ((size_t)(col + j) * 36 + xi) * g.Cp,
+                                         V + ((size_t)row * 36 + xi) * g.Cp, g.C, qu, qv), q);
         }
         out[j] = (HT)code;
       }
     }
-    HT* dst = h + ((size_t)xi * g.T + row) * g.Kp + col;
+    HT* dst = h + ((size_t)row * 36 + xi) * g.Kp + col;
     if (sizeof(HT) == 1) {
       *reinterpret_cast<int4*>(dst) = *reinterpret_cast<const int4*>(out);
     } else {
@@ -588,33 +619,37 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
   const unsigned tgrid = (unsigned)((tc + tb - 1) / tb);
   const int fin_blocks = 4 * 148;
   const int pgrid = (L.groups + 127) / 128;
-  if (!leg) {
-    in_a_kernel<0><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
-    finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
-    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
-    prof_mark("input_transform_max", st);
-    in_c_kernel<0><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
-    prof_mark("input_transform_codes", st);
-  } else {
-    in_a_kernel<1><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
-    finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
-    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
-    prof_mark("input_base_change_max", st);
-    in_b_kernel<<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs);
-    finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
-    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
-    prof_mark("input_transform_max", st);
-    in_c_kernel<1><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
-    prof_mark("input_transform_codes", st);
-  }
+  rc = dispatch_ld_in(g.Cp, [&](auto ldc) {
+    constexpr int LD = decltype(ldc)::value;
+    if (!leg) {
+      in_a_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
+      finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+      prof_mark("input_transform_max", st);
+      in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+      prof_mark("input_transform_codes", st);
+    } else {
+      in_a_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
+      finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
+      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
+      prof_mark("input_base_change_max", st);
+      in_b_kernel<LD><<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs);
+      finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+      prof_mark("input_transform_max", st);
+      in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+      prof_mark("input_transform_codes", st);
+    }
+  });
+  if (rc) return rc;
   WL_CUDA(cudaGetLastError());
   // padded channels of V must be zero for the GEMM: the stage kernels only write c < C
-  if (g.Cp != g.C) WL_CUDA(cudaMemset2DAsync(V + g.C, g.Cp, 0, g.Cp - g.C, (size_t)36 * g.T, st));
+  if (g.Cp != g.C) WL_CUDA(cudaMemset2DAsync(V + g.C, g.Cp, 0, g.Cp - g.C, (size_t)36 * g.T, st));  // [T*36][Cp]
 
   int bn, sw;
   gemm_tiles(g, &bn, &sw);
   CUtensorMap ta, tbm;
-  if (!make_tmap_i8_3d(&ta, V, g.Cp, g.T, 36, sw, 128) || !make_tmap_i8_3d(&tbm, U, g.Cp, g.Kp, 36, sw, bn))
+  if (!make_tmap_i8_3d(&ta, V, g.Cp, 36, g.T, sw, 1, 128) || !make_tmap_i8_3d(&tbm, U, g.Cp, 36, g.Kp, sw, 1, bn))
     return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   const int wstage = leg ? ST_WBC : ST_WT;
   const int qu = b.q[wstage];
@@ -663,35 +698,38 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
 
   const long long oc = (long long)g.T * g.K;
   const unsigned ogrid = (unsigned)((oc + tb - 1) / tb);
-#define WL_OUT(HT)                                                                                              \
-  if (!leg) {                                                                                                   \
-    out_a_kernel<0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, g, acc, tabs);                                  \
-    finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
-        tabs.t[ST_OUT], E.e[ST_OUT]); \
-    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);                        \
-    prof_mark("output_max", st);                                                                                \
-    out_c_kernel<0, HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, y, bias, g, b, acc, plan->d_pf);             \
-    prof_mark("output_write", st);                                                                              \
-  } else {                                                                                                      \
-    out_a_kernel<1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, g, acc, tabs);                                  \
-    finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
-        tabs.t[ST_OBC], E.e[ST_OBC]); \
-    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);                        \
-    prof_mark("output_base_change_max", st);                                                                    \
-    out_b_kernel<HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf, tabs);                  \
-    finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>((const HT*)h, c4, g, b, acc, plan->d_pf,  \
-        tabs.t[ST_OUT], E.e[ST_OUT]); \
-    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);                        \
-    prof_mark("output_max", st);                                                                                \
-    out_c_kernel<1, HT><<<ogrid, tb, 0, st>>>((const HT*)h, c4, y, bias, g, b, acc, plan->d_pf);             \
-    prof_mark("output_write", st);                                                                              \
-  }
-  if (L.hbytes == 1) {
-    WL_OUT(int8_t)
-  } else {
-    WL_OUT(int16_t)
-  }
-#undef WL_OUT
+  auto run_out = [&](auto ldc, auto ht) {
+    constexpr int LD = decltype(ldc)::value;
+    using HT = decltype(ht);
+    const HT* hh = reinterpret_cast<const HT*>(h);
+    if (!leg) {
+      out_a_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
+      finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+      prof_mark("output_max", st);
+      out_c_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf);
+      prof_mark("output_write", st);
+    } else {
+      out_a_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
+      finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
+      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
+      prof_mark("output_base_change_max", st);
+      out_b_kernel<HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs);
+      finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+      prof_mark("output_max", st);
+      out_c_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf);
+      prof_mark("output_write", st);
+    }
+  };
+  rc = dispatch_ld_out(g.Kp, [&](auto ldc) {
+    if (L.hbytes == 1)
+      run_out(ldc, int8_t{});
+    else
+      run_out(ldc, int16_t{});
+  });
+  if (rc) return rc;
+
   WL_CUDA(cudaGetLastError());
   return WL_OK;
 }

@@ -9,9 +9,11 @@
 //
 // Data layout in HBM (workspace):
 //   c0  int8 [N][H][W][Cp]     input codes, channel-last so (tile, channel) threads coalesce
-//   V   int8 [36][T][Cp]       input-transform codes, GEMM A operand (K-major)
-//   U   int8 [36][Kp][Cp]      weight-transform codes, GEMM B operand (K-major, cached)
-//   h   int8|int16 [36][T][Kp] hadamard codes
+//   V   int8 [T][36][Cp]       input-transform codes, GEMM A operand (K-major)
+//   U   int8 [Kp][36][Cp]      weight-transform codes, GEMM B operand (K-major, cached)
+//   h   int8|int16 [T][36][Kp] hadamard codes (c1 [T][36][Cp], c4 [T][36][Kp] likewise)
+// Cp, Kp are powers of two (>= 32 / 64, <= 512) so the 36 element offsets of a unit are
+// compile-time immediates in the templated kernels.
 //   acc Acc [groups][9]        per-group stage maxima
 // T = N * TP tiles, TP = ceil(Ho/4)*ceil(Wo/4); element xi = 6*i + j of a 6x6 tile.
 #pragma once
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(256) weight_stage_kernel(const float* __restri
   if constexpr (MODE == 0) {
     if (active)
 #pragma unroll
-      for (int e = 0; e < 36; ++e) U[((size_t)e * Kp + k) * Cp + c] = (int8_t)C1[e / 6][e % 6];
+      for (int e = 0; e < 36; ++e) U[((size_t)k * 36 + e) * Cp + c] = (int8_t)C1[e / 6][e % 6];
   } else {
     int U2[6][6];
     sandwich<tab::Leg_WBC>(C1, U2);
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(256) weight_stage_kernel(const float* __restri
       requant36(U2, q2, C1, q1, pf->wbc, C2);
       if (active)
 #pragma unroll
-        for (int e = 0; e < 36; ++e) U[((size_t)e * Kp + k) * Cp + c] = (int8_t)C2[e / 6][e % 6];
+        for (int e = 0; e < 36; ++e) U[((size_t)k * 36 + e) * Cp + c] = (int8_t)C2[e / 6][e % 6];
     }
   }
 }

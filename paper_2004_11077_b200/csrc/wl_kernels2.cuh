@@ -32,31 +32,60 @@ __device__ __forceinline__ float stage_error(const Acc& a, float rowsum) {
   return 6.5f * 5.9604645e-8f * rowsum * __uint_as_float(a.TM);
 }
 
+// Small integer -> float without the (slow) I2F pipe: |v| < 2^22 placed in the mantissa of 1.5*2^23.
+__device__ __forceinline__ float small_i2f(int v) { return __int_as_float(v + 0x4B400000) - kMagic; }
+template <typename XT>
+__device__ __forceinline__ XT to_x(int v) {
+  if constexpr (sizeof(XT) == 4 && XT(0.5) != XT(0))
+    return small_i2f(v);
+  else
+    return (XT)v;
+}
+
+// Window of one (tile, channel) unit in the NHWC input codes: base offset of pixel (r0, q0), the row
+// and column strides, and bit masks of the rows / columns inside the image (zero padding).
+struct C0Win {
+  const int8_t* p;
+  uint32_t base, rs, cs;
+  unsigned rmask, cmask;
+  __device__ __forceinline__ C0Win(const int8_t* c0, const Geo& g, int n, int tile, int c, uint32_t cstride)
+      : p(c0) {
+    const int ty = tile / g.tw, tx = tile % g.tw;
+    const int r0 = 4 * ty - g.pad, q0 = 4 * tx - g.pad;
+    cs = cstride;
+    rs = (uint32_t)g.W * cs;
+    base = ((uint32_t)(n * g.H + r0) * (uint32_t)g.W + (uint32_t)q0) * cs + (uint32_t)c;
+    rmask = cmask = 0;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      rmask |= (unsigned)((unsigned)(r0 + j) < (unsigned)g.H) << j;
+      cmask |= (unsigned)((unsigned)(q0 + j) < (unsigned)g.W) << j;
+    }
+  }
+  template <typename XT>
+  __device__ __forceinline__ void load(XT (&X)[6][6]) const {
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        const bool v = ((rmask >> i) & (cmask >> j) & 1u) != 0;
+        X[i][j] = to_x<XT>(v ? (int)__ldg(p + (base + (uint32_t)i * rs + (uint32_t)j * cs)) : 0);
+      }
+  }
+};
+
 // 6x6 window of input codes (NHWC int8, implicit zero padding).
 template <typename XT>
 __device__ __forceinline__ void load_c0(const int8_t* __restrict__ c0, const Geo& g, int n, int tile, int c,
                                         XT (&X)[6][6]) {
-  const int ty = tile / g.tw, tx = tile % g.tw;
-  const int r0 = 4 * ty - g.pad, q0 = 4 * tx - g.pad;
-  const uint32_t cp = (uint32_t)g.Cp;
-  const uint32_t base = ((uint32_t)(n * g.H + r0) * (uint32_t)g.W + (uint32_t)q0) * cp + (uint32_t)c;
-  bool cv[6];
-#pragma unroll
-  for (int j = 0; j < 6; ++j) cv[j] = (unsigned)(q0 + j) < (unsigned)g.W;
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    const bool rv = (unsigned)(r0 + i) < (unsigned)g.H;
-    const uint32_t rb = base + (uint32_t)i * (uint32_t)g.W * cp;
-#pragma unroll
-    for (int j = 0; j < 6; ++j) X[i][j] = (rv && cv[j]) ? (XT)__ldg(c0 + (rb + (uint32_t)j * cp)) : (XT)0;
-  }
+  C0Win(c0, g, n, tile, c, (uint32_t)g.Cp).load(X);
 }
 
-// 36 codes of one unit from a [36][rows][ld] plane layout.
+// 36 codes of one unit of a [T][36][LD] layout: element e at off + e * plane (plane = LD).
 template <typename HT, typename XT>
 __device__ __forceinline__ void load_planes(const HT* __restrict__ P, uint32_t plane, uint32_t off, XT (&X)[6][6]) {
 #pragma unroll
-  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = (XT)__ldg(P + (off + (uint32_t)e * plane));
+  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = to_x<XT>((int)__ldg(P + (off + (uint32_t)e * plane)));
 }
 
 // Max of one (unit row t, channel c) into table entry t*ceil(C/32) + c/32 and the group running max.
@@ -83,16 +112,16 @@ __device__ __forceinline__ void record_unit(float m, float tm, int grp, bool act
 // ---------------------------------------------------------------------------------- exact elements
 
 struct SrcC0 {  // input codes window
-  const int8_t* p;
-  Geo g;
-  int n, tile, c;
-  __device__ void load(int (&X)[6][6]) const { load_c0(p, g, n, tile, c, X); }
+  C0Win w;
+  template <typename XT>
+  __device__ void load(XT (&X)[6][6]) const { w.load(X); }
 };
 template <typename HT>
-struct SrcPlanes {  // [36][rows][ld] codes
+struct SrcPlanes {  // [T][36][LD] codes
   const HT* p;
   uint32_t plane, off;
-  __device__ void load(int (&X)[6][6]) const { load_planes(p, plane, off, X); }
+  template <typename XT>
+  __device__ void load(XT (&X)[6][6]) const { load_planes(p, plane, off, X); }
 };
 
 // Exact code of element (i, j) of stage L . X . L^T, X reloaded from src; ties replayed in fp64.
@@ -119,6 +148,32 @@ __device__ __noinline__ int exact_elem(Src src, int i, int j, const Acc* a_stage
   return code;
 }
 
+// Fast-path requantisation of one element (branch free): code from the magic-number rounding,
+// float code k, and the running max distance to the rounded value (band check once per unit).
+__device__ __forceinline__ int rq_nb(float T, float r, float& k, float& dmax) {
+  const float y = fmaf(T, r, kMagic);
+  k = y - kMagic;
+  dmax = fmaxf(dmax, fabsf(fmaf(T, r, -k)));
+  return __float_as_int(y) - 0x4B400000;
+}
+
+// Rare path for a unit whose fast path came within the band of a half-integer: redo the fp32
+// sandwich (deterministic, same values), and for every flagged element compute the exact code and
+// hand it to out(i, j, code), which overwrites what the fast path stored.
+template <class L, class Src, class Out>
+__device__ __noinline__ void fix_unit(Src src, float r, float thr, const Acc* a_stage, int qmax, const Acc* a_in,
+                                      int qmax_in, bool in_float, const double* __restrict__ Lf, Out out) {
+  float X[6][6];
+  src.load(X);
+  sandwich_cols<L>(X, [&](int j, const float (&col)[L::R]) {
+    for (int i = 0; i < L::R; ++i) {
+      const float y = fmaf(col[i], r, kMagic), k = y - kMagic;
+      if (fabsf(fmaf(col[i], r, -k)) > thr)
+        out(i, j, exact_elem<L>(src, i, j, a_stage, qmax, a_in, qmax_in, in_float, Lf));
+    }
+  });
+}
+
 // r, threshold and reference scale of one stage for every group, once its M and F are final.
 __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage, int qmax, float rowsum) {
   const int gi = blockIdx.x * blockDim.x + threadIdx.x;
@@ -138,7 +193,7 @@ __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage
 // ---------------------------------------------------------------------------------- input side
 
 // First input stage maximum: canonical input_transform (B^T), Legendre input_base_change (P^-T).
-template <int MODE>
+template <int MODE, int LD>
 __global__ void __launch_bounds__(256) in_a_kernel(const int8_t* __restrict__ c0, Geo g, Acc* __restrict__ acc,
                                                    Tables tabs) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -148,7 +203,7 @@ __global__ void __launch_bounds__(256) in_a_kernel(const int8_t* __restrict__ c0
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
   float X[6][6];
-  load_c0(c0, g, n, tile, c, X);
+  C0Win(c0, g, n, tile, c, LD).load(X);
   constexpr int st = MODE == 0 ? ST_IT : ST_IBC;
   float m = 0.f, tm = 0.f;
   auto mx = [&](int, const float (&col)[6]) {
@@ -163,6 +218,7 @@ __global__ void __launch_bounds__(256) in_a_kernel(const int8_t* __restrict__ c0
 }
 
 // Legendre: input_base_change codes c1 (stored) and input_transform maximum.
+template <int LD>
 __global__ void __launch_bounds__(256, 2) in_b_kernel(const int8_t* __restrict__ c0, int8_t* __restrict__ c1, Geo g,
                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                                    Tables tabs) {
@@ -174,22 +230,27 @@ __global__ void __launch_bounds__(256, 2) in_b_kernel(const int8_t* __restrict__
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_IBC].r, thr = ga[ST_IBC].thr;
-  const uint32_t plane = (uint32_t)g.T * g.Cp;
-  int8_t* dst = c1 + (uint32_t)t * g.Cp + c;
+  constexpr uint32_t plane = LD;
+  int8_t* dst = c1 + ((size_t)t * 36 * LD + c);
   float K1[6][6];
   {
+    const C0Win win(c0, g, n, tile, c, LD);
     float X[6][6];
-    load_c0(c0, g, n, tile, c, X);
+    win.load(X);
+    float dmax = 0.f;
     sandwich_cols<tab::Leg_IBC>(X, [&](int j, const float (&col)[6]) {
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        const int code = rq_elem(col[i], r, thr, [&] {
-          return exact_elem<tab::Leg_IBC>(SrcC0{c0, g, n, tile, c}, i, j, ga + ST_IBC, b.q[ST_IBC], ga + ST_INPUT,
-                                          b.q[ST_INPUT], true, pf->ibc);
-        }, K1[i][j]);
-        if (active) dst[(uint32_t)(6 * i + j) * plane] = (int8_t)code;
+        const int code = rq_nb(col[i], r, K1[i][j], dmax);
+        if (active) dst[(6 * i + j) * plane] = (int8_t)code;
       }
     });
+    if (dmax > thr && active) {
+      fix_unit<tab::Leg_IBC>(SrcC0{win}, r, thr, ga + ST_IBC, b.q[ST_IBC], ga + ST_INPUT, b.q[ST_INPUT], true,
+                             pf->ibc, [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; });
+#pragma unroll
+      for (int e = 0; e < 36; ++e) K1[e / 6][e % 6] = (float)dst[e * plane];
+    }
   }
   float m = 0.f, tm = 0.f;
   sandwich_cols<tab::Leg_IT>(K1, [&](int, const float (&col)[6]) {
@@ -200,7 +261,7 @@ __global__ void __launch_bounds__(256, 2) in_b_kernel(const int8_t* __restrict__
 }
 
 // V codes.  Canonical: from c0 through B^T.  Legendre: from the stored c1 through B_P^T.
-template <int MODE>
+template <int MODE, int LD>
 __global__ void __launch_bounds__(256) in_c_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
                                                    int8_t* __restrict__ V, Geo g, Bits b, Acc* __restrict__ acc,
                                                    const PlanF64* __restrict__ pf) {
@@ -211,35 +272,29 @@ __global__ void __launch_bounds__(256) in_c_kernel(const int8_t* __restrict__ c0
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_IT].r, thr = ga[ST_IT].thr;
-  const uint32_t plane = (uint32_t)g.T * g.Cp;
-  const uint32_t off = (uint32_t)t * g.Cp + c;
+  constexpr uint32_t plane = LD;
+  const uint32_t off = (uint32_t)t * 36u * LD + c;
   int8_t* dst = V + off;
   float X[6][6];
-  float kdummy;
-  if constexpr (MODE == 0) {
-    load_c0(c0, g, n, tile, c, X);
-    sandwich_cols<tab::Can_IT>(X, [&](int j, const float (&col)[6]) {
+  float dmax = 0.f, kd;
+  auto store = [&](int j, const float (&col)[6]) {
 #pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        const int code = rq_elem(col[i], r, thr, [&] {
-          return exact_elem<tab::Can_IT>(SrcC0{c0, g, n, tile, c}, i, j, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT,
-                                         b.q[ST_INPUT], true, pf->it);
-        }, kdummy);
-        dst[(uint32_t)(6 * i + j) * plane] = (int8_t)code;
-      }
-    });
+    for (int i = 0; i < 6; ++i) dst[(6 * i + j) * plane] = (int8_t)rq_nb(col[i], r, kd, dmax);
+  };
+  auto fix = [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; };
+  if constexpr (MODE == 0) {
+    const C0Win win(c0, g, n, tile, c, LD);
+    win.load(X);
+    sandwich_cols<tab::Can_IT>(X, store);
+    if (dmax > thr)
+      fix_unit<tab::Can_IT>(SrcC0{win}, r, thr, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT, b.q[ST_INPUT], true, pf->it,
+                            fix);
   } else {
     load_planes(c1, plane, off, X);
-    sandwich_cols<tab::Leg_IT>(X, [&](int j, const float (&col)[6]) {
-#pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        const int code = rq_elem(col[i], r, thr, [&] {
-          return exact_elem<tab::Leg_IT>(SrcPlanes<int8_t>{c1, plane, off}, i, j, ga + ST_IT, b.q[ST_IT],
-                                         ga + ST_IBC, b.q[ST_IBC], false, pf->it);
-        }, kdummy);
-        dst[(uint32_t)(6 * i + j) * plane] = (int8_t)code;
-      }
-    });
+    sandwich_cols<tab::Leg_IT>(X, store);
+    if (dmax > thr)
+      fix_unit<tab::Leg_IT>(SrcPlanes<int8_t>{c1, plane, off}, r, thr, ga + ST_IT, b.q[ST_IT], ga + ST_IBC,
+                            b.q[ST_IBC], false, pf->it, fix);
   }
 }
 
@@ -255,7 +310,7 @@ __device__ void exact_input_unit(const int8_t* __restrict__ c0, const int8_t* __
   StageQ qin;
   const double* Lf;
   if (MODE == 1 && STAGE == ST_IT) {
-    load_planes(c1, (uint32_t)g.T * g.Cp, (uint32_t)t * g.Cp + c, Xi);
+    load_planes(c1, (uint32_t)g.Cp, (uint32_t)t * 36u * g.Cp + c, Xi);
     sandwich<tab::Leg_IT>(Xi, T);
     qin = load_int_stage(ga[ST_IBC], b.q[ST_IBC]);
     Lf = pf->it;
@@ -321,7 +376,7 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
 
 // Thread per (tile t, out channel k), k fastest.
 // OUT_A: Legendre output_base_change max (P^-T on h) | canonical output max (A^T on h, cropped).
-template <int MODE, typename HT>
+template <int MODE, typename HT, int LD>
 __global__ void __launch_bounds__(256) out_a_kernel(const HT* __restrict__ h, Geo g, Acc* __restrict__ acc,
                                                     Tables tabs) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -332,7 +387,7 @@ __global__ void __launch_bounds__(256) out_a_kernel(const HT* __restrict__ h, Ge
   const int grp = n / g.ipg;
   const int ty = tile / g.tw, tx = tile % g.tw;
   float X[6][6];
-  load_planes(h, (uint32_t)g.T * g.Kp, (uint32_t)t * g.Kp + k, X);
+  load_planes(h, (uint32_t)LD, (uint32_t)t * 36u * LD + k, X);
   float m = 0.f, tm = 0.f;
   constexpr int st = MODE == 0 ? ST_OUT : ST_OBC;
   if constexpr (MODE == 0) {
@@ -351,7 +406,7 @@ __global__ void __launch_bounds__(256) out_a_kernel(const HT* __restrict__ h, Ge
 }
 
 // Legendre: output_base_change codes c4 (stored) and cropped output maximum.
-template <typename HT>
+template <typename HT, int LD>
 __global__ void __launch_bounds__(256, 2) out_b_kernel(const HT* __restrict__ h, int8_t* __restrict__ c4, Geo g, Bits b,
                                                     Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                                     Tables tabs) {
@@ -363,23 +418,28 @@ __global__ void __launch_bounds__(256, 2) out_b_kernel(const HT* __restrict__ h,
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr;
-  const uint32_t plane = (uint32_t)g.T * g.Kp;
-  const uint32_t off = (uint32_t)t * g.Kp + k;
+  constexpr uint32_t plane = LD;
+  const uint32_t off = (uint32_t)t * 36u * LD + k;
   int8_t* dst = c4 + off;
   float K4[6][6];
   {
     float X[6][6];
     load_planes(h, plane, off, X);
+    float dmax = 0.f;
     sandwich_cols<tab::Leg_OBC>(X, [&](int j, const float (&col)[6]) {
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        const int code = rq_elem(col[i], r, thr, [&] {
-          return exact_elem<tab::Leg_OBC>(SrcPlanes<HT>{h, plane, off}, i, j, ga + ST_OBC, b.q[ST_OBC], ga + ST_HAD,
-                                          b.q[ST_HAD], false, pf->obc);
-        }, K4[i][j]);
-        if (active) dst[(uint32_t)(6 * i + j) * plane] = (int8_t)code;
+        const int code = rq_nb(col[i], r, K4[i][j], dmax);
+        if (active) dst[(6 * i + j) * plane] = (int8_t)code;
       }
     });
+    if (dmax > thr && active) {
+      fix_unit<tab::Leg_OBC>(SrcPlanes<HT>{h, plane, off}, r, thr, ga + ST_OBC, b.q[ST_OBC], ga + ST_HAD,
+                             b.q[ST_HAD], false, pf->obc,
+                             [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; });
+#pragma unroll
+      for (int e = 0; e < 36; ++e) K4[e / 6][e % 6] = (float)dst[e * plane];
+    }
   }
   const int ty = tile / g.tw, tx = tile % g.tw;
   float m = 0.f, tm = 0.f;
@@ -392,7 +452,7 @@ __global__ void __launch_bounds__(256, 2) out_b_kernel(const HT* __restrict__ h,
 }
 
 // Final output: codes of the output stage, dequantised (snap +-qmax to +-max_abs), + bias, fp32 NCHW.
-template <int MODE, typename HT>
+template <int MODE, typename HT, int LD>
 __global__ void __launch_bounds__(256, 2) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
                                                     float* __restrict__ y, const float* __restrict__ bias, Geo g,
                                                     Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf) {
@@ -407,34 +467,41 @@ __global__ void __launch_bounds__(256, 2) out_c_kernel(const HT* __restrict__ h,
   const double scale = ga[ST_OUT].scale;
   const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
   const int qo = b.q[ST_OUT];
-  const uint32_t plane = (uint32_t)g.T * g.Kp;
-  const uint32_t off = (uint32_t)t * g.Kp + k;
+  constexpr uint32_t plane = LD;
+  const uint32_t off = (uint32_t)t * 36u * LD + k;
   float Yo[4][4];
   float X[6][6];
-  float kdummy;
-  auto emit = [&](int i, int j, int code) {
-    Yo[i][j] = code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+  float dmax = 0.f, kd;
+  auto deqf = [=](int code) {
+    return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+  };
+  auto emit = [&](int j, const float (&col)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) Yo[i][j] = deqf(rq_nb(col[i], r, kd, dmax));
   };
   if constexpr (MODE == 0) {
     load_planes(h, plane, off, X);
-    sandwich_cols<tab::Can_OT>(X, [&](int j, const float (&col)[4]) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        emit(i, j, rq_elem(col[i], r, thr, [&] {
-               return exact_elem<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, i, j, ga + ST_OUT, qo, ga + ST_HAD,
-                                              b.q[ST_HAD], false, pf->ot);
-             }, kdummy));
-    });
+    sandwich_cols<tab::Can_OT>(X, emit);
   } else {
     load_planes(c4, plane, off, X);
-    sandwich_cols<tab::Leg_OT>(X, [&](int j, const float (&col)[4]) {
+    sandwich_cols<tab::Leg_OT>(X, emit);
+  }
+  if (dmax > thr) {
+    float fixed[16];
+    unsigned mask = 0;
+    auto fix = [&](int i, int j, int code) {
+      fixed[4 * i + j] = deqf(code);
+      mask |= 1u << (4 * i + j);
+    };
+    if constexpr (MODE == 0)
+      fix_unit<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, r, thr, ga + ST_OUT, qo, ga + ST_HAD, b.q[ST_HAD], false,
+                            pf->ot, fix);
+    else
+      fix_unit<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, r, thr, ga + ST_OUT, qo, ga + ST_OBC, b.q[ST_OBC],
+                            false, pf->ot, fix);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        emit(i, j, rq_elem(col[i], r, thr, [&] {
-               return exact_elem<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, i, j, ga + ST_OUT, qo,
-                                              ga + ST_OBC, b.q[ST_OBC], false, pf->ot);
-             }, kdummy));
-    });
+    for (int e = 0; e < 16; ++e)
+      if ((mask >> e) & 1u) Yo[e / 4][e % 4] = fixed[e];
   }
   const float bk = bias ? __ldg(&bias[k]) : 0.f;
   const bool vec = (g.Wo & 3) == 0;
@@ -462,7 +529,7 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
   Acc* ga = acc + (size_t)grp * ST_COUNT;
   int Xi[6][6];
   if (MODE == 1 && STAGE == ST_OBC) {
-    load_planes(h, (uint32_t)g.T * g.Kp, (uint32_t)t * g.Kp + k, Xi);
+    load_planes(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
     int T[6][6];
     sandwich<tab::Leg_OBC>(Xi, T);
     const long long m = absmax36(T);
@@ -483,13 +550,13 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
   long long Y[4][4];
   StageQ qin;
   if (MODE == 0) {
-    load_planes(h, (uint32_t)g.T * g.Kp, (uint32_t)t * g.Kp + k, Xi);
+    load_planes(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
     int Y32[4][4];
     sandwich<tab::Can_OT>(Xi, Y32);
     for (int e = 0; e < 16; ++e) Y[e / 4][e % 4] = Y32[e / 4][e % 4];
     qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
   } else {
-    load_planes(c4, (uint32_t)g.T * g.Kp, (uint32_t)t * g.Kp + k, Xi);
+    load_planes(c4, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
     sandwich<tab::Leg_OT>(Xi, Y);
     qin = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
   }
@@ -570,10 +637,10 @@ __global__ void finalize_hadamard_kernel(const int8_t* __restrict__ U, const int
       const int grp = (t / g.TP) / g.ipg;
       Acc* ga = acc + (size_t)grp * ST_COUNT;
       const long long M = (long long)ga[ST_HAD].M;
-      const int8_t* vrow = V + ((size_t)xi * g.T + t) * g.Cp;
+      const int8_t* vrow = V + ((size_t)t * 36 + xi) * g.Cp;
       double f = 0.0;
       for (int k = chunk * bn + lane; k < min(chunk * bn + bn, g.K); k += 32) {
-        const int8_t* urow = U + ((size_t)xi * g.Kp + k) * g.Cp;
+        const int8_t* urow = U + ((size_t)k * 36 + xi) * g.Cp;
         long long s = 0;
         for (int c = 0; c < g.C; ++c) s += (int)urow[c] * (int)vrow[c];
         if ((s < 0 ? -s : s) == M)

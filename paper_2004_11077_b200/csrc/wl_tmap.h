@@ -23,14 +23,14 @@ inline EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 3-D int8 tensor [d2][d1][d0] (d0 contiguous), box {box0, box1, 1}, swizzle = box0 bytes (32/64/128).
+// 3-D int8 tensor [d2][d1][d0] (d0 contiguous), box {box0, box1, box2}, swizzle = box0 bytes (32/64/128).
 inline bool make_tmap_i8_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-                            uint32_t box0, uint32_t box1) {
+                            uint32_t box0, uint32_t box1, uint32_t box2 = 1) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {d0, d0 * d1};
-  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t box[3] = {box0, box1, box2};
   cuuint32_t estr[3] = {1, 1, 1};
   CUtensorMapSwizzle sw = box0 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                           : box0 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B

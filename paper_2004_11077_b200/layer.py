@@ -214,7 +214,8 @@ class QuantWinogradConv:
         return int(_lib.lib().wl_forward_launches(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs)))
 
     def debug_views(self):
-        """Views of the materialised codes of the last call: c0 [N,H,W,Cp], V [36,T,Cp], h [36,T,Kp]."""
+        """Views of the materialised codes of the last call in logical layouts:
+        c0 [N,H,W,C], V [36,T,C], h [36,T,K], U [36,K,C] (storage is [T][36][Cp] etc.)."""
         shape, cache = self._last
         off = (ctypes.c_size_t * 4)()
         dims = (ctypes.c_int * 4)()
@@ -224,12 +225,12 @@ class QuantWinogradConv:
         Cp, Kp, T, _ = dims[0], dims[1], dims[2], dims[3]
         ws = self.ws
         c0 = ws[off[0]: off[0] + shape.n * shape.h * shape.w * Cp].view(torch.int8).view(shape.n, shape.h, shape.w, Cp)
-        V = ws[off[1]: off[1] + 36 * T * Cp].view(torch.int8).view(36, T, Cp)
+        V = ws[off[1]: off[1] + 36 * T * Cp].view(torch.int8).view(T, 36, Cp).permute(1, 0, 2)
         hb = 2 if self.qconfig.hadamard_bits > 8 else 1
         hraw = ws[off[2]: off[2] + 36 * T * Kp * hb]
-        h = (hraw.view(torch.int16) if hb == 2 else hraw.view(torch.int8)).view(36, T, Kp)
+        h = (hraw.view(torch.int16) if hb == 2 else hraw.view(torch.int8)).view(T, 36, Kp).permute(1, 0, 2)
         cin, cout = shape.c_in, shape.c_out
-        ucodes = cache[cache.numel() - 36 * Kp * Cp:].view(torch.int8).view(36, Kp, Cp)
+        ucodes = cache[cache.numel() - 36 * Kp * Cp:].view(torch.int8).view(Kp, 36, Cp).permute(1, 0, 2)
         return {"c0": c0[..., :cin], "V": V[..., :cin], "h": h[..., :cout], "U": ucodes[:, :cout, :cin]}
 
 
