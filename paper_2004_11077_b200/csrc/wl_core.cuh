@@ -10,6 +10,7 @@
 // and sum rounded separately (__dmul_rn/__dadd_rn, never fused).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include "wl_tables.cuh"
 
 namespace wl {
@@ -25,6 +26,8 @@ struct Acc {
   float thr;              // fast path: 0.5 - band (set by stage_params_kernel once M is final)
   float r;                // fast path: qmax / M
   unsigned int TM;        // fp32 bits of max |first-half value| over the group (error bound input)
+  float ef;               // fast path: qmax * 6.5 * 2^-24 / M (per-element band = ef * rowsum_i * tmax_j)
+  float pad_;
   double scale;           // reference scale max_abs / qmax (1.0 when max_abs == 0)
 };
 
@@ -294,7 +297,14 @@ __device__ __forceinline__ void sandwich_cols(const float (&X)[L::C][L::C], F&& 
         if (L::e(i, l) != 0) s = fmaf((float)L::e(i, l), tc[l], s);
       col[i] = s;
     }
-    f(j, col);
+    if constexpr (std::is_invocable_v<F, int, const float (&)[L::R], float>) {
+      float cm = 0.f;
+#pragma unroll
+      for (int l = 0; l < L::C; ++l) cm = fmaxf(cm, fabsf(tc[l]));
+      f(j, col, cm);
+    } else {
+      f(j, col);
+    }
   }
 }
 
@@ -313,6 +323,14 @@ __device__ __forceinline__ int rq_elem(float T, float r, float thr, Exact&& exac
     kf = k;
   }
   return code;
+}
+
+// Row abs-sums of a compile-time matrix (error-bound factors).
+template <class L>
+__host__ __device__ constexpr float row_abs_sum(int i) {
+  int s = 0;
+  for (int l = 0; l < L::C; ++l) s += L::e(i, l) < 0 ? -L::e(i, l) : L::e(i, l);
+  return (float)s;
 }
 
 // Compile-time sandwich out = L . X . L^T with L a tab:: matrix (R x C), X (C x C).

@@ -287,7 +287,7 @@ struct EpiHadRq {
     grp = valid ? (row / g.TP) / g.ipg : 0;
     const Acc& a = acc[(size_t)grp * ST_COUNT + ST_HAD];
     s.r = a.r;
-    s.band = 0.5f - a.thr;
+    s.band = 0.5f - a.thr;  // exact int32 accumulator: only the r / fma slack
     s.qmax = qmax_h;
   }
   __device__ __forceinline__ void apply(int xi, int row, int col, const uint32_t* v, int n) {

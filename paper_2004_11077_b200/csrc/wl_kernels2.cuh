@@ -150,10 +150,11 @@ __device__ __noinline__ int exact_elem(Src src, int i, int j, const Acc* a_stage
 
 // Fast-path requantisation of one element (branch free): code from the magic-number rounding,
 // float code k, and the running max distance to the rounded value (band check once per unit).
-__device__ __forceinline__ int rq_nb(float T, float r, float& k, float& dmax) {
+// `band` is the element's certified error bound in code units (ef * rowsum_i * max|tmp col j|).
+__device__ __forceinline__ int rq_nb(float T, float r, float band, float& k, float& dmax) {
   const float y = fmaf(T, r, kMagic);
   k = y - kMagic;
-  dmax = fmaxf(dmax, fabsf(fmaf(T, r, -k)));
+  dmax = fmaxf(dmax, fabsf(fmaf(T, r, -k)) + band);
   return __float_as_int(y) - 0x4B400000;
 }
 
@@ -161,14 +162,15 @@ __device__ __forceinline__ int rq_nb(float T, float r, float& k, float& dmax) {
 // sandwich (deterministic, same values), and for every flagged element compute the exact code and
 // hand it to out(i, j, code), which overwrites what the fast path stored.
 template <class L, class Src, class Out>
-__device__ __noinline__ void fix_unit(Src src, float r, float thr, const Acc* a_stage, int qmax, const Acc* a_in,
-                                      int qmax_in, bool in_float, const double* __restrict__ Lf, Out out) {
+__device__ __noinline__ void fix_unit(Src src, float r, float thr, float ef, const Acc* a_stage, int qmax,
+                                      const Acc* a_in, int qmax_in, bool in_float, const double* __restrict__ Lf,
+                                      Out out) {
   float X[6][6];
   src.load(X);
-  sandwich_cols<L>(X, [&](int j, const float (&col)[L::R]) {
+  sandwich_cols<L>(X, [&](int j, const float (&col)[L::R], float cm) {
     for (int i = 0; i < L::R; ++i) {
       const float y = fmaf(col[i], r, kMagic), k = y - kMagic;
-      if (fabsf(fmaf(col[i], r, -k)) > thr)
+      if (fabsf(fmaf(col[i], r, -k)) + ef * cm * row_abs_sum<L>(i) > thr)
         out(i, j, exact_elem<L>(src, i, j, a_stage, qmax, a_in, qmax_in, in_float, Lf));
     }
   });
@@ -183,10 +185,11 @@ __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage
   const long long M = (long long)a.M;
   const double maxabs = __longlong_as_double((long long)a.F);
   a.r = M ? (float)((double)qmax / (double)M) : 0.f;
-  // band: E * qmax / M from the fp32 stage value, + 3e-5 for r's rounding (<= 1.6e-5 code units at
-  // qmax 255) and the fma rounding of the distance itself
-  const float band = M ? (float)((double)qmax * E / (double)M) + 3e-5f : 0.f;
-  a.thr = 0.5f - band;
+  (void)E;
+  // per-element band = ef * rowsum_i * max|tmp col j| (the element's fp32 error E_ij times qmax/M);
+  // slack for r = fl(qmax/M) (relative 2^-24 on a value <= qmax) and the fma rounding of d
+  a.ef = M ? (float)((double)qmax * 6.5 * 5.9604644775390625e-8 / (double)M) : 0.f;
+  a.thr = M ? 0.5f - (float)((qmax + 1) * 1.25 * 5.9604644775390625e-8) : 1.f;
   a.scale = maxabs > 0.0 ? maxabs / (double)qmax : 1.0;
 }
 
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(256, 2) in_b_kernel(const int8_t* __restrict__
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
-  const float r = ga[ST_IBC].r, thr = ga[ST_IBC].thr;
+  const float r = ga[ST_IBC].r, thr = ga[ST_IBC].thr, ef = ga[ST_IBC].ef;
   constexpr uint32_t plane = LD;
   int8_t* dst = c1 + ((size_t)t * 36 * LD + c);
   float K1[6][6];
@@ -238,15 +241,16 @@ __global__ void __launch_bounds__(256, 2) in_b_kernel(const int8_t* __restrict__
     float X[6][6];
     win.load(X);
     float dmax = 0.f;
-    sandwich_cols<tab::Leg_IBC>(X, [&](int j, const float (&col)[6]) {
+    sandwich_cols<tab::Leg_IBC>(X, [&](int j, const float (&col)[6], float cm) {
+      const float fj = ef * cm;
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        const int code = rq_nb(col[i], r, K1[i][j], dmax);
+        const int code = rq_nb(col[i], r, fj * row_abs_sum<tab::Leg_IBC>(i), K1[i][j], dmax);
         if (active) dst[(6 * i + j) * plane] = (int8_t)code;
       }
     });
     if (dmax > thr && active) {
-      fix_unit<tab::Leg_IBC>(SrcC0{win}, r, thr, ga + ST_IBC, b.q[ST_IBC], ga + ST_INPUT, b.q[ST_INPUT], true,
+      fix_unit<tab::Leg_IBC>(SrcC0{win}, r, thr, ef, ga + ST_IBC, b.q[ST_IBC], ga + ST_INPUT, b.q[ST_INPUT], true,
                              pf->ibc, [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; });
 #pragma unroll
       for (int e = 0; e < 36; ++e) K1[e / 6][e % 6] = (float)dst[e * plane];
@@ -271,15 +275,19 @@ __global__ void __launch_bounds__(256) in_c_kernel(const int8_t* __restrict__ c0
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
-  const float r = ga[ST_IT].r, thr = ga[ST_IT].thr;
+  const float r = ga[ST_IT].r, thr = ga[ST_IT].thr, ef = ga[ST_IT].ef;
   constexpr uint32_t plane = LD;
   const uint32_t off = (uint32_t)t * 36u * LD + c;
   int8_t* dst = V + off;
   float X[6][6];
   float dmax = 0.f, kd;
-  auto store = [&](int j, const float (&col)[6]) {
+  constexpr bool kCan = MODE == 0;
+  using LIT = std::conditional_t<kCan, tab::Can_IT, tab::Leg_IT>;
+  auto store = [&](int j, const float (&col)[6], float cm) {
+    const float fj = ef * cm;
 #pragma unroll
-    for (int i = 0; i < 6; ++i) dst[(6 * i + j) * plane] = (int8_t)rq_nb(col[i], r, kd, dmax);
+    for (int i = 0; i < 6; ++i)
+      dst[(6 * i + j) * plane] = (int8_t)rq_nb(col[i], r, fj * row_abs_sum<LIT>(i), kd, dmax);
   };
   auto fix = [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; };
   if constexpr (MODE == 0) {
@@ -287,13 +295,13 @@ __global__ void __launch_bounds__(256) in_c_kernel(const int8_t* __restrict__ c0
     win.load(X);
     sandwich_cols<tab::Can_IT>(X, store);
     if (dmax > thr)
-      fix_unit<tab::Can_IT>(SrcC0{win}, r, thr, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT, b.q[ST_INPUT], true, pf->it,
+      fix_unit<tab::Can_IT>(SrcC0{win}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT, b.q[ST_INPUT], true, pf->it,
                             fix);
   } else {
     load_planes(c1, plane, off, X);
     sandwich_cols<tab::Leg_IT>(X, store);
     if (dmax > thr)
-      fix_unit<tab::Leg_IT>(SrcPlanes<int8_t>{c1, plane, off}, r, thr, ga + ST_IT, b.q[ST_IT], ga + ST_IBC,
+      fix_unit<tab::Leg_IT>(SrcPlanes<int8_t>{c1, plane, off}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_IBC,
                             b.q[ST_IBC], false, pf->it, fix);
   }
 }
@@ -417,7 +425,7 @@ __global__ void __launch_bounds__(256, 2) out_b_kernel(const HT* __restrict__ h,
   const int n = t / g.TP, tile = t % g.TP;
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
-  const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr;
+  const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr, ef = ga[ST_OBC].ef;
   constexpr uint32_t plane = LD;
   const uint32_t off = (uint32_t)t * 36u * LD + k;
   int8_t* dst = c4 + off;
@@ -426,15 +434,16 @@ __global__ void __launch_bounds__(256, 2) out_b_kernel(const HT* __restrict__ h,
     float X[6][6];
     load_planes(h, plane, off, X);
     float dmax = 0.f;
-    sandwich_cols<tab::Leg_OBC>(X, [&](int j, const float (&col)[6]) {
+    sandwich_cols<tab::Leg_OBC>(X, [&](int j, const float (&col)[6], float cm) {
+      const float fj = ef * cm;
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        const int code = rq_nb(col[i], r, K4[i][j], dmax);
+        const int code = rq_nb(col[i], r, fj * row_abs_sum<tab::Leg_OBC>(i), K4[i][j], dmax);
         if (active) dst[(6 * i + j) * plane] = (int8_t)code;
       }
     });
     if (dmax > thr && active) {
-      fix_unit<tab::Leg_OBC>(SrcPlanes<HT>{h, plane, off}, r, thr, ga + ST_OBC, b.q[ST_OBC], ga + ST_HAD,
+      fix_unit<tab::Leg_OBC>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OBC, b.q[ST_OBC], ga + ST_HAD,
                              b.q[ST_HAD], false, pf->obc,
                              [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; });
 #pragma unroll
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(256, 2) out_c_kernel(const HT* __restrict__ h,
   const int ty = tile / g.tw, tx = tile % g.tw;
   const int grp = n / g.ipg;
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
-  const float r = ga[ST_OUT].r, thr = ga[ST_OUT].thr;
+  const float r = ga[ST_OUT].r, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
   const double scale = ga[ST_OUT].scale;
   const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
   const int qo = b.q[ST_OUT];
@@ -475,9 +484,11 @@ __global__ void __launch_bounds__(256, 2) out_c_kernel(const HT* __restrict__ h,
   auto deqf = [=](int code) {
     return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
   };
-  auto emit = [&](int j, const float (&col)[4]) {
+  using LOT = std::conditional_t<MODE == 0, tab::Can_OT, tab::Leg_OT>;
+  auto emit = [&](int j, const float (&col)[4], float cm) {
+    const float fj = ef * cm;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) Yo[i][j] = deqf(rq_nb(col[i], r, kd, dmax));
+    for (int i = 0; i < 4; ++i) Yo[i][j] = deqf(rq_nb(col[i], r, fj * row_abs_sum<LOT>(i), kd, dmax));
   };
   if constexpr (MODE == 0) {
     load_planes(h, plane, off, X);
@@ -494,10 +505,10 @@ __global__ void __launch_bounds__(256, 2) out_c_kernel(const HT* __restrict__ h,
       mask |= 1u << (4 * i + j);
     };
     if constexpr (MODE == 0)
-      fix_unit<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, r, thr, ga + ST_OUT, qo, ga + ST_HAD, b.q[ST_HAD], false,
+      fix_unit<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_HAD, b.q[ST_HAD], false,
                             pf->ot, fix);
     else
-      fix_unit<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, r, thr, ga + ST_OUT, qo, ga + ST_OBC, b.q[ST_OBC],
+      fix_unit<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_OBC, b.q[ST_OBC],
                             false, pf->ot, fix);
 #pragma unroll
     for (int e = 0; e < 16; ++e)
