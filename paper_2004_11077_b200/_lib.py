@@ -13,7 +13,8 @@ import os
 from .errors import CudaLayerError, DimensionError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwinoleg_b200.so")
+# WL_LIB_PATH selects an alternative build of the same library (measurement of kernel variants only)
+LIB_PATH = os.environ.get("WL_LIB_PATH") or os.path.join(_HERE, "libwinoleg_b200.so")
 
 WL_OK, WL_ERR_ARG, WL_ERR_PLAN, WL_ERR_BITS, WL_ERR_CUDA, WL_ERR_WORKSPACE = 0, -1, -2, -3, -4, -5
 WL_CANONICAL, WL_LEGENDRE = 0, 1

@@ -594,8 +594,8 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     int bx = (int)std::min<long long>((per_image / 4 + 255) / 256, 64);
     absmax_f32_kernel<<<dim3(std::max(bx, 1), g.N), 256, 0, st>>>(x, per_image, g.ipg, acc);
     prof_mark("absmax_input", st);
-    const int qrow = std::max(1, std::min(64, 160000 / (g.Cp + 4)));
-    const size_t qsm = (size_t)qrow * (g.Cp + 4);
+    const int qrow = std::max(4, std::min(64, (160000 / (g.Cp + 16)) & ~3));
+    const size_t qsm = (size_t)qrow * (g.Cp + 16);
     static bool qattr = false;
     if (!qattr) {
       WL_CUDA(cudaFuncSetAttribute(quant_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

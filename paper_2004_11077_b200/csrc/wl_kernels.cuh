@@ -72,28 +72,63 @@ __global__ void absmax_f32_kernel(const float* __restrict__ x, long long per_ima
 }
 
 // c0 = rint(x / s0) (quantize.py:118-119), NCHW fp32 -> NHWC int8.  Block = (row h, image n):
-// warps sweep channels with lanes along W (coalesced loads), codes land in a shared row buffer
-// [w][Cp+4] (the +4 pad keeps the byte stores bank-conflict free), which is copied out as words.
+// threads sweep (channel, 4-pixel chunk) with float4 loads, round with the magic-number fma (the
+// exact fp64 division of the reference only within 2^-20 of a half-integer), and deposit codes in a
+// shared row buffer [w][Cp+16] that is copied out as 16-byte vectors.
+__device__ __forceinline__ int quant_code(float v, float rc, float thr, double scale, int qmax) {
+  const float a = fabsf(v);
+  const float y = fmaf(a, rc, kMagic);
+  const float k = y - kMagic;
+  int c = __float_as_int(y) - 0x4B400000;
+  if (fabsf(fmaf(a, rc, -k)) > thr) {  // near a half-integer: the reference's fp64 quotient decides
+    double d = rint((double)a / scale);
+    c = (int)(d > qmax ? qmax : d);
+  }
+  c = c > qmax ? qmax : c;
+  return v < 0.f ? -c : c;
+}
+
 __global__ void __launch_bounds__(256) quant_input_kernel(const float* __restrict__ x, int8_t* __restrict__ c0, Geo g,
                                                           Bits b, const Acc* __restrict__ acc, int kQuantRowW) {
-  extern __shared__ int8_t srow[];
+  extern __shared__ __align__(16) int8_t srow[];
   const int h = blockIdx.x, n = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
-  const int ld = g.Cp + 4;
+  const float rc = q.maxabs > 0.0 ? (float)((double)q.qmax / q.maxabs) : 0.f;
+  // fast-path error: rc relative 2^-24 on a value <= qmax, plus the fma rounding of the distance
+  const float thr = 0.5f - (float)((q.qmax + 1) * 1.25 * 5.9604644775390625e-8);
+  const int ld = g.Cp + 16;
+  const bool vec = (g.W & 3) == 0;
   for (int w0 = 0; w0 < g.W; w0 += kQuantRowW) {
     const int wn = min(kQuantRowW, g.W - w0);
-    for (int c = warp; c < g.Cp; c += nwarps) {
-      const float* xr = x + (((size_t)n * g.C + c) * g.H + h) * g.W + w0;
-      for (int w = lane; w < wn; w += 32)
-        srow[w * ld + c] = c < g.C ? (int8_t)quant_float(__ldg(xr + w), q) : (int8_t)0;
+    if (vec) {
+      const int w4n = wn >> 2;
+      for (int i = threadIdx.x; i < g.Cp * w4n; i += blockDim.x) {
+        const int c = i / w4n, w4 = i - c * w4n;
+        int8_t* dst = srow + (4 * w4) * ld + c;
+        if (c < g.C) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(x + (((size_t)n * g.C + c) * g.H + h) * g.W + w0) + w4);
+          dst[0] = (int8_t)quant_code(v.x, rc, thr, q.scale, q.qmax);
+          dst[ld] = (int8_t)quant_code(v.y, rc, thr, q.scale, q.qmax);
+          dst[2 * ld] = (int8_t)quant_code(v.z, rc, thr, q.scale, q.qmax);
+          dst[3 * ld] = (int8_t)quant_code(v.w, rc, thr, q.scale, q.qmax);
+        } else {
+          dst[0] = dst[ld] = dst[2 * ld] = dst[3 * ld] = 0;
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < g.Cp * wn; i += blockDim.x) {
+        const int c = i / wn, w = i - c * wn;
+        srow[w * ld + c] = c < g.C ? (int8_t)quant_code(__ldg(x + (((size_t)n * g.C + c) * g.H + h) * g.W + w0 + w),
+                                                        rc, thr, q.scale, q.qmax)
+                                   : (int8_t)0;
+      }
     }
     __syncthreads();
-    int* dst = reinterpret_cast<int*>(c0 + (((size_t)n * g.H + h) * g.W + w0) * g.Cp);
-    const int words = g.Cp >> 2;
-    for (int i = threadIdx.x; i < wn * words; i += blockDim.x) {
-      const int w = i / words, j = i - w * words;
-      dst[i] = *reinterpret_cast<const int*>(srow + w * ld + 4 * j);
+    int4* dst = reinterpret_cast<int4*>(c0 + (((size_t)n * g.H + h) * g.W + w0) * g.Cp);
+    const int vpr = g.Cp >> 4;  // 16-byte vectors per pixel row
+    for (int i = threadIdx.x; i < wn * vpr; i += blockDim.x) {
+      const int w = i / vpr, j = i - w * vpr;
+      dst[i] = *reinterpret_cast<const int4*>(srow + w * ld + 16 * j);
     }
     __syncthreads();
   }

@@ -16,6 +16,10 @@
 #pragma once
 #include "wl_kernels.cuh"
 
+#ifndef WL_MINB
+#define WL_MINB 3  // resident blocks per SM requested for the heavy transform kernels (measured best)
+#endif
+
 namespace wl {
 
 struct Tables {  // max tables per stage id (only IBC, IT, HAD, OBC, OUT are used)
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(256) in_a_kernel(const int8_t* __restrict__ c0
 
 // Legendre: input_base_change codes c1 (stored) and input_transform maximum.
 template <int LD>
-__global__ void __launch_bounds__(256, 2) in_b_kernel(const int8_t* __restrict__ c0, int8_t* __restrict__ c1, Geo g,
+__global__ void __launch_bounds__(256, WL_MINB) in_b_kernel(const int8_t* __restrict__ c0, int8_t* __restrict__ c1, Geo g,
                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                                    Tables tabs) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(256, 2) in_b_kernel(const int8_t* __restrict__
 
 // V codes.  Canonical: from c0 through B^T.  Legendre: from the stored c1 through B_P^T.
 template <int MODE, int LD>
-__global__ void __launch_bounds__(256) in_c_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
+__global__ void __launch_bounds__(256, WL_MINB) in_c_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
                                                    int8_t* __restrict__ V, Geo g, Bits b, Acc* __restrict__ acc,
                                                    const PlanF64* __restrict__ pf) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(256) out_a_kernel(const HT* __restrict__ h, Ge
 
 // Legendre: output_base_change codes c4 (stored) and cropped output maximum.
 template <typename HT, int LD>
-__global__ void __launch_bounds__(256, 2) out_b_kernel(const HT* __restrict__ h, int8_t* __restrict__ c4, Geo g, Bits b,
+__global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restrict__ h, int8_t* __restrict__ c4, Geo g, Bits b,
                                                     Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                                     Tables tabs) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(256, 2) out_b_kernel(const HT* __restrict__ h,
 
 // Final output: codes of the output stage, dequantised (snap +-qmax to +-max_abs), + bias, fp32 NCHW.
 template <int MODE, typename HT, int LD>
-__global__ void __launch_bounds__(256, 2) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
+__global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
                                                     float* __restrict__ y, const float* __restrict__ bias, Geo g,
                                                     Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
