@@ -76,6 +76,15 @@ int wl_workspace_size(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, 
 int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
                const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Straight-through-estimator backward (no reference counterpart): casts are identity,
+ * scales detached, products use the forward's quantised U and V.  fwd_workspace must be the
+ * workspace of the wl_forward call being differentiated (it holds the V codes and stage scales).
+ * dx [n][c_in][h][w], dw [c_out][c_in][3][3], db [c_out] (may be NULL), all fp32. */
+int wl_backward_workspace_size(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* bytes);
+int wl_backward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* dy, const void* cache,
+                const void* fwd_workspace, float* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
+                void* stream);
+
 /* Per-group StageStat rows [n/images_per_group][nstages] after wl_forward (synchronises stream). */
 int wl_num_stages(const wl_plan* plan);
 int wl_read_stats(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, const void* cache,

@@ -120,7 +120,7 @@ __device__ __forceinline__ int quant_float(float v, const StageQ& q) {
 // ---------------------------------------------------------------- fp64 replays (rare path)
 
 // out[i][j] of L . X . L^T, L is R x B (row-major fp64), X is B x B given as codes + dequant params.
-__device__ __noinline__ double replay_sandwich(const double* __restrict__ L, int R, int B, const int* codes, int qmax,
+static __device__ __noinline__ double replay_sandwich(const double* __restrict__ L, int R, int B, const int* codes, int qmax,
                                                double maxabs, double scale, int i, int j) {
   (void)R;
   double tmp[6];
@@ -135,7 +135,7 @@ __device__ __noinline__ double replay_sandwich(const double* __restrict__ L, int
 }
 
 // Hadamard element: sum_c deq(u_c) * deq(v_c), c ascending from 0.0 (_kernels.py:99-104).
-__device__ __noinline__ double replay_hadamard(const int8_t* __restrict__ u, const int8_t* __restrict__ v, int C,
+static __device__ __noinline__ double replay_hadamard(const int8_t* __restrict__ u, const int8_t* __restrict__ v, int C,
                                                StageQ qu, StageQ qv) {
   double acc = 0.0;
   for (int c = 0; c < C; ++c)

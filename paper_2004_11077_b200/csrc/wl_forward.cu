@@ -14,6 +14,7 @@
 
 #include "../../include/winoleg_b200.h"
 #include "gemm_i8.cuh"
+#include "wl_backward.h"
 #include "wl_kernels2.cuh"
 #include "wl_tmap.h"
 
@@ -45,7 +46,6 @@ int pow2_at_least(int v, int lo) {
   while (p < v) p <<= 1;
   return p;
 }
-int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 }  // namespace
 
@@ -731,6 +731,45 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
   if (rc) return rc;
 
   WL_CUDA(cudaGetLastError());
+  return WL_OK;
+}
+
+static BwGeo bw_geo(const Layout& L) {
+  const Geo& g = L.g;
+  return BwGeo{g.N, g.C, g.K, g.H, g.W, g.pad, g.Ho, g.Wo, g.th, g.tw, g.TP, g.T, g.Cp, g.Kp, g.ipg, L.groups};
+}
+
+int wl_backward_workspace_size(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* bytes) {
+  if (!plan || !bytes) return fail(WL_ERR_ARG, "NULL argument");
+  int rc = check_bits(q);
+  if (rc) return rc;
+  Layout L;
+  rc = make_layout(s, q, &L);
+  if (rc) return rc;
+  *bytes = wl_bw_workspace_bytes(bw_geo(L));
+  return WL_OK;
+}
+
+int wl_backward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* dy, const void* cache,
+                const void* fwd_workspace, float* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
+                void* stream) {
+  if (!plan || !dy || !cache || !fwd_workspace || !dx || !dw || !workspace) return fail(WL_ERR_ARG, "NULL argument");
+  int rc = check_bits(q);
+  if (rc) return rc;
+  Layout L;
+  rc = make_layout(s, q, &L);
+  if (rc) return rc;
+  const BwGeo bg = bw_geo(L);
+  if (workspace_bytes < wl_bw_workspace_bytes(bg)) return fail(WL_ERR_WORKSPACE, "backward workspace too small");
+  const uint8_t* fws = reinterpret_cast<const uint8_t*>(fwd_workspace);
+  const WeightHeader* wh = reinterpret_cast<const WeightHeader*>(cache);
+  const int8_t* U = reinterpret_cast<const int8_t*>(cache) + align256(sizeof(WeightHeader));
+  const Bits b = make_bits(q);
+  const int wstage = plan->mode == WL_LEGENDRE ? ST_WBC : ST_WT;
+  std::string err;
+  rc = wl_bw_run(bg, dy, U, wh->wacc, wstage, b.q[wstage], reinterpret_cast<const int8_t*>(fws + L.off_v),
+                 reinterpret_cast<const Acc*>(fws + L.off_acc), dx, dw, db, workspace, (cudaStream_t)stream, &err);
+  if (rc) return fail(rc, "backward: %s", err.c_str());
   return WL_OK;
 }
 

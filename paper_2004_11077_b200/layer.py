@@ -162,7 +162,7 @@ class QuantWinogradConv:
         return nbytes.value
 
     def forward(self, x: torch.Tensor, w: torch.Tensor, bias=None, padding: int = 0, scale_groups="image",
-                out: torch.Tensor | None = None) -> torch.Tensor:
+                out: torch.Tensor | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
         _check_conv_args(x, w)
         if w.shape[2] != 3:
             raise DimensionError(f"plan is for k=3, weights have k={w.shape[2]}")
@@ -176,7 +176,11 @@ class QuantWinogradConv:
             raise DimensionError(f"input {shape.h}x{shape.w} (pad {shape.pad}) is smaller than the 3x3 kernel")
         cache = self.wcache.get(self.dplan, self.qconfig, w)
         nbytes = self.workspace_bytes(shape)
-        if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
+        if workspace is not None:
+            if workspace.numel() < nbytes:
+                raise ValueError(f"workspace needs {nbytes} bytes")
+            self.ws = workspace
+        elif self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
             self.ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
         if out is None:
             out = torch.empty((shape.n, shape.c_out, ho, wo), dtype=torch.float32, device=x.device)
@@ -192,6 +196,24 @@ class QuantWinogradConv:
             _stream_ptr()), "wl_forward")
         self._last = (shape, cache)
         return out
+
+    def backward(self, dy: torch.Tensor, shape, cache: torch.Tensor, fwd_ws: torch.Tensor, need_bias: bool):
+        """STE gradients (dx, dw, db) of the forward that used `fwd_ws` (C ABI wl_backward)."""
+        dy = dy.contiguous().float()
+        qs = qcfg_struct(self.qconfig)
+        nbytes = ctypes.c_size_t()
+        _lib.check(_lib.lib().wl_backward_workspace_size(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs),
+                                                          ctypes.byref(nbytes)), "wl_backward_workspace_size")
+        bws = torch.empty(nbytes.value, dtype=torch.uint8, device=dy.device)
+        dx = torch.empty((shape.n, shape.c_in, shape.h, shape.w), dtype=torch.float32, device=dy.device)
+        dw = torch.empty((shape.c_out, shape.c_in, 3, 3), dtype=torch.float32, device=dy.device)
+        db = torch.empty((shape.c_out,), dtype=torch.float32, device=dy.device) if need_bias else None
+        _lib.check(_lib.lib().wl_backward(
+            self.dplan.handle, ctypes.byref(qs), ctypes.byref(shape), ctypes.c_void_p(dy.data_ptr()),
+            ctypes.c_void_p(cache.data_ptr()), ctypes.c_void_p(fwd_ws.data_ptr()), ctypes.c_void_p(dx.data_ptr()),
+            ctypes.c_void_p(dw.data_ptr()), ctypes.c_void_p(db.data_ptr() if db is not None else 0),
+            ctypes.c_void_p(bws.data_ptr()), nbytes.value, _stream_ptr()), "wl_backward")
+        return dx, dw, db
 
     def stats(self):
         """StageStat rows of the last forward (synchronises the stream)."""
@@ -232,6 +254,65 @@ class QuantWinogradConv:
         cin, cout = shape.c_in, shape.c_out
         ucodes = cache[cache.numel() - 36 * Kp * Cp:].view(torch.int8).view(Kp, 36, Cp).permute(1, 0, 2)
         return {"c0": c0[..., :cin], "V": V[..., :cin], "h": h[..., :cout], "U": ucodes[:, :cout, :cin]}
+
+
+class _QuantWinogradFn(torch.autograd.Function):
+    """Forward on the sm_100a path; straight-through-estimator backward."""
+
+    @staticmethod
+    def forward(ctx, x, w, bias, runner: QuantWinogradConv, padding: int, scale_groups: str):
+        shape = runner._shape(x, w, padding, scale_groups)
+        ws = torch.empty(runner.workspace_bytes(shape), dtype=torch.uint8, device=x.device)
+        y = runner.forward(x, w, bias=bias, padding=padding, scale_groups=scale_groups, workspace=ws)
+        shape_, cache = runner._last
+        ctx.runner, ctx.shape, ctx.has_bias = runner, shape_, bias is not None
+        ctx.save_for_backward(ws, cache)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        ws, cache = ctx.saved_tensors
+        dx, dw, db = ctx.runner.backward(dy, ctx.shape, cache, ws, ctx.has_bias)
+        return dx, dw, db, None, None, None
+
+
+def winograd_conv2d(x: torch.Tensor, w: torch.Tensor, bias, runner: QuantWinogradConv, padding: int = 1,
+                    scale_groups: str = "image") -> torch.Tensor:
+    """Differentiable quantized Winograd convolution (3x3, stride 1)."""
+    return _QuantWinogradFn.apply(x, w, bias, runner, padding, scale_groups)
+
+
+class WinogradAwareConv2d(torch.nn.Module):
+    """3x3 stride-1 convolution computed by the 8/9-bit quantized Winograd F(4,3) layer
+    (canonical or Legendre base) with a straight-through-estimator backward."""
+
+    def __init__(self, in_channels: int, out_channels: int, padding: int = 1, bias: bool = False,
+                 mode: str = "legendre", qconfig: QuantConfig | None = None, scale_groups: str = "image",
+                 plan: WinogradPlan | None = None):
+        super().__init__()
+        self.in_channels, self.out_channels, self.padding = in_channels, out_channels, padding
+        self.mode, self.scale_groups = mode, scale_groups
+        self.qconfig = QuantConfig.uniform(8) if qconfig is None else qconfig
+        self.plan = build_plan(4, 3, use_legendre=True) if plan is None else plan
+        _require_mode(self.plan, mode)
+        self.weight = torch.nn.Parameter(torch.empty(out_channels, in_channels, 3, 3))
+        torch.nn.init.kaiming_normal_(self.weight, mode="fan_in", nonlinearity="relu")
+        self.bias = torch.nn.Parameter(torch.zeros(out_channels)) if bias else None
+        self._runners: dict = {}
+
+    def _runner(self, device) -> QuantWinogradConv:
+        r = self._runners.get(device.index)
+        if r is None:
+            r = QuantWinogradConv(self.plan, self.mode, self.qconfig, device)
+            self._runners[device.index] = r
+        return r
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return winograd_conv2d(x, self.weight, self.bias, self._runner(x.device), self.padding, self.scale_groups)
+
+    def extra_repr(self) -> str:
+        return (f"{self.in_channels}, {self.out_channels}, padding={self.padding}, mode={self.mode}, "
+                f"qconfig={self.qconfig}, scale_groups={self.scale_groups}")
 
 
 _runners: dict = {}
