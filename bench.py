@@ -53,7 +53,8 @@ def kernel_units(name, n, c, k, hw, pad, hbytes=1):
     """Algorithmic (compulsory) bytes and int8 ops of one launch of each forward kernel."""
     ho = hw + 2 * pad - 2
     T = n * (-(-ho // 4)) ** 2
-    cp, kp = -(-c // 32) * 32, (64 if k <= 64 else 128 if k <= 128 else -(-k // 256) * 256)
+    p2 = lambda v, lo: lo if v <= lo else 1 << (v - 1).bit_length()  # noqa: E731  (wl_forward.cu pow2_at_least)
+    cp, kp = p2(c, 32), p2(k, 64)
     x, c0, V, U, h, y = 4 * n * c * hw * hw, n * hw * hw * cp, 36 * T * cp, 36 * kp * cp, 36 * T * kp * hbytes, 4 * n * k * ho * ho
     table = {
         "absmax_input": (x, 0), "quant_input": (x + c0, 0),
@@ -320,6 +321,51 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_train(args, rank, world, local_rank):
+    """Config 5: ResNet-18 with every 3x3 stride-1 conv on the Legendre 8b Winograd layer, one
+    training step (forward, STE backward, SGD momentum 0.9, lr 0.1) on 256 synthetic 3x32x32 images
+    per GPU; data parallel with one NCCL gradient all-reduce per step (DDP) when N > 1."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2004_11077_b200 import training as TR
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    torch.manual_seed(0)
+    model = TR.ResNet18(TR.winograd_conv_factory("legendre")).to(dev)
+    nwino = TR.count_winograd_layers(model)
+    net = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local_rank]) if world > 1 else model
+    opt = TR.make_optimizer(net, lr=0.1)
+    batch = 256
+    x, y = TR.synthetic_batch(batch, rank, seed=0, device=dev)
+    for _ in range(args.warmup):
+        TR.train_step(net, opt, x, y)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        loss = TR.train_step(net, opt, x, y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": "ResNet-18 (Winograd-aware Legendre 8b) training throughput", "value": world * batch / (ms * 1e-3),
+            "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8 fwd / fp32 bwd",
+            "data": "synthetic N(0,1) 3x32x32, uniform labels", "loss": float(loss),
+            "config": {"workload": "config5: ResNet-18 32x32, %d Winograd layers, batch 256/GPU, SGD m=0.9 lr=0.1"
+                       % nwino, "global_batch": world * batch, "parallelism": f"DDP x{world} (NCCL all-reduce)"},
+        }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -328,6 +374,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="layer", choices=["layer", "train"],
+                    help="layer: config-4 layer throughput (default); train: config-5 ResNet-18 training step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -342,7 +390,10 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, rank, world, local_rank)
+    if args.workload == "train":
+        run_train(args, rank, world, local_rank)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
 
