@@ -122,3 +122,155 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 }  // namespace wl
+
+namespace wl {
+
+// ----------------------------------------------------------------------------------------------
+// Persistent variant: one CTA per SM walks tiles (xi, m-block, n-block) round-robin.  TMEM holds two
+// BN-column accumulators so the 8 epilogue warps drain tile i while the MMA warp fills tile i+1 and
+// the TMA warp streams tile i+2's operands.  Barriers: smem ring full/empty[STAGES], accumulator
+// full[2] (tcgen05.commit) / empty[2] (8 epilogue-warp arrivals).
+constexpr int kGemmPThreads = 320;  // w0 TMA, w1 MMA + TMEM owner, w2..w9 epilogue
+
+template <int BN, int SW, int STAGES>
+struct GemmPSmem {
+  static constexpr int kA = 128 * SW;
+  static constexpr int kB = BN * SW;
+  static constexpr int kBytes = 1024 + STAGES * (kA + kB) + 512;
+};
+
+template <int BN, int SW, int STAGES, class Epi>
+__global__ void __launch_bounds__(kGemmPThreads, 1)
+    gemm_i8_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int T,
+                       int Kout, int Cpad, int Kpad, Epi epi) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using L = GemmPSmem<BN, SW, STAGES>;
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * L::kA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * L::kB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accfull = empty + STAGES;   // [2]
+  uint64_t* accempty = accfull + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kblocks = Cpad / SW;
+  const int mblocks = (T + 127) / 128, nblocks = Kpad / BN;
+  const int ntiles = 36 * mblocks * nblocks;
+  constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&accfull[a], 1);
+      mbar_init(&accempty[a], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // tile -> (xi, m-block, n-block); consecutive tiles of a CTA share xi where possible (U reuse in L2)
+  auto decode = [&](int tile, int& xi, int& mb, int& nb) {
+    nb = tile % nblocks;
+    const int r = tile / nblocks;
+    mb = r % mblocks;
+    xi = r / mblocks;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int xi, mb, nb;
+        decode(tile, xi, mb, nb);
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], L::kA + L::kB);
+          tma_load_3d(sA + s * L::kA, &tmA, &full[s], kb * SW, xi, mb * 128);
+          tma_load_3d(sB + s * L::kB, &tmB, &full[s], kb * SW, xi, nb * BN);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_i8(128, BN);
+      int it = 0, local = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
+        const int a = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        mbar_wait(&accempty[a], aph ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem_base + (uint32_t)(a * BN);
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < SW / 32; ++k) {
+            const uint64_t ad = smem_desc_kmajor(sA + s * L::kA + k * 32, SW);
+            const uint64_t bd = smem_desc_kmajor(sB + s * L::kB + k * 32, SW);
+            umma_i8(dacc, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&accfull[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int ew = warp - 2;          // 0..7
+    const int q = warp & 3;           // TMEM lane quarter this warp may access
+    const int half = ew >> 2;         // column half of the tile
+    constexpr int HC = BN / 2;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
+      int xi, mb, nb;
+      decode(tile, xi, mb, nb);
+      const int a = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&accfull[a], aph);
+      tc_fence_after();
+      const int row = mb * 128 + 32 * q + lane;
+      const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + (uint32_t)(a * BN + half * HC);
+      const int n0 = nb * BN + half * HC;
+      epi.begin(xi, row, row < T);
+#pragma unroll 1
+      for (int c = 0; c < HC; c += 32) {
+        uint32_t r0[16], r1[16];
+        tmem_ld16(taddr + c, r0);
+        tmem_ld16(taddr + c + 16, r1);
+        tmem_ld_wait();
+        const int col = n0 + c;
+        const int nv0 = Kout - col, nv1 = Kout - col - 16;
+        if (row < T && nv0 > 0) epi.apply(xi, row, col, r0, nv0 > 16 ? 16 : nv0);
+        if (row < T && nv1 > 0) epi.apply(xi, row, col + 16, r1, nv1 > 16 ? 16 : nv1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty[a]);
+      epi.finish_chunk(xi, row, row < T, nb * 2 + half);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace wl

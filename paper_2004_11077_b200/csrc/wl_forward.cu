@@ -183,7 +183,7 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   o = align256(o + (size_t)36 * g.T * g.Cp);
   L->off_c4 = o;
   o = align256(o + (size_t)36 * g.T * g.Kp);
-  L->bn = g.Kp >= 128 ? 128 : g.Kp;
+  L->bn = (g.Kp >= 256 ? 256 : g.Kp) / 2;  // table chunk = half the GEMM N tile
   const size_t CB = (g.C + 31) / 32, KB = (g.K + 31) / 32;
   const size_t ents[kNumTables] = {g.T * CB, g.T * CB, (size_t)36 * g.T * (g.Kp / L->bn), g.T * KB, g.T * KB};
   for (int i = 0; i < kNumTables; ++i) {
@@ -258,8 +258,8 @@ struct EpiHadMax {
       }
     }
   }
-  __device__ __forceinline__ void finish(int xi, int row, bool valid) {
-    if (valid) table[((size_t)xi * g.T + row) * nchunk + blockIdx.y] = (unsigned)m;
+  __device__ __forceinline__ void finish_chunk(int xi, int row, bool valid, int chunk) {
+    if (valid) table[((size_t)xi * g.T + row) * nchunk + chunk] = (unsigned)m;
     bool uniform;
     long long wmax;
     Acc* a = acc + ST_HAD;
@@ -317,21 +317,33 @@ struct EpiHadRq {
       reinterpret_cast<int4*>(dst)[1] = reinterpret_cast<const int4*>(out)[1];
     }
   }
-  __device__ __forceinline__ void finish(int, int, bool) {}
+  __device__ __forceinline__ void finish_chunk(int, int, bool, int) {}
 };
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
 
 template <int BN, int SW, class Epi>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo& g, const Epi& e, cudaStream_t st) {
-  constexpr int STAGES = 3;
-  using L = GemmSmem<BN, SW, STAGES>;
-  auto kern = gemm_i8_kernel<BN, SW, STAGES, Epi>;
+  constexpr int STAGES = 4;
+  using L = GemmPSmem<BN, SW, STAGES>;
+  auto kern = gemm_i8_persistent<BN, SW, STAGES, Epi>;
   static bool attr_set = false;  // per instantiation; idempotent
   if (!attr_set) {
     WL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes));
     attr_set = true;
   }
-  dim3 grid((g.T + 127) / 128, g.Kp / BN, 36);
-  kern<<<grid, kGemmThreads, L::kBytes, st>>>(ta, tb, g.T, g.K, g.Cp, e);
+  const int ntiles = 36 * ((g.T + 127) / 128) * (g.Kp / BN);
+  const int grid = std::min(ntiles, num_sms());
+  kern<<<grid, kGemmPThreads, L::kBytes, st>>>(ta, tb, g.T, g.K, g.Cp, g.Kp, e);
   WL_CUDA(cudaGetLastError());
   return WL_OK;
 }
@@ -341,13 +353,16 @@ static int dispatch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo
                          cudaStream_t st) {
 #define WL_G(BN_, SW_) \
   if (bn == BN_ && sw == SW_) return launch_gemm<BN_, SW_, Epi>(ta, tb, g, e, st);
-  WL_G(64, 32) WL_G(64, 64) WL_G(64, 128) WL_G(128, 32) WL_G(128, 64) WL_G(128, 128)
+  WL_G(64, 32) WL_G(64, 64) WL_G(64, 128) WL_G(128, 32) WL_G(128, 64) WL_G(128, 128) WL_G(256, 32) WL_G(256, 64)
+  WL_G(256, 128)
 #undef WL_G
   return fail(WL_ERR_ARG, "no GEMM tile for BN=%d SW=%d", bn, sw);
 }
 
+// N tile = whole padded Kout up to 256 (2 TMEM accumulators of BN columns); the max tables hold one
+// entry per half tile (BN/2 columns), the epilogue warps' column split.
 static void gemm_tiles(const Geo& g, int* bn, int* sw) {
-  *bn = g.Kp >= 128 ? 128 : g.Kp;  // must match Layout::bn
+  *bn = g.Kp >= 256 ? 256 : g.Kp;  // must match Layout::bn
   *sw = g.Cp % 128 == 0 ? 128 : (g.Cp % 64 == 0 ? 64 : 32);
 }
 
@@ -658,11 +673,11 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     e.acc = acc;
     e.table = tabs.t[ST_HAD];
     e.g = g;
-    e.nchunk = g.Kp / bn;
+    e.nchunk = g.Kp / L.bn;
     rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
     if (rc) return rc;
     finalize_hadamard_kernel<<<fin_blocks, 256, 0, st>>>(U, V, g, acc, wh->wacc, wstage, qu, b.q[ST_IT],
-                                                         tabs.t[ST_HAD], bn);
+                                                         tabs.t[ST_HAD], L.bn);
     stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_HAD, b.q[ST_HAD], 0.f);
     prof_mark("gemm_hadamard_max", st);
   }
