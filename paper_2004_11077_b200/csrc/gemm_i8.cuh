@@ -132,11 +132,12 @@ namespace wl {
 // full[2] (tcgen05.commit) / empty[2] (8 epilogue-warp arrivals).
 constexpr int kGemmPThreads = 320;  // w0 TMA, w1 MMA + TMEM owner, w2..w9 epilogue
 
-template <int BN, int SW, int STAGES>
+template <int BN, int SW, int STAGES, int EPI_STAGE = 0>
 struct GemmPSmem {
   static constexpr int kA = 128 * SW;
   static constexpr int kB = BN * SW;
-  static constexpr int kBytes = 1024 + STAGES * (kA + kB) + 512;
+  static constexpr int kEpi = 8 * EPI_STAGE;  // per-epilogue-warp staging bytes
+  static constexpr int kBytes = 1024 + STAGES * (kA + kB) + 512 + kEpi;
 };
 
 template <int BN, int SW, int STAGES, class Epi>
@@ -145,10 +146,11 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
                        int Kout, int Cpad, int Kpad, Epi epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  using L = GemmPSmem<BN, SW, STAGES>;
+  using L = GemmPSmem<BN, SW, STAGES, Epi::kStageBytes>;
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * L::kA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * L::kB);
+  uint8_t* sEpi = sB + STAGES * L::kB;  // 8 x Epi::kStageBytes (16-byte aligned)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + L::kEpi);
   uint64_t* empty = full + STAGES;
   uint64_t* accfull = empty + STAGES;   // [2]
   uint64_t* accempty = accfull + 2;     // [2]
@@ -236,6 +238,7 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const int half = ew >> 2;         // column half of the tile
     constexpr int HC = BN / 2;
+    if constexpr (Epi::kStageBytes > 0) epi.set_stage(sEpi + ew * Epi::kStageBytes, HC);
     int local = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
       int xi, mb, nb;
@@ -263,6 +266,7 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&accempty[a]);
       epi.finish_chunk(xi, row, row < T, nb * 2 + half);
+      if constexpr (Epi::kStageBytes > 0) epi.flush(xi, mb * 128 + 32 * q, n0, HC, T, lane);
     }
   }
   tc_fence_before();

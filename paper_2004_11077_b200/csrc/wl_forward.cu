@@ -238,27 +238,35 @@ static int dispatch_ld_out(int ld, F&& f) {
 // reduced in place (atomicMax) and units that may hold the argmax are pushed as candidates for the
 // fp64 replay in finalize_hadamard_kernel.
 struct EpiHadMax {
+  static constexpr int kStageBytes = 0;
   Acc* acc;
   unsigned* table;
   Geo g;
   int nchunk;
   long long m;
+  int vmax, vmin;
   int grp;
   __device__ __forceinline__ void begin(int, int row, bool valid) {
-    m = 0;
+    vmax = 0;
+    vmin = 0;
     grp = valid ? (row / g.TP) / g.ipg : -1;
   }
   __device__ __forceinline__ void apply(int, int, int, const uint32_t* v, int n) {
+    if (n == 16) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j < n) {
-        const int x = (int)v[j];
-        const long long a = x < 0 ? -(long long)x : (long long)x;
-        m = a > m ? a : m;
+      for (int j = 0; j < 16; j += 2) {
+        vmax = __vimax3_s32(vmax, (int)v[j], (int)v[j + 1]);
+        vmin = __vimin3_s32(vmin, (int)v[j], (int)v[j + 1]);
+      }
+    } else {
+      for (int j = 0; j < n; ++j) {
+        vmax = max(vmax, (int)v[j]);
+        vmin = min(vmin, (int)v[j]);
       }
     }
   }
   __device__ __forceinline__ void finish_chunk(int xi, int row, bool valid, int chunk) {
+    m = max((long long)vmax, -(long long)vmin);
     if (valid) table[((size_t)xi * g.T + row) * nchunk + chunk] = (unsigned)m;
     bool uniform;
     long long wmax;
@@ -274,6 +282,16 @@ struct EpiHadMax {
 // decision, and exact ties are replayed in fp64 from the U and V codes.
 template <typename HT>
 struct EpiHadRq {
+  // each epilogue warp stages its 32 rows x 128 columns of codes (swizzled 16-byte slots) and
+  // writes them back as whole row segments
+  static constexpr int kStageBytes = 32 * 128 * (int)sizeof(HT);
+  static constexpr int kRowBytes = 128 * (int)sizeof(HT);
+  uint8_t* stage;
+  int hc;  // columns per epilogue warp (half the N tile)
+  __device__ __forceinline__ void set_stage(uint8_t* p, int half_cols) {
+    stage = p;
+    hc = half_cols;
+  }
   Acc* acc;
   const Acc* wacc;
   const int8_t* U;
@@ -282,20 +300,34 @@ struct EpiHadRq {
   Geo g;
   int wstage, qmax_u, qmax_v, qmax_h;
   StageF s;
+  float r_lo, r_hi;
   int grp;
+  bool small;  // |I| < 2^22: int -> float by the magic-number add instead of I2F
   __device__ __forceinline__ void begin(int, int row, bool valid) {
     grp = valid ? (row / g.TP) / g.ipg : 0;
     const Acc& a = acc[(size_t)grp * ST_COUNT + ST_HAD];
     s.r = a.r;
-    s.band = 0.5f - a.thr;  // exact int32 accumulator: only the r / fma slack
+    s.band = 0.5f - a.thr;
     s.qmax = qmax_h;
+    // r = fl(qmax/M) is within 2^-24 (relative) of qmax/M, so [r_lo, r_hi] brackets it; I is exact,
+    // hence rn(I*r_lo) == rn(I*r_hi) proves the half-even code of I*qmax/M (an exact tie always
+    // splits the bracket since I != 0 then).
+    r_lo = __fmul_rd(a.r, 1.f - 2.384185791015625e-7f);
+    r_hi = __fmul_ru(a.r, 1.f + 2.384185791015625e-7f);
+    small = (long long)g.C * qmax_u * qmax_v < (1LL << 22);
   }
   __device__ __forceinline__ void apply(int xi, int row, int col, const uint32_t* v, int n) {
     HT out[16];
-    float dmax = 0.f;
+    uint32_t diff = 0;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) out[j] = (HT)rq_fast((float)(int)v[j], s, dmax);
-    if (dmax > 0.5f - s.band) {
+    for (int j = 0; j < 16; ++j) {
+      const float fi = small ? __int_as_float((int)v[j] + 0x4B400000) - kMagic : (float)(int)v[j];
+      const uint32_t y1 = __float_as_uint(fmaf(fi, r_lo, kMagic));
+      const uint32_t y2 = __float_as_uint(fmaf(fi, r_hi, kMagic));
+      diff |= y1 ^ y2;
+      out[j] = (HT)(int)y1;  // low byte / half-word of 0x4B400000 + code is the two's-complement code
+    }
+    if (diff != 0) {
       const StageQ q = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h);
       for (int j = 0; j < 16; ++j) {
         bool tie = false;
@@ -309,15 +341,33 @@ struct EpiHadRq {
         out[j] = (HT)code;
       }
     }
-    HT* dst = h + ((size_t)row * 36 + xi) * g.Kp + col;
-    if (sizeof(HT) == 1) {
-      *reinterpret_cast<int4*>(dst) = *reinterpret_cast<const int4*>(out);
-    } else {
-      reinterpret_cast<int4*>(dst)[0] = reinterpret_cast<const int4*>(out)[0];
-      reinterpret_cast<int4*>(dst)[1] = reinterpret_cast<const int4*>(out)[1];
+    // stage: row `lane` of this warp, 16-byte slot (column offset within the half / 16 bytes)
+    const int lane = threadIdx.x & 31;
+    const int slot0 = ((col % hc) * (int)sizeof(HT)) >> 4;
+#pragma unroll
+    for (int v = 0; v < (int)sizeof(HT); ++v) {
+      const int slot = slot0 + v;
+      *reinterpret_cast<int4*>(stage + lane * kRowBytes + ((slot ^ (lane & 7)) << 4)) =
+          reinterpret_cast<const int4*>(out)[v];
     }
   }
   __device__ __forceinline__ void finish_chunk(int, int, bool, int) {}
+  // write the warp's 32 staged rows: each instruction covers whole 128/256-byte row segments
+  __device__ __forceinline__ void flush(int xi, int row0, int n0, int hc, int T, int lane) {
+    __syncwarp();
+    constexpr int kSlots = kRowBytes / 16;
+    constexpr int kRowsPerInstr = 32 / kSlots;
+    const int nbytes = min(hc, g.K - n0) * (int)sizeof(HT);  // valid bytes of each row segment
+    for (int r0 = 0; r0 < 32; r0 += kRowsPerInstr) {
+      const int r = r0 + lane / kSlots, sl = lane % kSlots;
+      const int row = row0 + r;
+      if (row < T && sl * 16 < nbytes) {
+        const int4 v = *reinterpret_cast<const int4*>(stage + r * kRowBytes + ((sl ^ (r & 7)) << 4));
+        *reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(h + ((size_t)row * 36 + xi) * g.Kp + n0) + sl * 16) = v;
+      }
+    }
+    __syncwarp();
+  }
 };
 
 static int num_sms() {
@@ -333,8 +383,8 @@ static int num_sms() {
 
 template <int BN, int SW, class Epi>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo& g, const Epi& e, cudaStream_t st) {
-  constexpr int STAGES = 4;
-  using L = GemmPSmem<BN, SW, STAGES>;
+  constexpr int STAGES = Epi::kStageBytes > 0 ? 3 : 4;
+  using L = GemmPSmem<BN, SW, STAGES, Epi::kStageBytes>;
   auto kern = gemm_i8_persistent<BN, SW, STAGES, Epi>;
   static bool attr_set = false;  // per instantiation; idempotent
   if (!attr_set) {
