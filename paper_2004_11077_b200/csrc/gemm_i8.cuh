@@ -130,13 +130,15 @@ namespace wl {
 // BN-column accumulators so the 8 epilogue warps drain tile i while the MMA warp fills tile i+1 and
 // the TMA warp streams tile i+2's operands.  Barriers: smem ring full/empty[STAGES], accumulator
 // full[2] (tcgen05.commit) / empty[2] (8 epilogue-warp arrivals).
-constexpr int kGemmPThreads = 320;  // w0 TMA, w1 MMA + TMEM owner, w2..w9 epilogue
+constexpr int kEpiGroups = 4;                          // column groups per TMEM lane quarter
+constexpr int kEpiWarps = 4 * kEpiGroups;              // 16 epilogue warps
+constexpr int kGemmPThreads = 64 + 32 * kEpiWarps;     // w0 TMA, w1 MMA + TMEM owner, w2.. epilogue
 
 template <int BN, int SW, int STAGES, int EPI_STAGE = 0>
 struct GemmPSmem {
   static constexpr int kA = 128 * SW;
   static constexpr int kB = BN * SW;
-  static constexpr int kEpi = 8 * EPI_STAGE;  // per-epilogue-warp staging bytes
+  static constexpr int kEpi = kEpiWarps * EPI_STAGE;  // per-epilogue-warp staging bytes
   static constexpr int kBytes = 1024 + STAGES * (kA + kB) + 512 + kEpi;
 };
 
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
   using L = GemmPSmem<BN, SW, STAGES, Epi::kStageBytes>;
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * L::kA;
-  uint8_t* sEpi = sB + STAGES * L::kB;  // 8 x Epi::kStageBytes (16-byte aligned)
+  uint8_t* sEpi = sB + STAGES * L::kB;  // kEpiWarps x Epi::kStageBytes (16-byte aligned)
   uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + L::kEpi);
   uint64_t* empty = full + STAGES;
   uint64_t* accfull = empty + STAGES;   // [2]
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&accfull[a], 1);
-      mbar_init(&accempty[a], 8);
+      mbar_init(&accempty[a], kEpiWarps);
     }
     fence_mbar_init();
   }
@@ -234,10 +236,10 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
     }
     __syncwarp();
   } else {
-    const int ew = warp - 2;          // 0..7
+    const int ew = warp - 2;          // 0..kEpiWarps-1
     const int q = warp & 3;           // TMEM lane quarter this warp may access
-    const int half = ew >> 2;         // column half of the tile
-    constexpr int HC = BN / 2;
+    const int half = ew >> 2;         // column group of the tile
+    constexpr int HC = BN / kEpiGroups;
     if constexpr (Epi::kStageBytes > 0) epi.set_stage(sEpi + ew * Epi::kStageBytes, HC);
     int local = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
@@ -251,21 +253,22 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
       const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + (uint32_t)(a * BN + half * HC);
       const int n0 = nb * BN + half * HC;
       epi.begin(xi, row, row < T);
+      static_assert(HC % 16 == 0, "epilogue column group must be a multiple of 16");
 #pragma unroll 1
       for (int c = 0; c < HC; c += 32) {
         uint32_t r0[16], r1[16];
         tmem_ld16(taddr + c, r0);
-        tmem_ld16(taddr + c + 16, r1);
+        if (c + 16 < HC) tmem_ld16(taddr + c + 16, r1);
         tmem_ld_wait();
         const int col = n0 + c;
         const int nv0 = Kout - col, nv1 = Kout - col - 16;
         if (row < T && nv0 > 0) epi.apply(xi, row, col, r0, nv0 > 16 ? 16 : nv0);
-        if (row < T && nv1 > 0) epi.apply(xi, row, col + 16, r1, nv1 > 16 ? 16 : nv1);
+        if (c + 16 < HC && row < T && nv1 > 0) epi.apply(xi, row, col + 16, r1, nv1 > 16 ? 16 : nv1);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&accempty[a]);
-      epi.finish_chunk(xi, row, row < T, nb * 2 + half);
+      epi.finish_chunk(xi, row, row < T, nb * kEpiGroups + half);
       if constexpr (Epi::kStageBytes > 0) epi.flush(xi, mb * 128 + 32 * q, n0, HC, T, lane);
     }
   }

@@ -183,7 +183,7 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   o = align256(o + (size_t)36 * g.T * g.Cp);
   L->off_c4 = o;
   o = align256(o + (size_t)36 * g.T * g.Kp);
-  L->bn = (g.Kp >= 256 ? 256 : g.Kp) / 2;  // table chunk = half the GEMM N tile
+  L->bn = (g.Kp >= 256 ? 256 : g.Kp) / kEpiGroups;  // table chunk = one epilogue warp's columns
   const size_t CB = (g.C + 31) / 32, KB = (g.K + 31) / 32;
   const size_t ents[kNumTables] = {g.T * CB, g.T * CB, (size_t)36 * g.T * (g.Kp / L->bn), g.T * KB, g.T * KB};
   for (int i = 0; i < kNumTables; ++i) {
@@ -259,10 +259,12 @@ struct EpiHadMax {
         vmin = __vimin3_s32(vmin, (int)v[j], (int)v[j + 1]);
       }
     } else {
-      for (int j = 0; j < n; ++j) {
-        vmax = max(vmax, (int)v[j]);
-        vmin = min(vmin, (int)v[j]);
-      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < n) {
+          vmax = max(vmax, (int)v[j]);
+          vmin = min(vmin, (int)v[j]);
+        }
     }
   }
   __device__ __forceinline__ void finish_chunk(int xi, int row, bool valid, int chunk) {
@@ -284,8 +286,9 @@ template <typename HT>
 struct EpiHadRq {
   // each epilogue warp stages its 32 rows x 128 columns of codes (swizzled 16-byte slots) and
   // writes them back as whole row segments
-  static constexpr int kStageBytes = 32 * 128 * (int)sizeof(HT);
-  static constexpr int kRowBytes = 128 * (int)sizeof(HT);
+  static constexpr int kStageBytes = 32 * 64 * (int)sizeof(HT);
+  static constexpr int kRowBytes = 64 * (int)sizeof(HT);
+  static constexpr int kSwz = kRowBytes / 16 - 1;  // XOR swizzle of the 16-byte slots within a row
   uint8_t* stage;
   int hc;  // columns per epilogue warp (half the N tile)
   __device__ __forceinline__ void set_stage(uint8_t* p, int half_cols) {
@@ -329,6 +332,7 @@ struct EpiHadRq {
     }
     if (diff != 0) {
       const StageQ q = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h);
+#pragma unroll
       for (int j = 0; j < 16; ++j) {
         bool tie = false;
         int code = rq((long long)(int)v[j], q, tie);
@@ -347,7 +351,7 @@ struct EpiHadRq {
 #pragma unroll
     for (int v = 0; v < (int)sizeof(HT); ++v) {
       const int slot = slot0 + v;
-      *reinterpret_cast<int4*>(stage + lane * kRowBytes + ((slot ^ (lane & 7)) << 4)) =
+      *reinterpret_cast<int4*>(stage + lane * kRowBytes + ((slot ^ (lane & kSwz)) << 4)) =
           reinterpret_cast<const int4*>(out)[v];
     }
   }
@@ -362,7 +366,7 @@ struct EpiHadRq {
       const int r = r0 + lane / kSlots, sl = lane % kSlots;
       const int row = row0 + r;
       if (row < T && sl * 16 < nbytes) {
-        const int4 v = *reinterpret_cast<const int4*>(stage + r * kRowBytes + ((sl ^ (r & 7)) << 4));
+        const int4 v = *reinterpret_cast<const int4*>(stage + r * kRowBytes + ((sl ^ (r & kSwz)) << 4));
         *reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(h + ((size_t)row * 36 + xi) * g.Kp + n0) + sl * 16) = v;
       }
     }
@@ -410,7 +414,7 @@ static int dispatch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo
 }
 
 // N tile = whole padded Kout up to 256 (2 TMEM accumulators of BN columns); the max tables hold one
-// entry per half tile (BN/2 columns), the epilogue warps' column split.
+// entry per epilogue warp's column group (BN / kEpiGroups columns).
 static void gemm_tiles(const Geo& g, int* bn, int* sw) {
   *bn = g.Kp >= 256 ? 256 : g.Kp;  // must match Layout::bn
   *sw = g.Cp % 128 == 0 ? 128 : (g.Cp % 64 == 0 ? 64 : 32);
