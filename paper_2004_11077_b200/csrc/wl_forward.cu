@@ -136,7 +136,7 @@ static const int kTableStage[kNumTables] = {ST_IBC, ST_IT, ST_HAD, ST_OBC, ST_OU
 
 struct Layout {
   Geo g;
-  size_t off_acc, off_c0, off_v, off_h, off_c1, off_c4, off_tab[kNumTables], tab_bytes[kNumTables], total;
+  size_t off_acc, off_c0, off_v, off_h, off_c1, off_c4, off_tab[kNumTables], tab_bytes[kNumTables], off_otab, total;
   int groups, hbytes, bn;
 };
 
@@ -191,6 +191,9 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
     L->tab_bytes[i] = ents[i] * sizeof(unsigned);
     o = align256(o + L->tab_bytes[i]);
   }
+  // dequantised output table (output widths <= 12 bits; wider widths dequantise in fp64 inline)
+  L->off_otab = o;
+  if (q->output_transform_bits <= 12) o = align256(o + sizeof(float) * (size_t)L->groups * ((1 << q->output_transform_bits) - 1));
   L->total = o;
   return WL_OK;
 }
@@ -626,12 +629,12 @@ int wl_debug_layout(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, si
   return WL_OK;
 }
 
-int wl_forward_launches(const wl_plan* plan, const wl_shape*, const wl_qcfg*) {
+int wl_forward_launches(const wl_plan* plan, const wl_shape*, const wl_qcfg* q) {
   if (!plan) return WL_ERR_ARG;
-  // absmax, quant, input passes (2|3), gemm max, gemm requant, output passes (2|3)
-  // absmax, quant, then (Legendre) in_a + fin, in_b + fin, in_c, gemm + fin, gemm, out_a + fin, out_b + fin,
-  // out_c  | (canonical) in_a + fin, in_c, gemm + fin, gemm, out_a + fin, out_c
-  return plan->mode == WL_LEGENDRE ? 17 : 12;
+  // absmax, quant, [in_a, finalize, params] x2|1, in_c, gemm max, finalize, params, gemm codes,
+  // [out_a|out_b, finalize, params] x2|1, output table, out_c
+  const int otab = (q && q->output_transform_bits <= 12) ? 1 : 0;
+  return (plan->mode == WL_LEGENDRE ? 20 : 14) + otab;
 }
 
 int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
@@ -767,6 +770,12 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
 
   const long long oc = (long long)g.T * g.K;
   const unsigned ogrid = (unsigned)((oc + tb - 1) / tb);
+  float* otab = q->output_transform_bits <= 12 ? reinterpret_cast<float*>(ws + L.off_otab) : nullptr;
+  auto make_otab = [&]() {
+    if (!otab) return;
+    const long long n = (long long)L.groups * (2 * b.q[ST_OUT] + 1);
+    out_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(acc, L.groups, b.q[ST_OUT], otab);
+  };
   auto run_out = [&](auto ldc, auto ht) {
     constexpr int LD = decltype(ldc)::value;
     using HT = decltype(ht);
@@ -776,7 +785,8 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
       finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
       stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
       prof_mark("output_max", st);
-      out_c_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf);
+      make_otab();
+      out_c_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
       prof_mark("output_write", st);
     } else {
       out_a_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
@@ -787,7 +797,8 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
       finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
       stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
       prof_mark("output_max", st);
-      out_c_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf);
+      make_otab();
+      out_c_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
       prof_mark("output_write", st);
     }
   };

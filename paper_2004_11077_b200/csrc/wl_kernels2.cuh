@@ -197,6 +197,18 @@ __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage
   a.scale = maxabs > 0.0 ? maxabs / (double)qmax : 1.0;
 }
 
+// Dequantised fp32 output of every code of the output stage, per group (quantize.py:120-125:
+// code * scale in fp64, +-qmax snapped to +-max_abs, then rounded to fp32): table[g][code + qmax].
+__global__ void out_table_kernel(const Acc* __restrict__ acc, int groups, int qmax, float* __restrict__ table) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int width = 2 * qmax + 1;
+  if (idx >= (long long)groups * width) return;
+  const int gi = (int)(idx / width), code = (int)(idx % width) - qmax;
+  const Acc& a = acc[(size_t)gi * ST_COUNT + ST_OUT];
+  const double maxabs = __longlong_as_double((long long)a.F);
+  table[idx] = code == qmax ? (float)maxabs : (code == -qmax ? (float)-maxabs : (float)((double)code * a.scale));
+}
+
 // ---------------------------------------------------------------------------------- input side
 
 // First input stage maximum: canonical input_transform (B^T), Legendre input_base_change (P^-T).
@@ -468,7 +480,8 @@ __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restric
 template <int MODE, typename HT, int LD>
 __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
                                                     float* __restrict__ y, const float* __restrict__ bias, Geo g,
-                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf) {
+                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
+                                                    const float* __restrict__ otab) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (uint32_t)g.T * (uint32_t)g.K) return;
   const int k = (int)(idx % (uint32_t)g.K), t = (int)(idx / (uint32_t)g.K);
@@ -485,7 +498,9 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
   float Yo[4][4];
   float X[6][6];
   float dmax = 0.f, kd;
+  const float* tabg = otab ? otab + (size_t)grp * (2 * qo + 1) + qo : nullptr;
   auto deqf = [=](int code) {
+    if (tabg) return __ldg(tabg + code);
     return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
   };
   using LOT = std::conditional_t<MODE == 0, tab::Can_OT, tab::Leg_OT>;
