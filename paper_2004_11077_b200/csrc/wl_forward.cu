@@ -16,6 +16,7 @@
 #include "gemm_i8.cuh"
 #include "wl_backward.h"
 #include "wl_kernels2.cuh"
+#include "wl_staged.cuh"
 #include "wl_tmap.h"
 
 using namespace wl;
@@ -73,7 +74,20 @@ void prof_begin() {
   g_prof.calls.emplace_back();
   g_prof.cur = &g_prof.calls.back();
 }
+// WL_DEBUG_SYNC=1: synchronise after every marked kernel group and report the first failing one.
+const char* g_debug_fail = nullptr;
+bool debug_sync_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("WL_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 void prof_mark(const char* name, cudaStream_t st) {
+  if (debug_sync_enabled() && !g_debug_fail) {
+    if (cudaStreamSynchronize(st) != cudaSuccess) g_debug_fail = name;
+  }
   if (!g_prof.on || !g_prof.cur) return;
   cudaEvent_t e;
   cudaEventCreate(&e);
@@ -208,6 +222,21 @@ static size_t weight_cache_bytes(int K, int C, int* Kp, int* Cp) {
   *Cp = pow2_at_least(C, 32);
   *Kp = pow2_at_least(K, 64);
   return align256(sizeof(WeightHeader)) + (size_t)36 * (*Kp) * (*Cp);
+}
+
+// Persistent grid for a staged kernel: resident blocks per SM (occupancy query, cached) x SMs.
+template <class K>
+static int staged_grid(K kern, int threads, int smem, long long work_items) {
+  static int per_sm = 0;  // per instantiation
+  if (!per_sm) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int dev_sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+  return (int)std::max(1LL, std::min<long long>(work_items, (long long)per_sm * dev_sms));
 }
 
 // ------------------------------------------------------------------ compile-time strides
@@ -691,26 +720,59 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
   const unsigned tgrid = (unsigned)((tc + tb - 1) / tb);
   const int fin_blocks = 4 * 148;
   const int pgrid = (L.groups + 127) / 128;
+  const bool staged_in = !getenv("WL_NO_STAGED_IN"), staged_out = !getenv("WL_NO_STAGED_OUT");  // debug switches
+  CUtensorMap c0map;
+  if (g.Cp <= 256 && !make_tmap_i8_4d(&c0map, c0, g.Cp, g.W, g.H, g.N, g.Cp, 6, 6))
+    return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled (input window) failed");
   rc = dispatch_ld_in(g.Cp, [&](auto ldc) {
     constexpr int LD = decltype(ldc)::value;
-    if (!leg) {
-      in_a_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
-      finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
-      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
-      prof_mark("input_transform_max", st);
-      in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
-      prof_mark("input_transform_codes", st);
+    if (LD <= 256 && staged_in) {
+      using S = Staged<(LD <= 256 ? LD : 256), 1>;
+      constexpr int LDs = LD <= 256 ? LD : 256;
+      const long long iters = (g.T + S::TPB - 1) / S::TPB;
+      if (!leg) {
+        auto ka = sin_a_kernel<0, LDs>;
+        sin_a_kernel<0, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
+        finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+        prof_mark("input_transform_max", st);
+        // the code passes are store-bound: the plain grid (more resident warps) is faster than staging
+        in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+        prof_mark("input_transform_codes", st);
+      } else {
+        auto ka = sin_a_kernel<1, LDs>;
+        sin_a_kernel<1, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
+        finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
+        prof_mark("input_base_change_max", st);
+        auto kb = sin_b_kernel<LDs>;
+        sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs);
+        finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+        prof_mark("input_transform_max", st);
+        in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+        prof_mark("input_transform_codes", st);
+      }
     } else {
-      in_a_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
-      finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
-      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
-      prof_mark("input_base_change_max", st);
-      in_b_kernel<LD><<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs);
-      finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
-      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
-      prof_mark("input_transform_max", st);
-      in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
-      prof_mark("input_transform_codes", st);
+      if (!leg) {
+        in_a_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
+        finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+        prof_mark("input_transform_max", st);
+        in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+        prof_mark("input_transform_codes", st);
+      } else {
+        in_a_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
+        finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
+        prof_mark("input_base_change_max", st);
+        in_b_kernel<LD><<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs);
+        finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+        prof_mark("input_transform_max", st);
+        in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+        prof_mark("input_transform_codes", st);
+      }
     }
   });
   if (rc) return rc;
@@ -780,26 +842,56 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
     constexpr int LD = decltype(ldc)::value;
     using HT = decltype(ht);
     const HT* hh = reinterpret_cast<const HT*>(h);
-    if (!leg) {
-      out_a_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
-      finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
-      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
-      prof_mark("output_max", st);
-      make_otab();
-      out_c_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
-      prof_mark("output_write", st);
+    if (LD <= 256 && staged_out) {
+      constexpr int LDs = LD <= 256 ? LD : 256;
+      using SH = Staged<LDs, sizeof(HT)>;
+      const long long iters = (g.T + SH::TPB - 1) / SH::TPB;
+      if (!leg) {
+        auto ka = sout_a_kernel<0, HT, LDs>;
+        sout_a_kernel<0, HT, LDs><<<staged_grid(ka, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, g, acc, tabs);
+        finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+        prof_mark("output_max", st);
+        make_otab();
+        out_c_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        prof_mark("output_write", st);
+      } else {
+        auto ka = sout_a_kernel<1, HT, LDs>;
+        sout_a_kernel<1, HT, LDs><<<staged_grid(ka, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, g, acc, tabs);
+        finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
+        prof_mark("output_base_change_max", st);
+        auto kb = sout_b_kernel<HT, LDs>;
+        sout_b_kernel<HT, LDs><<<staged_grid(kb, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs);
+        finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+        prof_mark("output_max", st);
+        make_otab();
+        out_c_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        prof_mark("output_write", st);
+      }
     } else {
-      out_a_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
-      finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
-      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
-      prof_mark("output_base_change_max", st);
-      out_b_kernel<HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs);
-      finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
-      stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
-      prof_mark("output_max", st);
-      make_otab();
-      out_c_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
-      prof_mark("output_write", st);
+      if (!leg) {
+        out_a_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
+        finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+        prof_mark("output_max", st);
+        make_otab();
+        out_c_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        prof_mark("output_write", st);
+      } else {
+        out_a_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
+        finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
+        prof_mark("output_base_change_max", st);
+        out_b_kernel<HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs);
+        finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+        prof_mark("output_max", st);
+        make_otab();
+        out_c_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        prof_mark("output_write", st);
+      }
     }
   };
   rc = dispatch_ld_out(g.Kp, [&](auto ldc) {
@@ -811,6 +903,8 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
   if (rc) return rc;
 
   WL_CUDA(cudaGetLastError());
+  if (g_debug_fail) return fail(WL_ERR_CUDA, "kernel group '%s' failed: %s", g_debug_fail,
+                                cudaGetErrorString(cudaGetLastError()));
   return WL_OK;
 }
 
