@@ -76,7 +76,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -247,25 +247,24 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    # end to end through the public API with host buffers: pinned x -> device, forward, y -> pinned host
+    # end to end through the public API with host buffers: pinned x -> device, forward, y -> pinned host,
+    # copies inside the timed region (chunked so copy-in / compute / copy-out overlap; per-image scale
+    # groups make the chunks independent, results identical to one call)
     e2e = None
     if not args.no_e2e:
-        xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
-        xh.copy_(x)
-        yh = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
-        xd = torch.empty_like(x)
-        for _ in range(1):
-            xd.copy_(xh, non_blocking=True)
-            r.forward(xd, w, padding=pad, out=y)
-            yh.copy_(y, non_blocking=True)
+        del x
+        torch.cuda.empty_cache()
+        xh = torch.empty((n, c, hw, hw), dtype=torch.float32, pin_memory=True)
+        xh.normal_(generator=torch.Generator().manual_seed(1000 + rank))
+        yh = torch.empty(tuple(y.shape), dtype=torch.float32, pin_memory=True)
+        for _ in range(2):
+            r.forward_host(xh, w, yh, padding=pad)
         torch.cuda.synchronize()
         barrier()
         ke = max(1, min(args.steps, 5))
         e0.record(stream)
         for _ in range(ke):
-            xd.copy_(xh, non_blocking=True)
-            r.forward(xd, w, padding=pad, out=y)
-            yh.copy_(y, non_blocking=True)
+            r.forward_host(xh, w, yh, padding=pad)
         e1.record(stream)
         torch.cuda.synchronize()
         me = e0.elapsed_time(e1) / ke
@@ -274,9 +273,10 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             me = float(t.item())
         e2e = {"value": world * n / (me * 1e-3), "unit": "images/s",
-               "h2d_bytes_per_step": int(x.numel() * 4), "d2h_bytes_per_step": int(y.numel() * 4),
-               "ms_per_step": me, "path": "QuantWinogradConv.forward (C ABI wl_forward) with pinned host x/y"}
-        del xh, yh, xd
+               "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4),
+               "ms_per_step": me,
+               "path": "QuantWinogradConv.forward_host (C ABI wl_forward per chunk), pinned host x/y, 8 chunks"}
+        del xh, yh
 
     if rank != 0:
         return

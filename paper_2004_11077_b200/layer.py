@@ -197,6 +197,61 @@ class QuantWinogradConv:
         self._last = (shape, cache)
         return out
 
+    def forward_host(self, xh: torch.Tensor, w: torch.Tensor, yh: torch.Tensor, bias=None, padding: int = 0,
+                     chunks: int = 8) -> torch.Tensor:
+        """End-to-end call on HOST buffers (pinned for overlap): x [N,C,H,W] -> y [N,K,Ho,Wo] in place.
+
+        With per-image scale groups the batch splits exactly into independent chunks, so the copy
+        in of chunk i+1, the forward of chunk i and the copy out of chunk i-1 overlap on three
+        streams (per-chunk workspaces, shared weight cache)."""
+        if xh.is_cuda or yh.is_cuda:
+            raise ValueError("forward_host takes host tensors")
+        n = xh.shape[0]
+        chunks = max(1, min(chunks, n))
+        dev = w.device
+        bounds = [n * i // chunks for i in range(chunks + 1)]
+        cur = torch.cuda.current_stream(dev)
+        s_in, s_out = self._streams(dev)
+        if not hasattr(self, "_pool") or self._pool_key != (tuple(xh.shape), tuple(yh.shape), chunks):
+            mx = max(bounds[i + 1] - bounds[i] for i in range(chunks))
+            self._pool = [(torch.empty((mx,) + tuple(xh.shape[1:]), device=dev),
+                           torch.empty((mx,) + tuple(yh.shape[1:]), device=dev), None) for _ in range(2)]
+            self._pool_ws = [None, None]
+            self._pool_key = (tuple(xh.shape), tuple(yh.shape), chunks)
+        ev_in = [torch.cuda.Event() for _ in range(chunks)]
+        ev_comp = [torch.cuda.Event() for _ in range(chunks)]
+        ev_out = [torch.cuda.Event() for _ in range(chunks)]
+        self.wcache.get(self.dplan, self.qconfig, w.contiguous().float())
+        for i in range(chunks):
+            a, b = bounds[i], bounds[i + 1]
+            xd, yd, _ = self._pool[i % 2]
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev_comp[i - 2])   # buffer reuse: chunk i-2 consumed xd
+                xd[: b - a].copy_(xh[a:b], non_blocking=True)
+                ev_in[i].record(s_in)
+            cur.wait_event(ev_in[i])
+            if i >= 2:
+                cur.wait_event(ev_out[i - 2])          # yd of chunk i-2 copied out
+            shape = self._shape(xd[: b - a], w, padding, "image")
+            nbytes = self.workspace_bytes(shape)
+            k = i % 2
+            if self._pool_ws[k] is None or self._pool_ws[k].numel() < nbytes:
+                self._pool_ws[k] = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            self.forward(xd[: b - a], w, bias=bias, padding=padding, out=yd[: b - a], workspace=self._pool_ws[k])
+            ev_comp[i].record(cur)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_comp[i])
+                yh[a:b].copy_(yd[: b - a], non_blocking=True)
+                ev_out[i].record(s_out)
+        cur.wait_event(ev_out[chunks - 1])
+        return yh
+
+    def _streams(self, dev):
+        if not hasattr(self, "_aux_streams"):
+            self._aux_streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        return self._aux_streams
+
     def backward(self, dy: torch.Tensor, shape, cache: torch.Tensor, fwd_ws: torch.Tensor, need_bias: bool):
         """STE gradients (dx, dw, db) of the forward that used `fwd_ws` (C ABI wl_backward)."""
         dy = dy.contiguous().float()

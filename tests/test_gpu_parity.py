@@ -193,3 +193,15 @@ def test_identity_free_errors():
             x, torch.zeros((2, 4, 3, 3), device="cuda"))
     with pytest.raises(ValueError):
         W.QuantWinogradConv(W.build_plan(4, 3), "legendre", W.QuantConfig.uniform(8))
+
+
+def test_forward_host_chunked_equals_device_call():
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((10, 32, 14, 14)).astype(np.float32)
+    w = _kaiming(rng, 48, 32)
+    r, y = run_gpu(x, w, "legendre", W.QuantConfig.uniform(8), 1)
+    xh = torch.tensor(x).pin_memory()
+    yh = torch.empty(tuple(y.shape)).pin_memory()
+    r.forward_host(xh, torch.tensor(w, device="cuda"), yh, padding=1, chunks=4)
+    torch.cuda.synchronize()
+    assert torch.equal(yh, y.cpu())
