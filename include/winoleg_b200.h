@@ -70,11 +70,20 @@ int wl_plan_mode(const wl_plan* plan);
 int wl_weight_cache_size(const wl_plan* plan, int c_out, int c_in, size_t* bytes);
 int wl_weight_transform(const wl_plan* plan, const wl_qcfg* q, const float* w, int c_out, int c_in, void* cache,
                         size_t cache_bytes, void* stream);
+/* Same from fp64 weights: the reference's own operand dtype (pipeline.py:112-113 copies to fp64);
+ * the "weights" codes are rint(w / scale) in fp64 exactly as quantize.py:118-119. */
+int wl_weight_transform_f64(const wl_plan* plan, const wl_qcfg* q, const double* w, int c_out, int c_in, void* cache,
+                            size_t cache_bytes, void* stream);
 
 /* Forward: y [n][c_out][h+2pad-2][w+2pad-2] fp32 = dequantised output codes (+ bias if non-NULL). */
 int wl_workspace_size(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* bytes);
 int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
                const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream);
+/* fp64 in / fp64 out (quantize.py:129-148 returns fp64): x is quantised in fp64 as the reference
+ * does, so y is bit-identical to the reference's output for ANY fp64 input; all stages after
+ * "input" run on integer codes exactly as in wl_forward. Same workspace as wl_forward. */
+int wl_forward_f64(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const double* x, const void* cache,
+                   const double* bias, double* y, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Straight-through-estimator backward (no reference counterpart): casts are identity,
  * scales detached, products use the forward's quantised U and V.  fwd_workspace must be the

@@ -37,7 +37,7 @@ class wl_stage_stat(ctypes.Structure):
 _lib = None
 
 EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_mode", "wl_weight_cache_size", "wl_weight_transform",
-           "wl_workspace_size", "wl_forward", "wl_num_stages", "wl_read_stats", "wl_debug_layout",
+           "wl_weight_transform_f64", "wl_workspace_size", "wl_forward", "wl_forward_f64", "wl_num_stages", "wl_read_stats", "wl_debug_layout",
            "wl_forward_launches", "wl_profile_enable", "wl_profile_read", "wl_backward_workspace_size",
            "wl_backward", "wl_last_error")
 

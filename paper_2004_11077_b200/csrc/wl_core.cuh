@@ -20,7 +20,7 @@ enum StageId { ST_INPUT = 0, ST_WEIGHTS, ST_WT, ST_WBC, ST_IBC, ST_IT, ST_HAD, S
 // Per (group, stage) reduction slot: M = max |T| (integer stages) or fp32 bits of max |x| (input /
 // weights); F = fp64 bits of the reference's max_abs (positive doubles order like uint64).
 struct Acc {
-  unsigned long long M;   // exact integer max |T| (fp32 bits of max|x| for input / weights)
+  unsigned long long M;   // exact integer max |T| (fp64 bits of max|x| for input / weights)
   unsigned long long F;   // fp64 bits of the reference max_abs
   unsigned int MF;        // fp32 bits of the running max of the fp32 fast-path values
   float thr;              // fast path: 0.5 - band (set by stage_params_kernel once M is final)
@@ -55,7 +55,7 @@ __device__ __forceinline__ StageQ load_int_stage(const Acc& a, int qmax) {
 __device__ __forceinline__ StageQ load_float_stage(const Acc& a, int qmax) {
   StageQ s;
   s.M = 0;
-  s.maxabs = (double)__uint_as_float((unsigned)a.M);
+  s.maxabs = __longlong_as_double((long long)a.M);
   s.qmax = qmax;
   s.scale = s.maxabs > 0.0 ? s.maxabs / (double)qmax : 1.0;
   s.rcp = s.maxabs > 0.0 ? (float)((double)qmax / s.maxabs) : 0.f;
@@ -112,6 +112,15 @@ __device__ __forceinline__ int quant_float(float v, const StageQ& q) {
     return v < 0.f ? -c : c;
   }
   double d = rint((double)v / q.scale);
+  d = d > q.qmax ? q.qmax : d;
+  d = d < -q.qmax ? -q.qmax : d;
+  return (int)d;
+}
+
+// fp64 operand: the reference's own arithmetic (quantize.py:118-119), c = clip(rint(v / scale)).
+__device__ __forceinline__ int quant_float(double v, const StageQ& q) {
+  if (q.maxabs == 0.0) return 0;
+  double d = rint(__ddiv_rn(v, q.scale));
   d = d > q.qmax ? q.qmax : d;
   d = d < -q.qmax ? -q.qmax : d;
   return (int)d;

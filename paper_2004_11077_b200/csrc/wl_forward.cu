@@ -590,8 +590,11 @@ int wl_weight_cache_size(const wl_plan* plan, int c_out, int c_in, size_t* bytes
   return WL_OK;
 }
 
-int wl_weight_transform(const wl_plan* plan, const wl_qcfg* q, const float* w, int c_out, int c_in, void* cache,
-                        size_t cache_bytes, void* stream) {
+}  // extern "C"
+
+template <typename XT>
+static int weight_transform_impl(const wl_plan* plan, const wl_qcfg* q, const XT* w, int c_out, int c_in, void* cache,
+                                 size_t cache_bytes, void* stream) {
   if (!plan || !w || !cache) return fail(WL_ERR_ARG, "NULL argument");
   int rc = check_bits(q);
   if (rc) return rc;
@@ -614,19 +617,31 @@ int wl_weight_transform(const wl_plan* plan, const wl_qcfg* q, const float* w, i
   WL_CUDA(cudaMemsetAsync(U, 0, (size_t)36 * Kp * Cp, st));
   const Bits b = make_bits(q);
   const long long nw = (long long)c_out * c_in * 9;
-  absmax_weights_kernel<<<(int)std::min<long long>((nw + 255) / 256, 1024), 256, 0, st>>>(w, nw, dh->wacc);
+  absmax_weights_kernel<XT><<<(int)std::min<long long>((nw + 255) / 256, 1024), 256, 0, st>>>(w, nw, dh->wacc);
   // "weights" stage max_abs is exact: F = fp64(max |w|) is filled by the readers from M.
   const int threads = 256, blocks = (c_out * c_in + threads - 1) / threads;
   if (plan->mode == WL_CANONICAL) {
-    weight_stage_kernel<0, 0><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
-    weight_stage_kernel<0, 2><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+    weight_stage_kernel<0, 0, XT><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+    weight_stage_kernel<0, 2, XT><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
   } else {
-    weight_stage_kernel<1, 0><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
-    weight_stage_kernel<1, 1><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
-    weight_stage_kernel<1, 2><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+    weight_stage_kernel<1, 0, XT><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+    weight_stage_kernel<1, 1, XT><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
+    weight_stage_kernel<1, 2, XT><<<blocks, threads, 0, st>>>(w, c_out, c_in, Kp, Cp, U, b, dh->wacc, plan->d_pf);
   }
   WL_CUDA(cudaGetLastError());
   return WL_OK;
+}
+
+extern "C" {
+
+int wl_weight_transform(const wl_plan* plan, const wl_qcfg* q, const float* w, int c_out, int c_in, void* cache,
+                        size_t cache_bytes, void* stream) {
+  return weight_transform_impl(plan, q, w, c_out, c_in, cache, cache_bytes, stream);
+}
+
+int wl_weight_transform_f64(const wl_plan* plan, const wl_qcfg* q, const double* w, int c_out, int c_in, void* cache,
+                            size_t cache_bytes, void* stream) {
+  return weight_transform_impl(plan, q, w, c_out, c_in, cache, cache_bytes, stream);
 }
 
 int wl_workspace_size(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* bytes) {
@@ -666,8 +681,11 @@ int wl_forward_launches(const wl_plan* plan, const wl_shape*, const wl_qcfg* q) 
   return (plan->mode == WL_LEGENDRE ? 20 : 14) + otab;
 }
 
-int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
-               const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+template <typename XT, typename YT>
+static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const XT* x, const void* cache,
+                        const YT* bias, YT* y, void* workspace, size_t workspace_bytes, void* stream) {
   if (!plan || !x || !cache || !y || !workspace) return fail(WL_ERR_ARG, "NULL argument");
   int rc = check_bits(q);
   if (rc) return rc;
@@ -693,16 +711,16 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
   {
     const long long per_image = (long long)g.C * g.H * g.W;
     int bx = (int)std::min<long long>((per_image / 4 + 255) / 256, 64);
-    absmax_f32_kernel<<<dim3(std::max(bx, 1), g.N), 256, 0, st>>>(x, per_image, g.ipg, acc);
+    absmax_input_kernel<XT><<<dim3(std::max(bx, 1), g.N), 256, 0, st>>>(x, per_image, g.ipg, acc);
     prof_mark("absmax_input", st);
     const int qrow = std::max(4, std::min(64, (160000 / (g.Cp + 16)) & ~3));
     const size_t qsm = (size_t)qrow * (g.Cp + 16);
     static bool qattr = false;
     if (!qattr) {
-      WL_CUDA(cudaFuncSetAttribute(quant_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      WL_CUDA(cudaFuncSetAttribute(quant_input_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       qattr = true;
     }
-    quant_input_kernel<<<dim3(g.H, g.N), 256, qsm, st>>>(x, c0, g, b, acc, qrow);
+    quant_input_kernel<XT><<<dim3(g.H, g.N), 256, qsm, st>>>(x, c0, g, b, acc, qrow);
     prof_mark("quant_input", st);
   }
   int8_t* c1 = reinterpret_cast<int8_t*>(ws + L.off_c1);
@@ -832,7 +850,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
 
   const long long oc = (long long)g.T * g.K;
   const unsigned ogrid = (unsigned)((oc + tb - 1) / tb);
-  float* otab = q->output_transform_bits <= 12 ? reinterpret_cast<float*>(ws + L.off_otab) : nullptr;
+  float* otab = sizeof(YT) == 4 && q->output_transform_bits <= 12 ? reinterpret_cast<float*>(ws + L.off_otab) : nullptr;
   auto make_otab = [&]() {
     if (!otab) return;
     const long long n = (long long)L.groups * (2 * b.q[ST_OUT] + 1);
@@ -853,7 +871,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
         prof_mark("output_write", st);
       } else {
         auto ka = sout_a_kernel<1, HT, LDs>;
@@ -867,7 +885,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
         prof_mark("output_write", st);
       }
     } else {
@@ -877,7 +895,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
         prof_mark("output_write", st);
       } else {
         out_a_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
@@ -889,7 +907,7 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
         prof_mark("output_write", st);
       }
     }
@@ -906,6 +924,18 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
   if (g_debug_fail) return fail(WL_ERR_CUDA, "kernel group '%s' failed: %s", g_debug_fail,
                                 cudaGetErrorString(cudaGetLastError()));
   return WL_OK;
+}
+
+extern "C" {
+
+int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
+               const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream) {
+  return forward_impl(plan, q, s, x, cache, bias, y, workspace, workspace_bytes, stream);
+}
+
+int wl_forward_f64(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const double* x, const void* cache,
+                   const double* bias, double* y, void* workspace, size_t workspace_bytes, void* stream) {
+  return forward_impl(plan, q, s, x, cache, bias, y, workspace, workspace_bytes, stream);
 }
 
 static BwGeo bw_geo(const Layout& L) {
@@ -973,10 +1003,8 @@ int wl_read_stats(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, cons
       const int bits = wside ? stage_bits(&wh.q, stg) : stage_bits(q, stg);
       double mx;
       if (stg == ST_INPUT || stg == ST_WEIGHTS) {
-        unsigned u = (unsigned)a.M;
-        float fv;
-        memcpy(&fv, &u, 4);
-        mx = (double)fv;
+        long long mb = (long long)a.M;  // fp64 bits of max |x| (exact for fp32 and fp64 operands)
+        memcpy(&mx, &mb, 8);
       } else {
         long long fb = (long long)a.F;
         memcpy(&mx, &fb, 8);

@@ -37,37 +37,51 @@ __device__ __forceinline__ int group_of_image(int n, const Geo& g) { return n / 
 
 // ---------------------------------------------------------------------------------- input side
 
-// max|x| per group (cast "input", quantize.py:141).  x is NCHW fp32; grid.y = image.
-__global__ void absmax_f32_kernel(const float* __restrict__ x, long long per_image, int ipg, Acc* acc) {
+// max|x| per group (cast "input", quantize.py:141).  x is NCHW fp32 or fp64; grid.y = image.
+// The group max is kept as fp64 bits in Acc::M (monotone for non-negative values).
+__device__ __forceinline__ unsigned long long abs_bits(float v) { return __float_as_uint(fabsf(v)); }
+__device__ __forceinline__ unsigned long long abs_bits(double v) {
+  return (unsigned long long)__double_as_longlong(fabs(v));
+}
+template <typename XT>
+__device__ __forceinline__ unsigned long long max_to_f64_bits(unsigned long long m) {
+  if constexpr (sizeof(XT) == 4)
+    return (unsigned long long)__double_as_longlong((double)__uint_as_float((unsigned)m));
+  else
+    return m;
+}
+
+template <typename XT>
+__global__ void absmax_input_kernel(const XT* __restrict__ x, long long per_image, int ipg, Acc* acc) {
   const int n = blockIdx.y;
-  const float* xi = x + (size_t)n * per_image;
-  unsigned m = 0;
-  const bool vec = (per_image % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const XT* xi = x + (size_t)n * per_image;
+  unsigned long long m = 0;
+  const bool vec = sizeof(XT) == 4 && (per_image % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   if (vec) {
     const float4* x4 = reinterpret_cast<const float4*>(xi);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_image / 4;
          i += (long long)gridDim.x * blockDim.x) {
       float4 v = __ldg(&x4[i]);
-      m = max(m, __float_as_uint(fabsf(v.x)));
-      m = max(m, __float_as_uint(fabsf(v.y)));
-      m = max(m, __float_as_uint(fabsf(v.z)));
-      m = max(m, __float_as_uint(fabsf(v.w)));
+      m = max(m, abs_bits(v.x));
+      m = max(m, abs_bits(v.y));
+      m = max(m, abs_bits(v.z));
+      m = max(m, abs_bits(v.w));
     }
   } else {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_image;
          i += (long long)gridDim.x * blockDim.x)
-      m = max(m, __float_as_uint(fabsf(__ldg(&xi[i]))));
+      m = max(m, abs_bits(__ldg(&xi[i])));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ unsigned sm[32];
+  __shared__ unsigned long long sm[32];
   if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x < 32) {
-    m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0u;
+    m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0 && m) atomicMax(&acc[(size_t)(n / ipg) * ST_COUNT + ST_INPUT].M, (unsigned long long)m);
+    if (threadIdx.x == 0 && m) atomicMax(&acc[(size_t)(n / ipg) * ST_COUNT + ST_INPUT].M, max_to_f64_bits<XT>(m));
   }
 }
 
@@ -87,8 +101,15 @@ __device__ __forceinline__ int quant_code(float v, float rc, float thr, double s
   c = c > qmax ? qmax : c;
   return v < 0.f ? -c : c;
 }
+__device__ __forceinline__ int quant_code(double v, float, float, double scale, int qmax) {
+  double d = rint(__ddiv_rn(v, scale));  // quantize.py:118-119 in the reference's own precision
+  d = d > qmax ? qmax : d;
+  d = d < -qmax ? -qmax : d;
+  return (int)d;
+}
 
-__global__ void __launch_bounds__(256) quant_input_kernel(const float* __restrict__ x, int8_t* __restrict__ c0, Geo g,
+template <typename XT>
+__global__ void __launch_bounds__(256) quant_input_kernel(const XT* __restrict__ x, int8_t* __restrict__ c0, Geo g,
                                                           Bits b, const Acc* __restrict__ acc, int kQuantRowW) {
   extern __shared__ __align__(16) int8_t srow[];
   const int h = blockIdx.x, n = blockIdx.y;
@@ -97,7 +118,7 @@ __global__ void __launch_bounds__(256) quant_input_kernel(const float* __restric
   // fast-path error: rc relative 2^-24 on a value <= qmax, plus the fma rounding of the distance
   const float thr = 0.5f - (float)((q.qmax + 1) * 1.25 * 5.9604644775390625e-8);
   const int ld = g.Cp + 16;
-  const bool vec = (g.W & 3) == 0;
+  const bool vec = sizeof(XT) == 4 && (g.W & 3) == 0;
   for (int w0 = 0; w0 < g.W; w0 += kQuantRowW) {
     const int wn = min(kQuantRowW, g.W - w0);
     if (vec) {
@@ -106,7 +127,9 @@ __global__ void __launch_bounds__(256) quant_input_kernel(const float* __restric
         const int c = i / w4n, w4 = i - c * w4n;
         int8_t* dst = srow + (4 * w4) * ld + c;
         if (c < g.C) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(x + (((size_t)n * g.C + c) * g.H + h) * g.W + w0) + w4);
+          const float4 v = __ldg(reinterpret_cast<const float4*>(
+                                     reinterpret_cast<const float*>(x) + (((size_t)n * g.C + c) * g.H + h) * g.W + w0) +
+                                 w4);
           dst[0] = (int8_t)quant_code(v.x, rc, thr, q.scale, q.qmax);
           dst[ld] = (int8_t)quant_code(v.y, rc, thr, q.scale, q.qmax);
           dst[2 * ld] = (int8_t)quant_code(v.z, rc, thr, q.scale, q.qmax);
@@ -276,8 +299,8 @@ __global__ void __launch_bounds__(256) input_stage_kernel(const int8_t* __restri
 
 // Thread per (out channel k, in channel c), c fastest.  PASS 0: weight_transform max; PASS 1
 // (Legendre): weight_base_change max; PASS 2: emit U codes [36][Kp][Cp].
-template <int MODE, int PASS>
-__global__ void __launch_bounds__(256) weight_stage_kernel(const float* __restrict__ w, int K, int C, int Kp, int Cp,
+template <int MODE, int PASS, typename XT>
+__global__ void __launch_bounds__(256) weight_stage_kernel(const XT* __restrict__ w, int K, int C, int Kp, int Cp,
                                                            int8_t* __restrict__ U, Bits b, Acc* __restrict__ wacc,
                                                            const PlanF64* __restrict__ pf) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -350,13 +373,14 @@ __global__ void __launch_bounds__(256) weight_stage_kernel(const float* __restri
   }
 }
 
-__global__ void absmax_weights_kernel(const float* __restrict__ w, long long n, Acc* wacc) {
-  unsigned m = 0;
+template <typename XT>
+__global__ void absmax_weights_kernel(const XT* __restrict__ w, long long n, Acc* wacc) {
+  unsigned long long m = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    m = max(m, __float_as_uint(fabsf(__ldg(&w[i]))));
+    m = max(m, abs_bits(__ldg(&w[i])));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(&wacc[ST_WEIGHTS].M, (unsigned long long)m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(&wacc[ST_WEIGHTS].M, max_to_f64_bits<XT>(m));
 }
 
 // ---------------------------------------------------------------------------------- output side

@@ -476,10 +476,11 @@ __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restric
   record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K);
 }
 
-// Final output: codes of the output stage, dequantised (snap +-qmax to +-max_abs), + bias, fp32 NCHW.
-template <int MODE, typename HT, int LD>
+// Final output: codes of the output stage, dequantised (snap +-qmax to +-max_abs), + bias, NCHW in
+// fp32 (YT = float, dequant table optional) or in the reference's fp64 (YT = double, quantize.py:120-125).
+template <int MODE, typename HT, int LD, typename YT = float>
 __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
-                                                    float* __restrict__ y, const float* __restrict__ bias, Geo g,
+                                                    YT* __restrict__ y, const YT* __restrict__ bias, Geo g,
                                                     Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                                     const float* __restrict__ otab) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -495,13 +496,14 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
   const int qo = b.q[ST_OUT];
   constexpr uint32_t plane = LD;
   const uint32_t off = (uint32_t)t * 36u * LD + k;
-  float Yo[4][4];
+  YT Yo[4][4];
   float X[6][6];
   float dmax = 0.f, kd;
   const float* tabg = otab ? otab + (size_t)grp * (2 * qo + 1) + qo : nullptr;
-  auto deqf = [=](int code) {
-    if (tabg) return __ldg(tabg + code);
-    return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+  auto deqf = [=](int code) -> YT {
+    if constexpr (sizeof(YT) == 4)
+      if (tabg) return __ldg(tabg + code);
+    return code == qo ? (YT)maxabs : (code == -qo ? (YT)-maxabs : (YT)((double)code * scale));
   };
   using LOT = std::conditional_t<MODE == 0, tab::Can_OT, tab::Leg_OT>;
   auto emit = [&](int j, const float (&col)[4], float cm) {
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
     sandwich_cols<tab::Leg_OT>(X, emit);
   }
   if (dmax > thr) {
-    float fixed[16];
+    YT fixed[16];
     unsigned mask = 0;
     auto fix = [&](int i, int j, int code) {
       fixed[4 * i + j] = deqf(code);
@@ -533,15 +535,16 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
     for (int e = 0; e < 16; ++e)
       if ((mask >> e) & 1u) Yo[e / 4][e % 4] = fixed[e];
   }
-  const float bk = bias ? __ldg(&bias[k]) : 0.f;
-  const bool vec = (g.Wo & 3) == 0;
+  const YT bk = bias ? __ldg(&bias[k]) : (YT)0;
+  const bool vec = sizeof(YT) == 4 && (g.Wo & 3) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int rr = 4 * ty + i;
     if (rr >= g.Ho) continue;
-    float* row = y + (((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + 4 * tx;
+    YT* row = y + (((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + 4 * tx;
     if (vec) {
-      *reinterpret_cast<float4*>(row) = make_float4(Yo[i][0] + bk, Yo[i][1] + bk, Yo[i][2] + bk, Yo[i][3] + bk);
+      *reinterpret_cast<float4*>(row) = make_float4((float)(Yo[i][0] + bk), (float)(Yo[i][1] + bk),
+                                                    (float)(Yo[i][2] + bk), (float)(Yo[i][3] + bk));
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j)

@@ -100,10 +100,11 @@ class WeightCache:
     def __init__(self):
         self.key = None
         self.buf = None
+        self.w = None  # strong ref: a fresh tensor can never reuse the cached tensor's address
 
     def get(self, dplan: DevicePlan, q: QuantConfig, w: torch.Tensor) -> torch.Tensor:
-        key = (id(dplan), q, w.data_ptr(), w._version, tuple(w.shape), w.device.index)
-        if self.key == key and self.buf is not None:
+        key = (id(dplan), q, w.data_ptr(), w._version, tuple(w.shape), tuple(w.stride()), w.device.index)
+        if self.w is w and self.key == key and self.buf is not None:
             return self.buf
         cout, cin = int(w.shape[0]), int(w.shape[1])
         nbytes = ctypes.c_size_t()
@@ -112,10 +113,12 @@ class WeightCache:
         if self.buf is None or self.buf.numel() < nbytes.value or self.buf.device != w.device:
             self.buf = torch.empty(nbytes.value, dtype=torch.uint8, device=w.device)
         qs = qcfg_struct(q)
-        _lib.check(_lib.lib().wl_weight_transform(
+        fn = _lib.lib().wl_weight_transform_f64 if w.dtype == torch.float64 else _lib.lib().wl_weight_transform
+        _lib.check(fn(
             dplan.handle, ctypes.byref(qs), ctypes.c_void_p(w.data_ptr()), cout, cin,
             ctypes.c_void_p(self.buf.data_ptr()), nbytes.value, _stream_ptr()), "wl_weight_transform")
         self.key = key
+        self.w = w
         return self.buf
 
 
@@ -168,8 +171,12 @@ class QuantWinogradConv:
             raise DimensionError(f"plan is for k=3, weights have k={w.shape[2]}")
         if not (x.is_cuda and w.is_cuda):
             raise ValueError("x and w must be CUDA tensors")
-        x = x.contiguous().float()
-        w = w.contiguous().float()
+        # fp64 operands take the reference's own precision end to end (fp64 in, fp64 out); anything
+        # else computes from fp32 (codes are exact for fp32-representable values either way).
+        f64 = x.dtype == torch.float64
+        x = x.contiguous() if f64 else x.contiguous().float()
+        w = w.contiguous() if w.dtype == torch.float64 else w.contiguous().float()
+        ydt = torch.float64 if f64 else torch.float32
         shape = self._shape(x, w, padding, scale_groups)
         ho, wo = shape.h + 2 * shape.pad - 2, shape.w + 2 * shape.pad - 2
         if ho < 1 or wo < 1:
@@ -183,13 +190,16 @@ class QuantWinogradConv:
         elif self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
             self.ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
         if out is None:
-            out = torch.empty((shape.n, shape.c_out, ho, wo), dtype=torch.float32, device=x.device)
+            out = torch.empty((shape.n, shape.c_out, ho, wo), dtype=ydt, device=x.device)
+        elif out.dtype != ydt or not out.is_contiguous() or tuple(out.shape) != (shape.n, shape.c_out, ho, wo):
+            raise ValueError(f"out must be a contiguous {ydt} tensor of shape {(shape.n, shape.c_out, ho, wo)}")
         if bias is not None:
-            bias = bias.contiguous().float()
+            bias = bias.contiguous().to(ydt)
             if bias.shape != (shape.c_out,):
                 raise DimensionError(f"bias must be [{shape.c_out}], got {tuple(bias.shape)}")
         qs = qcfg_struct(self.qconfig)
-        _lib.check(_lib.lib().wl_forward(
+        fwd = _lib.lib().wl_forward_f64 if f64 else _lib.lib().wl_forward
+        _lib.check(fwd(
             self.dplan.handle, ctypes.byref(qs), ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()),
             ctypes.c_void_p(cache.data_ptr()), ctypes.c_void_p(bias.data_ptr() if bias is not None else 0),
             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
@@ -209,19 +219,23 @@ class QuantWinogradConv:
         n = xh.shape[0]
         chunks = max(1, min(chunks, n))
         dev = w.device
+        w = w.contiguous() if w.dtype == torch.float64 else w.contiguous().float()  # the object forward() caches
+        xdt = torch.float64 if xh.dtype == torch.float64 else torch.float32
         bounds = [n * i // chunks for i in range(chunks + 1)]
         cur = torch.cuda.current_stream(dev)
         s_in, s_out = self._streams(dev)
-        if not hasattr(self, "_pool") or self._pool_key != (tuple(xh.shape), tuple(yh.shape), chunks):
+        if yh.dtype != xdt:
+            raise ValueError(f"yh must be {xdt} for {xh.dtype} input")
+        if not hasattr(self, "_pool") or self._pool_key != (tuple(xh.shape), tuple(yh.shape), chunks, xdt):
             mx = max(bounds[i + 1] - bounds[i] for i in range(chunks))
-            self._pool = [(torch.empty((mx,) + tuple(xh.shape[1:]), device=dev),
-                           torch.empty((mx,) + tuple(yh.shape[1:]), device=dev), None) for _ in range(2)]
+            self._pool = [(torch.empty((mx,) + tuple(xh.shape[1:]), dtype=xdt, device=dev),
+                           torch.empty((mx,) + tuple(yh.shape[1:]), dtype=xdt, device=dev), None) for _ in range(2)]
             self._pool_ws = [None, None]
-            self._pool_key = (tuple(xh.shape), tuple(yh.shape), chunks)
+            self._pool_key = (tuple(xh.shape), tuple(yh.shape), chunks, xdt)
         ev_in = [torch.cuda.Event() for _ in range(chunks)]
         ev_comp = [torch.cuda.Event() for _ in range(chunks)]
         ev_out = [torch.cuda.Event() for _ in range(chunks)]
-        self.wcache.get(self.dplan, self.qconfig, w.contiguous().float())
+        self.wcache.get(self.dplan, self.qconfig, w)
         for i in range(chunks):
             a, b = bounds[i], bounds[i + 1]
             xd, yd, _ = self._pool[i % 2]
@@ -321,6 +335,7 @@ class _QuantWinogradFn(torch.autograd.Function):
         y = runner.forward(x, w, bias=bias, padding=padding, scale_groups=scale_groups, workspace=ws)
         shape_, cache = runner._last
         ctx.runner, ctx.shape, ctx.has_bias = runner, shape_, bias is not None
+        ctx.dtypes = (x.dtype, w.dtype, bias.dtype if bias is not None else None)
         ctx.save_for_backward(ws, cache)
         return y
 
@@ -328,6 +343,9 @@ class _QuantWinogradFn(torch.autograd.Function):
     def backward(ctx, dy):
         ws, cache = ctx.saved_tensors
         dx, dw, db = ctx.runner.backward(dy, ctx.shape, cache, ws, ctx.has_bias)
+        dx, dw = dx.to(ctx.dtypes[0]), dw.to(ctx.dtypes[1])  # fp32 STE gradients, cast to the operand dtypes
+        if db is not None:
+            db = db.to(ctx.dtypes[2])
         return dx, dw, db, None, None, None
 
 
@@ -380,10 +398,12 @@ def conv2d_winograd_quantized(x, w, plan: WinogradPlan, mode: str, qconfig: Quan
     as_numpy = isinstance(x, np.ndarray) or isinstance(w, np.ndarray)
     if as_numpy:
         dev = torch.device("cuda", torch.cuda.current_device())
-        x = torch.as_tensor(np.asarray(x, dtype=np.float32), device=dev)
-        w = torch.as_tensor(np.asarray(w, dtype=np.float32), device=dev)
+        # the reference copies to contiguous fp64 (pipeline.py:112-113): so does this path, and the
+        # fp64 kernels return the reference's fp64 output bit for bit
+        x = torch.as_tensor(np.asarray(x, dtype=np.float64), device=dev)
+        w = torch.as_tensor(np.asarray(w, dtype=np.float64), device=dev)
         if bias is not None:
-            bias = torch.as_tensor(np.asarray(bias, dtype=np.float32), device=dev)
+            bias = torch.as_tensor(np.asarray(bias, dtype=np.float64), device=dev)
     single = x.dim() == 3
     if single:
         x = x.unsqueeze(0)
@@ -398,7 +418,7 @@ def conv2d_winograd_quantized(x, w, plan: WinogradPlan, mode: str, qconfig: Quan
     if single:
         y = y[0]
     if as_numpy:
-        y = y.double().cpu().numpy()
+        y = y.cpu().numpy()
     return y, stats
 
 

@@ -167,7 +167,7 @@ def test_reference_shaped_numpy_call():
     y, st = W.conv2d_winograd_quantized(x, c["w"].astype(np.float64), PLAN, meta["mode"],
                                         W.QuantConfig(**meta["bits"]))
     assert y.dtype == np.float64 and y.shape == c["y"].shape
-    assert np.array_equal(y, c["y"].astype(np.float32).astype(np.float64))
+    assert np.array_equal(y, c["y"])  # fp64 in -> the reference's fp64 output, bit for bit
     assert [s.stage for s in st] == meta["stages"]
 
 
@@ -205,3 +205,45 @@ def test_forward_host_chunked_equals_device_call():
     r.forward_host(xh, torch.tensor(w, device="cuda"), yh, padding=1, chunks=4)
     torch.cuda.synchronize()
     assert torch.equal(yh, y.cpu())
+
+
+def test_weight_cache_not_fooled_by_recycled_address():
+    """A fresh weight tensor allocated at a freed tensor's address must not hit the weight cache."""
+    rng = np.random.default_rng(13)
+    x = torch.tensor(rng.standard_normal((2, 8, 10, 10)), dtype=torch.float32, device="cuda")
+    r = W.QuantWinogradConv(PLAN, "legendre", W.QuantConfig.uniform(8))
+    for t in range(4):
+        w64 = torch.tensor(rng.standard_normal((6, 8, 3, 3)), dtype=torch.float64, device="cuda")
+        y = r.forward(x, w64.float(), padding=1)   # temporary fp32 weights, freed after the call
+        fresh = W.QuantWinogradConv(PLAN, "legendre", W.QuantConfig.uniform(8)).forward(x, w64.float(), padding=1)
+        assert torch.equal(y, fresh), t
+
+
+@pytest.mark.parametrize("mode", ["legendre", "canonical"])
+@pytest.mark.parametrize("qname", ["8b", "8b+9b"])
+def test_fp64_boundary_bit_exact_arbitrary_doubles(mode, qname):
+    """fp64 operands (not fp32-representable): codes, stats and the fp64 output equal the oracle's."""
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((3, 7, 13, 14)) * 3.7
+    w = rng.standard_normal((5, 7, 3, 3))
+    qc = W.QuantConfig.from_name(qname)
+    r = W.QuantWinogradConv(PLAN, mode, qc)
+    for pad in (0, 1):
+        y = r.forward(torch.tensor(x, device="cuda"), torch.tensor(w, device="cuda"), padding=pad)
+        assert y.dtype == torch.float64
+        yo, so, _ = O.quant_conv_batch(x, w, mode, {f: getattr(qc, f) for f in O.BIT_FIELDS}, padding=pad,
+                                       images_per_group=1)
+        assert np.array_equal(y.cpu().numpy(), yo)
+        for i, st in enumerate(r.stats()):
+            assert stats_tuples(st) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[i]]
+
+
+def test_fp64_numpy_call_equals_oracle_single_image():
+    rng = np.random.default_rng([424242, 3])
+    x = rng.standard_normal((3, 13, 14))
+    w = rng.standard_normal((2, 3, 3, 3))
+    for mode in ("canonical", "legendre"):
+        y, st = W.conv2d_winograd_quantized(x, w, PLAN, mode, W.QuantConfig.uniform(8, hadamard_bits=9))
+        yo, so = O.conv2d_winograd_quantized(x, w, mode, O.uniform_bits(8, 9))
+        assert np.array_equal(y, yo)
+        assert stats_tuples(st) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so]
