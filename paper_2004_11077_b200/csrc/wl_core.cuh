@@ -280,32 +280,100 @@ __device__ __forceinline__ void sandwich_f(const float (&X)[L::C][L::C], float (
   sandwich_f<L>(X, tmp, out);
 }
 
-// Column-streaming fp32 sandwich: for each output column j, tc = X . L[j]^T (exact) and
-// col = L . tc; f(j, col) consumes the column before the next is formed, so only X and one column
-// are live (same operation count and error bound as sandwich_f).
-template <class L, class F>
-__device__ __forceinline__ void sandwich_cols(const float (&X)[L::C][L::C], F&& f, float* tmax = nullptr) {
-#pragma unroll
-  for (int j = 0; j < L::R; ++j) {
-    float tc[L::C];
+// Even/odd row pairs of a stage matrix: rows a, b with L[b][l] = +-L[a][l] for every l (at least one
+// + and one - nonzero), as in B^T / B_P^T.  Both rows come from e = sum of the "+" terms and
+// o = sum of the "-" terms: out[a] = e + o, out[b] = e - o, saving ~1/3 of the multiply-adds.
+template <class L>
+__host__ __device__ constexpr bool rows_pair(int a, int b) {
+  bool ev = false, od = false;
+  for (int l = 0; l < L::C; ++l) {
+    const int x = L::e(a, l), y = L::e(b, l);
+    if (x == y) {
+      if (x != 0) ev = true;
+    } else if (x == -y) {
+      od = true;
+    } else {
+      return false;
+    }
+  }
+  return ev && od;
+}
+template <class L>
+__host__ __device__ constexpr int row_partner(int a) {
+  // greedy in index order, so the relation is symmetric
+  int p[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  for (int i = 0; i < L::R; ++i)
+    if (p[i] < 0)
+      for (int k = i + 1; k < L::R; ++k)
+        if (p[k] < 0 && rows_pair<L>(i, k)) {
+          p[i] = k;
+          p[k] = i;
+          break;
+        }
+  return p[a];
+}
+
+// Compile-time loop: f(std::integral_constant<int, i>) for i in [B, E), so per-index properties of
+// the stage matrix (row partners) are constant-evaluated by the front end.
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+// Row J (and its partner P > J, if any) of L dotted with v.
+template <class L, int J, int P>
+__device__ __forceinline__ void lrows_dot(const float (&v)[L::C], float& oj, float& op) {
+  if constexpr (P > J) {
+    float e = 0.f, o = 0.f;
 #pragma unroll
     for (int l = 0; l < L::C; ++l) {
-      float s = 0.f;
-#pragma unroll
-      for (int l2 = 0; l2 < L::C; ++l2)
-        if (L::e(j, l2) != 0) s = fmaf(X[l][l2], (float)L::e(j, l2), s);
-      tc[l] = s;
-      if (tmax) *tmax = fmaxf(*tmax, fabsf(s));
+      const int a = L::e(J, l);
+      if (a != 0) {
+        if (a == L::e(P, l))
+          e = fmaf(v[l], (float)a, e);
+        else
+          o = fmaf(v[l], (float)a, o);
+      }
     }
+    oj = e + o;
+    op = e - o;
+  } else {
+    float s = 0.f;
+#pragma unroll
+    for (int l = 0; l < L::C; ++l)
+      if (L::e(J, l) != 0) s = fmaf(v[l], (float)L::e(J, l), s);
+    oj = s;
+    op = 0.f;
+  }
+}
+
+// out = L . v (second half), row pairs shared.  Rounding depth <= 4 per element, inside the
+// 6.5 * 2^-24 * rowsum * max|v| bound the fast path certifies.
+template <class L>
+__device__ __forceinline__ void lapply(const float (&v)[L::C], float (&out)[L::R]) {
+  static_for<0, L::R>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    constexpr int p = row_partner<L>(i);
+    if constexpr (!(p >= 0 && p < i)) {
+      float a, b;
+      lrows_dot<L, i, p>(v, a, b);
+      out[i] = a;
+      if constexpr (p > i) out[p] = b;
+    }
+  });
+}
+
+// Column-streaming fp32 sandwich: for each output column j, tc = X . L[j]^T (exact) and
+// col = L . tc; f(j, col) consumes the column before the next is formed, so only X and one or two
+// columns are live.  Paired rows of L produce columns j and partner(j) together.
+template <class L, class F>
+__device__ __forceinline__ void sandwich_cols(const float (&X)[L::C][L::C], F&& f, float* tmax = nullptr) {
+  auto emit = [&](int j, const float (&tc)[L::C]) {
     float col[L::R];
-#pragma unroll
-    for (int i = 0; i < L::R; ++i) {
-      float s = 0.f;
-#pragma unroll
-      for (int l = 0; l < L::C; ++l)
-        if (L::e(i, l) != 0) s = fmaf((float)L::e(i, l), tc[l], s);
-      col[i] = s;
-    }
+    lapply<L>(tc, col);
     if constexpr (std::is_invocable_v<F, int, const float (&)[L::R], float>) {
       float cm = 0.f;
 #pragma unroll
@@ -314,27 +382,35 @@ __device__ __forceinline__ void sandwich_cols(const float (&X)[L::C][L::C], F&& 
     } else {
       f(j, col);
     }
-  }
+  };
+  static_for<0, L::R>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    constexpr int p = row_partner<L>(j);
+    if constexpr (!(p >= 0 && p < j)) {
+      float tc[L::C], tp[L::C];
+#pragma unroll
+      for (int l = 0; l < L::C; ++l) {
+        lrows_dot<L, j, p>(X[l], tc[l], tp[l]);
+        if (tmax) *tmax = fmaxf(*tmax, p > j ? fmaxf(fabsf(tc[l]), fabsf(tp[l])) : fabsf(tc[l]));
+      }
+      emit(j, tc);
+      if constexpr (p > j) emit(p, tp);
+    }
+  });
 }
 
-// Fast-path code of one element: y = fl(T*r + magic) (single rounding of the exact product);
-// when |T*r - k| is within the certified band of a half-integer, `exact()` recomputes the element
-// in integers (out of line, reloading its inputs from global memory).
-template <class Exact>
-__device__ __forceinline__ int rq_elem(float T, float r, float thr, Exact&& exact, float& kf) {
-  const float y = fmaf(T, r, kMagic);
-  const float k = y - kMagic;
-  int code = __float_as_int(y) - 0x4B400000;
-  if (fabsf(fmaf(T, r, -k)) > thr) {
-    code = exact();
-    kf = (float)code;
-  } else {
-    kf = k;
+// Largest row abs-sum of L (the per-column band uses it for every row of the column).
+template <class L>
+__host__ __device__ constexpr float max_row_abs_sum() {
+  int m = 0;
+  for (int i = 0; i < L::R; ++i) {
+    int s = 0;
+    for (int l = 0; l < L::C; ++l) s += L::e(i, l) < 0 ? -L::e(i, l) : L::e(i, l);
+    m = s > m ? s : m;
   }
-  return code;
+  return (float)m;
 }
 
-// Row abs-sums of a compile-time matrix (error-bound factors).
 template <class L>
 __host__ __device__ constexpr float row_abs_sum(int i) {
   int s = 0;

@@ -150,7 +150,9 @@ static const int kTableStage[kNumTables] = {ST_IBC, ST_IT, ST_HAD, ST_OBC, ST_OU
 
 struct Layout {
   Geo g;
-  size_t off_acc, off_c0, off_v, off_h, off_c1, off_c4, off_tab[kNumTables], tab_bytes[kNumTables], off_otab, total;
+  size_t off_acc, off_c0, off_v, off_h, off_c1, off_c4, off_tab[kNumTables], tab_bytes[kNumTables], off_otab, off_fix,
+      total;
+  unsigned fix_cap;
   int groups, hbytes, bn;
 };
 
@@ -208,6 +210,11 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   // dequantised output table (output widths <= 12 bits; wider widths dequantise in fp64 inline)
   L->off_otab = o;
   if (q->output_transform_bits <= 12) o = align256(o + sizeof(float) * (size_t)L->groups * ((1 << q->output_transform_bits) - 1));
+  // deferred-fix list: counters + unit ids (expected ~0.2% of units; overflow falls back inline)
+  L->off_fix = o;
+  const size_t units = (size_t)g.T * std::max(g.C, g.K);
+  L->fix_cap = (unsigned)std::max<size_t>(4096, units / 16);
+  o = align256(o + 64 + sizeof(unsigned) * (size_t)L->fix_cap);
   L->total = o;
   return WL_OK;
 }
@@ -675,10 +682,10 @@ int wl_debug_layout(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, si
 
 int wl_forward_launches(const wl_plan* plan, const wl_shape*, const wl_qcfg* q) {
   if (!plan) return WL_ERR_ARG;
-  // absmax, quant, [in_a, finalize, params] x2|1, in_c, gemm max, finalize, params, gemm codes,
-  // [out_a|out_b, finalize, params] x2|1, output table, out_c
+  // absmax, quant, [in_a|in_b(+fixup), finalize, params] x2|1, in_c, fixup, gemm max, finalize, params,
+  // gemm codes, [out_a|out_b(+fixup), finalize, params] x2|1, output table, out_c, fixup
   const int otab = (q && q->output_transform_bits <= 12) ? 1 : 0;
-  return (plan->mode == WL_LEGENDRE ? 20 : 14) + otab;
+  return (plan->mode == WL_LEGENDRE ? 24 : 16) + otab;
 }
 
 }  // extern "C"
@@ -732,6 +739,12 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     if (kTableStage[i] != ST_HAD) WL_CUDA(cudaMemsetAsync(ws + L.off_tab[i], 0, L.tab_bytes[i], st));
   }
   const StageE E = stage_rowsums(plan->mode);
+  FixList fl;
+  fl.count = reinterpret_cast<unsigned*>(ws + L.off_fix);
+  fl.items = reinterpret_cast<unsigned*>(ws + L.off_fix + 64);
+  fl.cap = L.fix_cap;
+  WL_CUDA(cudaMemsetAsync(fl.count, 0, 64, st));
+  const int fix_blocks = 2 * 148;
 
   const long long tc = (long long)g.T * g.C;
   const int tb = 256;
@@ -755,7 +768,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
         prof_mark("input_transform_max", st);
         // the code passes are store-bound: the plain grid (more resident warps) is faster than staging
-        in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+        in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
+        fixup_it_kernel<0><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
         prof_mark("input_transform_codes", st);
       } else {
         auto ka = sin_a_kernel<1, LDs>;
@@ -764,11 +778,13 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
         prof_mark("input_base_change_max", st);
         auto kb = sin_b_kernel<LDs>;
-        sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs);
+        sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs, fl);
+        fixup_ibc_kernel<<<fix_blocks, 128, 0, st>>>(fl, c0, c1, g, b, acc, plan->d_pf, tabs);
         finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
         prof_mark("input_transform_max", st);
-        in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+        in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
+        fixup_it_kernel<1><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
         prof_mark("input_transform_codes", st);
       }
     } else {
@@ -777,18 +793,21 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
         prof_mark("input_transform_max", st);
-        in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+        in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
+        fixup_it_kernel<0><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
         prof_mark("input_transform_codes", st);
       } else {
         in_a_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
         finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
         prof_mark("input_base_change_max", st);
-        in_b_kernel<LD><<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs);
+        in_b_kernel<LD><<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs, fl);
+        fixup_ibc_kernel<<<fix_blocks, 128, 0, st>>>(fl, c0, c1, g, b, acc, plan->d_pf, tabs);
         finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
         prof_mark("input_transform_max", st);
-        in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf);
+        in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
+        fixup_it_kernel<1><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
         prof_mark("input_transform_codes", st);
       }
     }
@@ -871,7 +890,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
+        fixup_out_kernel<0, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       } else {
         auto ka = sout_a_kernel<1, HT, LDs>;
@@ -880,12 +900,14 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
         prof_mark("output_base_change_max", st);
         auto kb = sout_b_kernel<HT, LDs>;
-        sout_b_kernel<HT, LDs><<<staged_grid(kb, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs);
+        sout_b_kernel<HT, LDs><<<staged_grid(kb, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
+        fixup_obc_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, g, b, acc, plan->d_pf, tabs);
         finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
+        fixup_out_kernel<1, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       }
     } else {
@@ -895,19 +917,22 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
+        fixup_out_kernel<0, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       } else {
         out_a_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
         finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
         prof_mark("output_base_change_max", st);
-        out_b_kernel<HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs);
+        out_b_kernel<HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
+        fixup_obc_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, g, b, acc, plan->d_pf, tabs);
         finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab);
+        out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
+        fixup_out_kernel<1, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       }
     }

@@ -180,6 +180,109 @@ __device__ __noinline__ void fix_unit(Src src, float r, float thr, float ef, con
   });
 }
 
+// Per-column fast-path requantisation: code from the magic-number rounding, float code k, and the
+// column's max distance to the rounded value; the caller adds the column band
+// ef * max|tmp col| * max_row_abs_sum once per column (coarser than per row, 2 fewer ops/element;
+// fix_unit re-checks flagged units element by element with the per-row band).
+__device__ __forceinline__ int rq_col(float T, float r, float& k, float& dcol) {
+  const float y = fmaf(T, r, kMagic);
+  k = y - kMagic;
+  dcol = fmaxf(dcol, fabsf(fmaf(T, r, -k)));
+  return __float_as_int(y) - 0x4B400000;
+}
+
+// ---------------------------------------------------------------------------------- deferred fixes
+// A unit whose fast path came within the band of a half-integer is appended to a fix list instead
+// of being fixed inline (which stalls its warp, and in the staged kernels the whole CTA at the next
+// barrier).  A follow-up kernel fixes the listed units one per thread before anything reads them.
+// If the list is full the producer fixes inline, so any capacity is correct.
+enum FixListId { FIX_IBC = 0, FIX_IT, FIX_OBC, FIX_OUT, kFixLists };
+struct FixList {
+  unsigned* count;  // [kFixLists]
+  unsigned* items;  // unit ids t * nch + c, shared by the lists (producer/fixup pairs run in sequence)
+  unsigned cap;
+};
+
+// Warp-aggregated append; returns true if this lane's unit was deferred.
+__device__ __forceinline__ bool defer_fix(const FixList& f, int list, unsigned unit, bool want) {
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, want);
+  if (!m) return false;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned base = 0;
+  if (lane == leader) base = atomicAdd(f.count + list, (unsigned)__popc(m));
+  base = __shfl_sync(act, base, leader);
+  if (!want) return false;
+  const unsigned idx = base + (unsigned)__popc(m & ((1u << lane) - 1u));
+  if (idx >= f.cap) return false;
+  f.items[idx] = unit;
+  return true;
+}
+
+__device__ __forceinline__ unsigned fix_count(const FixList& f, int list) {
+  const unsigned n = *(volatile const unsigned*)(f.count + list);
+  return n < f.cap ? n : f.cap;
+}
+
+// Max contribution of one unit from a fixup thread (no warp cooperation).
+__device__ __forceinline__ void record_unit_single(float m, float tm, int grp, Acc* acc, int stage, unsigned* table,
+                                                   int t, int c, int C) {
+  const int CB = (C + 31) >> 5;
+  atomicMax(table + (size_t)t * CB + (c >> 5), __float_as_uint(m));
+  if (m > 0.f) atomicMax(&acc[(size_t)grp * ST_COUNT + stage].MF, __float_as_uint(m));
+  if (tm > 0.f) atomicMax(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tm));
+}
+
+// Exact fix of one input_transform unit (V codes); inline fallback and fixup_it_kernel.
+template <int MODE>
+__device__ __noinline__ void fix_it_unit(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
+                                         int8_t* __restrict__ V, const Geo& g, const Bits& b, const Acc* acc,
+                                         const PlanF64* __restrict__ pf, int t, int c, uint32_t plane) {
+  const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
+  const Acc* ga = acc + (size_t)grp * ST_COUNT;
+  const float r = ga[ST_IT].r, thr = ga[ST_IT].thr, ef = ga[ST_IT].ef;
+  const uint32_t off = (uint32_t)t * 36u * plane + (uint32_t)c;
+  int8_t* dst = V + off;
+  auto fix = [dst, plane](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; };
+  if constexpr (MODE == 0) {
+    const C0Win win(c0, g, n, tile, c, plane);
+    fix_unit<tab::Can_IT>(SrcC0{win}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT, b.q[ST_INPUT], true, pf->it,
+                          fix);
+  } else {
+    fix_unit<tab::Leg_IT>(SrcPlanes<int8_t>{c1, plane, off}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_IBC,
+                          b.q[ST_IBC], false, pf->it, fix);
+  }
+}
+
+// Exact fix of one output unit: flagged elements of y rewritten (dequantised, + bias, cropped).
+template <int MODE, typename HT, typename YT>
+__device__ __noinline__ void fix_out_unit(const HT* __restrict__ h, const int8_t* __restrict__ c4, YT* __restrict__ y,
+                                          const YT* __restrict__ bias, const Geo& g, const Bits& b, const Acc* acc,
+                                          const PlanF64* __restrict__ pf, int t, int k, uint32_t plane) {
+  const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
+  const int ty = tile / g.tw, tx = tile % g.tw;
+  const Acc* ga = acc + (size_t)grp * ST_COUNT;
+  const float r = ga[ST_OUT].r, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
+  const double scale = ga[ST_OUT].scale;
+  const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
+  const int qo = b.q[ST_OUT];
+  const YT bk = bias ? bias[k] : (YT)0;
+  const uint32_t off = (uint32_t)t * 36u * plane + (uint32_t)k;
+  auto fix = [&](int i, int j, int code) {
+    const int rr = 4 * ty + i, cc = 4 * tx + j;
+    if (rr < g.Ho && cc < g.Wo) {
+      const YT v = code == qo ? (YT)maxabs : (code == -qo ? (YT)-maxabs : (YT)((double)code * scale));
+      y[(((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + cc] = v + bk;
+    }
+  };
+  if constexpr (MODE == 0)
+    fix_unit<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_HAD, b.q[ST_HAD], false,
+                          pf->ot, fix);
+  else
+    fix_unit<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_OBC, b.q[ST_OBC],
+                          false, pf->ot, fix);
+}
+
 // r, threshold and reference scale of one stage for every group, once its M and F are final.
 __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage, int qmax, float rowsum) {
   const int gi = blockIdx.x * blockDim.x + threadIdx.x;
@@ -240,7 +343,7 @@ __global__ void __launch_bounds__(256) in_a_kernel(const int8_t* __restrict__ c0
 template <int LD>
 __global__ void __launch_bounds__(256, WL_MINB) in_b_kernel(const int8_t* __restrict__ c0, int8_t* __restrict__ c1, Geo g,
                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                                   Tables tabs) {
+                                                   Tables tabs, FixList fl) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = idx < (uint32_t)g.T * (uint32_t)g.C;
   const uint32_t id = active ? idx : 0u;
@@ -252,20 +355,24 @@ __global__ void __launch_bounds__(256, WL_MINB) in_b_kernel(const int8_t* __rest
   constexpr uint32_t plane = LD;
   int8_t* dst = c1 + ((size_t)t * 36 * LD + c);
   float K1[6][6];
+  bool deferred = false;
   {
     const C0Win win(c0, g, n, tile, c, LD);
     float X[6][6];
     win.load(X);
     float dmax = 0.f;
     sandwich_cols<tab::Leg_IBC>(X, [&](int j, const float (&col)[6], float cm) {
-      const float fj = ef * cm;
+      float dcol = 0.f;
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        const int code = rq_nb(col[i], r, fj * row_abs_sum<tab::Leg_IBC>(i), K1[i][j], dmax);
+        const int code = rq_col(col[i], r, K1[i][j], dcol);
         if (active) dst[(6 * i + j) * plane] = (int8_t)code;
       }
+      dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<tab::Leg_IBC>(), dcol));
     });
-    if (dmax > thr && active) {
+    const bool want = dmax > thr && active;
+    deferred = defer_fix(fl, FIX_IBC, id, want);
+    if (want && !deferred) {
       fix_unit<tab::Leg_IBC>(SrcC0{win}, r, thr, ef, ga + ST_IBC, b.q[ST_IBC], ga + ST_INPUT, b.q[ST_INPUT], true,
                              pf->ibc, [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; });
 #pragma unroll
@@ -277,6 +384,7 @@ __global__ void __launch_bounds__(256, WL_MINB) in_b_kernel(const int8_t* __rest
 #pragma unroll
     for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
   }, &tm);
+  if (deferred) m = tm = 0.f;  // recorded by fixup_ibc_kernel from the exact codes
   record_unit(m, tm, grp, active, acc, ST_IT, tabs.t[ST_IT], t, c, g.C);
 }
 
@@ -284,7 +392,7 @@ __global__ void __launch_bounds__(256, WL_MINB) in_b_kernel(const int8_t* __rest
 template <int MODE, int LD>
 __global__ void __launch_bounds__(256, WL_MINB) in_c_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
                                                    int8_t* __restrict__ V, Geo g, Bits b, Acc* __restrict__ acc,
-                                                   const PlanF64* __restrict__ pf) {
+                                                   const PlanF64* __restrict__ pf, FixList fl) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (uint32_t)g.T * (uint32_t)g.C) return;
   const int c = (int)(idx % (uint32_t)g.C), t = (int)(idx / (uint32_t)g.C);
@@ -300,26 +408,20 @@ __global__ void __launch_bounds__(256, WL_MINB) in_c_kernel(const int8_t* __rest
   constexpr bool kCan = MODE == 0;
   using LIT = std::conditional_t<kCan, tab::Can_IT, tab::Leg_IT>;
   auto store = [&](int j, const float (&col)[6], float cm) {
-    const float fj = ef * cm;
+    float dcol = 0.f;
 #pragma unroll
-    for (int i = 0; i < 6; ++i)
-      dst[(6 * i + j) * plane] = (int8_t)rq_nb(col[i], r, fj * row_abs_sum<LIT>(i), kd, dmax);
+    for (int i = 0; i < 6; ++i) dst[(6 * i + j) * plane] = (int8_t)rq_col(col[i], r, kd, dcol);
+    dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<LIT>(), dcol));
   };
-  auto fix = [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; };
   if constexpr (MODE == 0) {
     const C0Win win(c0, g, n, tile, c, LD);
     win.load(X);
-    sandwich_cols<tab::Can_IT>(X, store);
-    if (dmax > thr)
-      fix_unit<tab::Can_IT>(SrcC0{win}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT, b.q[ST_INPUT], true, pf->it,
-                            fix);
   } else {
     load_planes(c1, plane, off, X);
-    sandwich_cols<tab::Leg_IT>(X, store);
-    if (dmax > thr)
-      fix_unit<tab::Leg_IT>(SrcPlanes<int8_t>{c1, plane, off}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_IBC,
-                            b.q[ST_IBC], false, pf->it, fix);
   }
+  sandwich_cols<LIT>(X, store);
+  const bool want = dmax > thr;
+  if (want && !defer_fix(fl, FIX_IT, idx, want)) fix_it_unit<MODE>(c0, c1, V, g, b, acc, pf, t, c, LD);
 }
 
 // Exact recomputation of one input-side unit: local exact max and fp64 max_abs of its argmax.
@@ -433,7 +535,7 @@ __global__ void __launch_bounds__(256) out_a_kernel(const HT* __restrict__ h, Ge
 template <typename HT, int LD>
 __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restrict__ h, int8_t* __restrict__ c4, Geo g, Bits b,
                                                     Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                                    Tables tabs) {
+                                                    Tables tabs, FixList fl) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = idx < (uint32_t)g.T * (uint32_t)g.K;
   const uint32_t id = active ? idx : 0u;
@@ -446,19 +548,23 @@ __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restric
   const uint32_t off = (uint32_t)t * 36u * LD + k;
   int8_t* dst = c4 + off;
   float K4[6][6];
+  bool deferred = false;
   {
     float X[6][6];
     load_planes(h, plane, off, X);
     float dmax = 0.f;
     sandwich_cols<tab::Leg_OBC>(X, [&](int j, const float (&col)[6], float cm) {
-      const float fj = ef * cm;
+      float dcol = 0.f;
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        const int code = rq_nb(col[i], r, fj * row_abs_sum<tab::Leg_OBC>(i), K4[i][j], dmax);
+        const int code = rq_col(col[i], r, K4[i][j], dcol);
         if (active) dst[(6 * i + j) * plane] = (int8_t)code;
       }
+      dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<tab::Leg_OBC>(), dcol));
     });
-    if (dmax > thr && active) {
+    const bool want = dmax > thr && active;
+    deferred = defer_fix(fl, FIX_OBC, id, want);
+    if (want && !deferred) {
       fix_unit<tab::Leg_OBC>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OBC, b.q[ST_OBC], ga + ST_HAD,
                              b.q[ST_HAD], false, pf->obc,
                              [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; });
@@ -473,6 +579,7 @@ __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restric
     for (int i = 0; i < 4; ++i)
       if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[i]));
   }, &tm);
+  if (deferred) m = tm = 0.f;  // recorded by fixup_obc_kernel from the exact codes
   record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K);
 }
 
@@ -482,7 +589,7 @@ template <int MODE, typename HT, int LD, typename YT = float>
 __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
                                                     YT* __restrict__ y, const YT* __restrict__ bias, Geo g,
                                                     Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                                    const float* __restrict__ otab) {
+                                                    const float* __restrict__ otab, FixList fl) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (uint32_t)g.T * (uint32_t)g.K) return;
   const int k = (int)(idx % (uint32_t)g.K), t = (int)(idx / (uint32_t)g.K);
@@ -507,34 +614,16 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
   };
   using LOT = std::conditional_t<MODE == 0, tab::Can_OT, tab::Leg_OT>;
   auto emit = [&](int j, const float (&col)[4], float cm) {
-    const float fj = ef * cm;
+    float dcol = 0.f;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) Yo[i][j] = deqf(rq_nb(col[i], r, fj * row_abs_sum<LOT>(i), kd, dmax));
+    for (int i = 0; i < 4; ++i) Yo[i][j] = deqf(rq_col(col[i], r, kd, dcol));
+    dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<LOT>(), dcol));
   };
-  if constexpr (MODE == 0) {
+  if constexpr (MODE == 0)
     load_planes(h, plane, off, X);
-    sandwich_cols<tab::Can_OT>(X, emit);
-  } else {
+  else
     load_planes(c4, plane, off, X);
-    sandwich_cols<tab::Leg_OT>(X, emit);
-  }
-  if (dmax > thr) {
-    YT fixed[16];
-    unsigned mask = 0;
-    auto fix = [&](int i, int j, int code) {
-      fixed[4 * i + j] = deqf(code);
-      mask |= 1u << (4 * i + j);
-    };
-    if constexpr (MODE == 0)
-      fix_unit<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_HAD, b.q[ST_HAD], false,
-                            pf->ot, fix);
-    else
-      fix_unit<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_OBC, b.q[ST_OBC],
-                            false, pf->ot, fix);
-#pragma unroll
-    for (int e = 0; e < 16; ++e)
-      if ((mask >> e) & 1u) Yo[e / 4][e % 4] = fixed[e];
-  }
+  sandwich_cols<LOT>(X, emit);
   const YT bk = bias ? __ldg(&bias[k]) : (YT)0;
   const bool vec = sizeof(YT) == 4 && (g.Wo & 3) == 0;
 #pragma unroll
@@ -551,6 +640,9 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
         if (4 * tx + j < g.Wo) row[j] = Yo[i][j] + bk;
     }
   }
+  const bool want = dmax > thr;
+  if (want && !defer_fix(fl, FIX_OUT, idx, want))
+    fix_out_unit<MODE, HT, YT>(h, c4, y, bias, g, b, acc, pf, t, k, plane);
 }
 
 template <int MODE, int STAGE, typename HT>
@@ -682,6 +774,94 @@ __global__ void finalize_hadamard_kernel(const int8_t* __restrict__ U, const int
       }
       if (f > 0.0) atomicMax(&ga[ST_HAD].F, dbits(f));
     }
+  }
+}
+
+// ---------------------------------------------------------------------------------- fixup kernels
+// One deferred unit per thread; the list length is read on the device (no host round trip).
+
+// Legendre input_base_change: exact c1 codes, then the unit's input_transform maximum.
+__global__ void __launch_bounds__(128) fixup_ibc_kernel(FixList fl, const int8_t* __restrict__ c0,
+                                                        int8_t* __restrict__ c1, Geo g, Bits b, Acc* __restrict__ acc,
+                                                        const PlanF64* __restrict__ pf, Tables tabs) {
+  const unsigned cnt = fix_count(fl, FIX_IBC);
+  const uint32_t plane = (uint32_t)g.Cp;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const unsigned u = fl.items[i];
+    const int c = (int)(u % (unsigned)g.C), t = (int)(u / (unsigned)g.C);
+    const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
+    const Acc* ga = acc + (size_t)grp * ST_COUNT;
+    const float r = ga[ST_IBC].r, thr = ga[ST_IBC].thr, ef = ga[ST_IBC].ef;
+    int8_t* dst = c1 + ((size_t)t * 36 * plane + c);
+    const C0Win win(c0, g, n, tile, c, plane);
+    fix_unit<tab::Leg_IBC>(SrcC0{win}, r, thr, ef, ga + ST_IBC, b.q[ST_IBC], ga + ST_INPUT, b.q[ST_INPUT], true,
+                           pf->ibc, [dst, plane](int ii, int jj, int code) { dst[(6 * ii + jj) * plane] = (int8_t)code; });
+    float K1[6][6];
+#pragma unroll
+    for (int e = 0; e < 36; ++e) K1[e / 6][e % 6] = (float)dst[e * plane];
+    float m = 0.f, tm = 0.f;
+    sandwich_cols<tab::Leg_IT>(K1, [&](int, const float (&col)[6]) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) m = fmaxf(m, fabsf(col[q]));
+    }, &tm);
+    record_unit_single(m, tm, grp, acc, ST_IT, tabs.t[ST_IT], t, c, g.C);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) fixup_it_kernel(FixList fl, const int8_t* __restrict__ c0,
+                                                       const int8_t* __restrict__ c1, int8_t* __restrict__ V, Geo g,
+                                                       Bits b, const Acc* __restrict__ acc,
+                                                       const PlanF64* __restrict__ pf) {
+  const unsigned cnt = fix_count(fl, FIX_IT);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const unsigned u = fl.items[i];
+    fix_it_unit<MODE>(c0, c1, V, g, b, acc, pf, (int)(u / (unsigned)g.C), (int)(u % (unsigned)g.C), (uint32_t)g.Cp);
+  }
+}
+
+// Legendre output_base_change: exact c4 codes, then the unit's (cropped) output maximum.
+template <typename HT>
+__global__ void __launch_bounds__(128) fixup_obc_kernel(FixList fl, const HT* __restrict__ h, int8_t* __restrict__ c4,
+                                                        Geo g, Bits b, Acc* __restrict__ acc,
+                                                        const PlanF64* __restrict__ pf, Tables tabs) {
+  const unsigned cnt = fix_count(fl, FIX_OBC);
+  const uint32_t plane = (uint32_t)g.Kp;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const unsigned u = fl.items[i];
+    const int k = (int)(u % (unsigned)g.K), t = (int)(u / (unsigned)g.K);
+    const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
+    const int ty = tile / g.tw, tx = tile % g.tw;
+    const Acc* ga = acc + (size_t)grp * ST_COUNT;
+    const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr, ef = ga[ST_OBC].ef;
+    const uint32_t off = (uint32_t)t * 36u * plane + (uint32_t)k;
+    int8_t* dst = c4 + off;
+    fix_unit<tab::Leg_OBC>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OBC, b.q[ST_OBC], ga + ST_HAD,
+                           b.q[ST_HAD], false, pf->obc,
+                           [dst, plane](int ii, int jj, int code) { dst[(6 * ii + jj) * plane] = (int8_t)code; });
+    float K4[6][6];
+#pragma unroll
+    for (int e = 0; e < 36; ++e) K4[e / 6][e % 6] = (float)dst[e * plane];
+    float m = 0.f, tm = 0.f;
+    sandwich_cols<tab::Leg_OT>(K4, [&](int j, const float (&col)[4]) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * ty + q < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[q]));
+    }, &tm);
+    record_unit_single(m, tm, grp, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K);
+  }
+}
+
+template <int MODE, typename HT, typename YT>
+__global__ void __launch_bounds__(128) fixup_out_kernel(FixList fl, const HT* __restrict__ h,
+                                                        const int8_t* __restrict__ c4, YT* __restrict__ y,
+                                                        const YT* __restrict__ bias, Geo g, Bits b,
+                                                        const Acc* __restrict__ acc, const PlanF64* __restrict__ pf) {
+  const unsigned cnt = fix_count(fl, FIX_OUT);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const unsigned u = fl.items[i];
+    fix_out_unit<MODE, HT, YT>(h, c4, y, bias, g, b, acc, pf, (int)(u / (unsigned)g.K), (int)(u % (unsigned)g.K),
+                               (uint32_t)g.Kp);
   }
 }
 

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(Staged<LD, 1>::THREADS, WL_MINB)
 template <int LD>
 __global__ void __launch_bounds__(Staged<LD, 1>::THREADS, WL_MINB)
     sin_b_kernel(const __grid_constant__ CUtensorMap c0map, const int8_t* __restrict__ c0, int8_t* __restrict__ c1,
-                 Geo g, Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf, Tables tabs) {
+                 Geo g, Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf, Tables tabs, FixList fl) {
   staged_loop<LD, 1, true>(g, g.C, nullptr, &c0map, [&](int t, int c, bool active, const uint8_t* st) {
     const int tt = active ? t : 0;
     const int n = tt / g.TP, tile = tt % g.TP, grp = n / g.ipg;
@@ -112,19 +112,23 @@ __global__ void __launch_bounds__(Staged<LD, 1>::THREADS, WL_MINB)
     constexpr uint32_t plane = LD;
     int8_t* dst = c1 + ((size_t)tt * 36 * LD + c);
     float K1[6][6];
+    bool deferred = false;
     {
       float X[6][6];
       stage_x<LD, int8_t>(st, c, X);
       float dmax = 0.f;
       sandwich_cols<tab::Leg_IBC>(X, [&](int j, const float (&col)[6], float cm) {
-        const float fj = ef * cm;
+        float dcol = 0.f;
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
-          const int code = rq_nb(col[i], r, fj * row_abs_sum<tab::Leg_IBC>(i), K1[i][j], dmax);
+          const int code = rq_col(col[i], r, K1[i][j], dcol);
           if (active) dst[(6 * i + j) * plane] = (int8_t)code;
         }
+        dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<tab::Leg_IBC>(), dcol));
       });
-      if (dmax > thr && active) {
+      const bool want = dmax > thr && active;
+      deferred = defer_fix(fl, FIX_IBC, (unsigned)tt * (unsigned)g.C + (unsigned)c, want);
+      if (want && !deferred) {
         const C0Win win(c0, g, n, tile, c, LD);
         fix_unit<tab::Leg_IBC>(SrcC0{win}, r, thr, ef, ga + ST_IBC, b.q[ST_IBC], ga + ST_INPUT, b.q[ST_INPUT], true,
                                pf->ibc, [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; });
@@ -137,6 +141,7 @@ __global__ void __launch_bounds__(Staged<LD, 1>::THREADS, WL_MINB)
 #pragma unroll
       for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
     }, &tm);
+    if (deferred) m = tm = 0.f;  // recorded by fixup_ibc_kernel from the exact codes
     record_unit(m, tm, grp, active, acc, ST_IT, tabs.t[ST_IT], tt, c, g.C);
   });
 }
@@ -146,7 +151,7 @@ template <int MODE, int LD>
 __global__ void __launch_bounds__(Staged<LD, 1>::THREADS, WL_MINB)
     sin_c_kernel(const __grid_constant__ CUtensorMap c0map, const int8_t* __restrict__ c0,
                  const int8_t* __restrict__ c1, int8_t* __restrict__ V, Geo g, Bits b, Acc* __restrict__ acc,
-                 const PlanF64* __restrict__ pf) {
+                 const PlanF64* __restrict__ pf, FixList fl) {
   staged_loop<LD, 1, MODE == 0>(g, g.C, c1, &c0map, [&](int t, int c, bool active, const uint8_t* st) {
     if (!active) return;
     const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
@@ -160,22 +165,14 @@ __global__ void __launch_bounds__(Staged<LD, 1>::THREADS, WL_MINB)
     float dmax = 0.f, kd;
     using LIT = std::conditional_t<MODE == 0, tab::Can_IT, tab::Leg_IT>;
     sandwich_cols<LIT>(X, [&](int j, const float (&col)[6], float cm) {
-      const float fj = ef * cm;
+      float dcol = 0.f;
 #pragma unroll
-      for (int i = 0; i < 6; ++i)
-        dst[(6 * i + j) * plane] = (int8_t)rq_nb(col[i], r, fj * row_abs_sum<LIT>(i), kd, dmax);
+      for (int i = 0; i < 6; ++i) dst[(6 * i + j) * plane] = (int8_t)rq_col(col[i], r, kd, dcol);
+      dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<LIT>(), dcol));
     });
-    if (dmax > thr) {
-      auto fix = [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; };
-      if constexpr (MODE == 0) {
-        const C0Win win(c0, g, n, tile, c, LD);
-        fix_unit<tab::Can_IT>(SrcC0{win}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT, b.q[ST_INPUT], true,
-                              pf->it, fix);
-      } else {
-        fix_unit<tab::Leg_IT>(SrcPlanes<int8_t>{c1, plane, off}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_IBC,
-                              b.q[ST_IBC], false, pf->it, fix);
-      }
-    }
+    const bool want = dmax > thr;
+    if (want && !defer_fix(fl, FIX_IT, (unsigned)t * (unsigned)g.C + (unsigned)c, want))
+      fix_it_unit<MODE>(c0, c1, V, g, b, acc, pf, t, c, LD);
   });
 }
 
@@ -211,7 +208,7 @@ __global__ void __launch_bounds__(Staged<LD, sizeof(HT)>::THREADS, WL_MINB)
 template <typename HT, int LD>
 __global__ void __launch_bounds__(Staged<LD, sizeof(HT)>::THREADS, WL_MINB)
     sout_b_kernel(const HT* __restrict__ h, int8_t* __restrict__ c4, Geo g, Bits b, Acc* __restrict__ acc,
-                  const PlanF64* __restrict__ pf, Tables tabs) {
+                  const PlanF64* __restrict__ pf, Tables tabs, FixList fl) {
   staged_loop<LD, sizeof(HT), false>(g, g.K, h, nullptr, [&](int t, int k, bool active, const uint8_t* st) {
     const int tt = active ? t : 0;
     const int n = tt / g.TP, tile = tt % g.TP, grp = n / g.ipg;
@@ -221,19 +218,23 @@ __global__ void __launch_bounds__(Staged<LD, sizeof(HT)>::THREADS, WL_MINB)
     const uint32_t off = (uint32_t)tt * 36u * LD + k;
     int8_t* dst = c4 + off;
     float K4[6][6];
+    bool deferred = false;
     {
       float X[6][6];
       stage_x<LD, HT>(st, k, X);
       float dmax = 0.f;
       sandwich_cols<tab::Leg_OBC>(X, [&](int j, const float (&col)[6], float cm) {
-        const float fj = ef * cm;
+        float dcol = 0.f;
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
-          const int code = rq_nb(col[i], r, fj * row_abs_sum<tab::Leg_OBC>(i), K4[i][j], dmax);
+          const int code = rq_col(col[i], r, K4[i][j], dcol);
           if (active) dst[(6 * i + j) * plane] = (int8_t)code;
         }
+        dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<tab::Leg_OBC>(), dcol));
       });
-      if (dmax > thr && active) {
+      const bool want = dmax > thr && active;
+      deferred = defer_fix(fl, FIX_OBC, (unsigned)tt * (unsigned)g.K + (unsigned)k, want);
+      if (want && !deferred) {
         fix_unit<tab::Leg_OBC>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OBC, b.q[ST_OBC], ga + ST_HAD,
                                b.q[ST_HAD], false, pf->obc,
                                [dst](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; });
@@ -248,78 +249,8 @@ __global__ void __launch_bounds__(Staged<LD, sizeof(HT)>::THREADS, WL_MINB)
       for (int i = 0; i < 4; ++i)
         if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[i]));
     }, &tm);
+    if (deferred) m = tm = 0.f;  // recorded by fixup_obc_kernel from the exact codes
     record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], tt, k, g.K);
-  });
-}
-
-template <int MODE, typename HT, int LD>
-__global__ void __launch_bounds__(Staged<LD, (MODE == 0 ? sizeof(HT) : 1)>::THREADS, WL_MINB)
-    sout_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4, float* __restrict__ y,
-                  const float* __restrict__ bias, Geo g, Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                  const float* __restrict__ otab) {
-  constexpr int EB = MODE == 0 ? (int)sizeof(HT) : 1;
-  const void* src = MODE == 0 ? (const void*)h : (const void*)c4;
-  staged_loop<LD, EB, false>(g, g.K, src, nullptr, [&](int t, int k, bool active, const uint8_t* st) {
-    if (!active) return;
-    const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
-    const int ty = tile / g.tw, tx = tile % g.tw;
-    const Acc* ga = acc + (size_t)grp * ST_COUNT;
-    const float r = ga[ST_OUT].r, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
-    const double scale = ga[ST_OUT].scale;
-    const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
-    const int qo = b.q[ST_OUT];
-    constexpr uint32_t plane = LD;
-    const uint32_t off = (uint32_t)t * 36u * LD + k;
-    const float* tabg = otab ? otab + (size_t)grp * (2 * qo + 1) + qo : nullptr;
-    auto deqf = [=](int code) {
-      if (tabg) return __ldg(tabg + code);
-      return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
-    };
-    float Yo[4][4];
-    float X[6][6];
-    float dmax = 0.f, kd;
-    using LOT = std::conditional_t<MODE == 0, tab::Can_OT, tab::Leg_OT>;
-    if constexpr (MODE == 0)
-      stage_x<LD, HT>(st, k, X);
-    else
-      stage_x<LD, int8_t>(st, k, X);
-    sandwich_cols<LOT>(X, [&](int j, const float (&col)[4], float cm) {
-      const float fj = ef * cm;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) Yo[i][j] = deqf(rq_nb(col[i], r, fj * row_abs_sum<LOT>(i), kd, dmax));
-    });
-    if (dmax > thr) {
-      float fixed[16];
-      unsigned mask = 0;
-      auto fix = [&](int i, int j, int code) {
-        fixed[4 * i + j] = deqf(code);
-        mask |= 1u << (4 * i + j);
-      };
-      if constexpr (MODE == 0)
-        fix_unit<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_HAD, b.q[ST_HAD],
-                              false, pf->ot, fix);
-      else
-        fix_unit<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_OBC,
-                              b.q[ST_OBC], false, pf->ot, fix);
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if ((mask >> e) & 1u) Yo[e / 4][e % 4] = fixed[e];
-    }
-    const float bk = bias ? __ldg(&bias[k]) : 0.f;
-    const bool vec = (g.Wo & 3) == 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int rr = 4 * ty + i;
-      if (rr >= g.Ho) continue;
-      float* row = y + (((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + 4 * tx;
-      if (vec) {
-        *reinterpret_cast<float4*>(row) = make_float4(Yo[i][0] + bk, Yo[i][1] + bk, Yo[i][2] + bk, Yo[i][3] + bk);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (4 * tx + j < g.Wo) row[j] = Yo[i][j] + bk;
-      }
-    }
   });
 }
 
