@@ -7,6 +7,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <vector>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -156,6 +158,15 @@ struct Layout {
   int groups, hbytes, bn;
 };
 
+static FastDiv make_fastdiv(unsigned d) {
+  FastDiv f;
+  f.d = d;
+  f.s = 0;
+  while ((1ull << f.s) < d) ++f.s;
+  f.m = (unsigned)((((1ull << 32) * ((1ull << f.s) - d)) / d) + 1);
+  return f;
+}
+
 static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   if (!s) return fail(WL_ERR_ARG, "shape is NULL");
   if (s->n < 1 || s->c_in < 1 || s->c_out < 1 || s->pad < 0)
@@ -180,6 +191,11 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   g.Cp = pow2_at_least(g.C, 32);
   g.Kp = pow2_at_least(g.K, 64);
   g.ipg = s->images_per_group;
+  g.fTP = make_fastdiv((unsigned)g.TP);
+  g.ftw = make_fastdiv((unsigned)g.tw);
+  g.fipg = make_fastdiv((unsigned)g.ipg);
+  g.fC = make_fastdiv((unsigned)g.C);
+  g.fK = make_fastdiv((unsigned)g.K);
   if ((unsigned long long)g.T * std::max(g.Cp, g.Kp) * 36 >= (1ULL << 32) ||
       (unsigned long long)g.N * g.H * g.W * g.Cp >= (1ULL << 32) || g.Cp > 512 || g.Kp > 512)
     return fail(WL_ERR_ARG, "problem too large for one call (split the batch; per-image scale groups are "
@@ -234,11 +250,22 @@ static size_t weight_cache_bytes(int K, int C, int* Kp, int* Cp) {
 // Persistent grid for a staged kernel: resident blocks per SM (occupancy query, cached) x SMs.
 template <class K>
 static int staged_grid(K kern, int threads, int smem, long long work_items) {
-  static int per_sm = 0;  // per instantiation
-  if (!per_sm) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-    if (per_sm < 1) per_sm = 1;
+  // keyed by kernel: instantiations with identical parameter types share K
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), smem);
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      per_sm = it->second;
+    } else {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+      if (per_sm < 1) per_sm = 1;
+      cache[key] = per_sm;
+    }
   }
   int dev_sms = 0, dev = 0;
   cudaGetDevice(&dev);
@@ -288,7 +315,7 @@ struct EpiHadMax {
   __device__ __forceinline__ void begin(int, int row, bool valid) {
     vmax = 0;
     vmin = 0;
-    grp = valid ? (row / g.TP) / g.ipg : -1;
+    grp = valid ? (int)g.fipg.div(g.fTP.div((unsigned)row)) : -1;
   }
   __device__ __forceinline__ void apply(int, int, int, const uint32_t* v, int n) {
     if (n == 16) {
@@ -346,7 +373,7 @@ struct EpiHadRq {
   int grp;
   bool small;  // |I| < 2^22: int -> float by the magic-number add instead of I2F
   __device__ __forceinline__ void begin(int, int row, bool valid) {
-    grp = valid ? (row / g.TP) / g.ipg : 0;
+    grp = valid ? (int)g.fipg.div(g.fTP.div((unsigned)row)) : 0;
     const Acc& a = acc[(size_t)grp * ST_COUNT + ST_HAD];
     s.r = a.r;
     s.band = 0.5f - a.thr;
@@ -752,6 +779,9 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
   const int fin_blocks = 4 * 148;
   const int pgrid = (L.groups + 127) / 128;
   const bool staged_in = !getenv("WL_NO_STAGED_IN"), staged_out = !getenv("WL_NO_STAGED_OUT");  // debug switches
+  // the input code pass is staged (bulk-copied c0 windows / c1 blocks); the output code pass stays on
+  // the plain grid (staged it measured 2.8x slower: y stores from few resident CTAs)
+  const bool staged_c = !getenv("WL_PLAIN_IN_C");
   CUtensorMap c0map;
   if (g.Cp <= 256 && !make_tmap_i8_4d(&c0map, c0, g.Cp, g.W, g.H, g.N, g.Cp, 6, 6))
     return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled (input window) failed");
@@ -767,7 +797,10 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
         prof_mark("input_transform_max", st);
-        // the code passes are store-bound: the plain grid (more resident warps) is faster than staging
+        if (staged_c) {
+          auto kc = sin_c_kernel<0, LDs>;
+          sin_c_kernel<0, LDs><<<staged_grid(kc, S::THREADS, S::SMEM_OUT, iters), S::THREADS, S::SMEM_OUT, st>>>(c0map, c0, c1, V, g, b, acc, plan->d_pf, fl);
+        } else
         in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
         fixup_it_kernel<0><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
         prof_mark("input_transform_codes", st);
@@ -778,11 +811,15 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
         prof_mark("input_base_change_max", st);
         auto kb = sin_b_kernel<LDs>;
-        sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs, fl);
+        sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM_OUT, iters), S::THREADS, S::SMEM_OUT, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs, fl);
         fixup_ibc_kernel<<<fix_blocks, 128, 0, st>>>(fl, c0, c1, g, b, acc, plan->d_pf, tabs);
         finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
         prof_mark("input_transform_max", st);
+        if (staged_c) {
+          auto kc = sin_c_kernel<1, LDs>;
+          sin_c_kernel<1, LDs><<<staged_grid(kc, S::THREADS, S::SMEM_OUT, iters), S::THREADS, S::SMEM_OUT, st>>>(c0map, c0, c1, V, g, b, acc, plan->d_pf, fl);
+        } else
         in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
         fixup_it_kernel<1><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
         prof_mark("input_transform_codes", st);
@@ -900,7 +937,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
         prof_mark("output_base_change_max", st);
         auto kb = sout_b_kernel<HT, LDs>;
-        sout_b_kernel<HT, LDs><<<staged_grid(kb, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
+        sout_b_kernel<HT, LDs><<<staged_grid(kb, SH::THREADS, SH::SMEM_OUT, iters), SH::THREADS, SH::SMEM_OUT, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
         fixup_obc_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, g, b, acc, plan->d_pf, tabs);
         finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);

@@ -21,8 +21,18 @@
 
 namespace wl {
 
+// Division by a run-time invariant d for 0 <= n < 2^31: q = (umulhi(n, m) + n) >> s
+// (Granlund-Montgomery; m, s set on the host by make_fastdiv).  Replaces the ~20-instruction
+// integer division sequences in the per-unit index math.
+struct FastDiv {
+  unsigned d, m, s;
+  __device__ __forceinline__ unsigned div(unsigned n) const { return (__umulhi(n, m) + n) >> s; }
+  __device__ __forceinline__ unsigned mod(unsigned n) const { return n - div(n) * d; }
+};
+
 struct Geo {
   int N, C, K, H, W, pad, Ho, Wo, th, tw, TP, T, Cp, Kp, ipg;
+  FastDiv fTP, ftw, fipg, fC, fK;
 };
 
 struct Bits {
@@ -33,7 +43,7 @@ struct PlanF64 {  // fp64 left matrices (nearest doubles of the exact rationals,
   double wt[6 * 3], wbc[36], ibc[36], it[36], obc[36], ot[4 * 6];
 };
 
-__device__ __forceinline__ int group_of_image(int n, const Geo& g) { return n / g.ipg; }
+__device__ __forceinline__ int group_of_image(int n, const Geo& g) { return (int)g.fipg.div((unsigned)n); }
 
 // ---------------------------------------------------------------------------------- input side
 
@@ -159,7 +169,7 @@ __global__ void __launch_bounds__(256) quant_input_kernel(const XT* __restrict__
 
 __device__ __forceinline__ void load_input_tile(const int8_t* __restrict__ c0, const Geo& g, int n, int tile, int c,
                                                 int (&X)[6][6]) {
-  const int ty = tile / g.tw, tx = tile % g.tw;
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const int r = 4 * ty + i - g.pad;
@@ -251,7 +261,7 @@ __global__ void __launch_bounds__(256) input_stage_kernel(const int8_t* __restri
   const long long id = active ? idx : 0;
   const int c = (int)(id % g.C);
   const int t = (int)(id / g.C);
-  const int n = t / g.TP, tile = t % g.TP;
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
   const int grp = group_of_image(n, g);
   Acc* ga = acc + (size_t)grp * ST_COUNT;
   int X[6][6];
@@ -420,8 +430,8 @@ __global__ void __launch_bounds__(256) output_stage_kernel(const HT* __restrict_
   const long long id = active ? idx : 0;
   const int k = (int)(id % g.K);
   const int t = (int)(id / g.K);
-  const int n = t / g.TP, tile = t % g.TP;
-  const int ty = tile / g.tw, tx = tile % g.tw;
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
   const int grp = group_of_image(n, g);
   Acc* ga = acc + (size_t)grp * ST_COUNT;
   int H0[6][6];

@@ -54,7 +54,7 @@ struct C0Win {
   unsigned rmask, cmask;
   __device__ __forceinline__ C0Win(const int8_t* c0, const Geo& g, int n, int tile, int c, uint32_t cstride)
       : p(c0) {
-    const int ty = tile / g.tw, tx = tile % g.tw;
+    const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
     const int r0 = 4 * ty - g.pad, q0 = 4 * tx - g.pad;
     cs = cstride;
     rs = (uint32_t)g.W * cs;
@@ -88,8 +88,9 @@ __device__ __forceinline__ void load_c0(const int8_t* __restrict__ c0, const Geo
 // 36 codes of one unit of a [T][36][LD] layout: element e at off + e * plane (plane = LD).
 template <typename HT, typename XT>
 __device__ __forceinline__ void load_planes(const HT* __restrict__ P, uint32_t plane, uint32_t off, XT (&X)[6][6]) {
+  const HT* p = P + off;  // 64-bit base once; e * plane folds into the load's immediate offset
 #pragma unroll
-  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = to_x<XT>((int)__ldg(P + (off + (uint32_t)e * plane)));
+  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = to_x<XT>((int)__ldg(p + (size_t)e * plane));
 }
 
 // Max of one (unit row t, channel c) into table entry t*ceil(C/32) + c/32 and the group running max.
@@ -234,16 +235,16 @@ __device__ __forceinline__ void record_unit_single(float m, float tm, int grp, A
 }
 
 // Exact fix of one input_transform unit (V codes); inline fallback and fixup_it_kernel.
+// `dst` = the unit's element 0 (global V or a staged shared block), elements `dstride` apart.
 template <int MODE>
-__device__ __noinline__ void fix_it_unit(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
-                                         int8_t* __restrict__ V, const Geo& g, const Bits& b, const Acc* acc,
+__device__ __noinline__ void fix_it_unit(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1, int8_t* dst,
+                                         uint32_t dstride, const Geo& g, const Bits& b, const Acc* acc,
                                          const PlanF64* __restrict__ pf, int t, int c, uint32_t plane) {
-  const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_IT].r, thr = ga[ST_IT].thr, ef = ga[ST_IT].ef;
   const uint32_t off = (uint32_t)t * 36u * plane + (uint32_t)c;
-  int8_t* dst = V + off;
-  auto fix = [dst, plane](int i, int j, int code) { dst[(6 * i + j) * plane] = (int8_t)code; };
+  auto fix = [dst, dstride](int i, int j, int code) { dst[(6 * i + j) * dstride] = (int8_t)code; };
   if constexpr (MODE == 0) {
     const C0Win win(c0, g, n, tile, c, plane);
     fix_unit<tab::Can_IT>(SrcC0{win}, r, thr, ef, ga + ST_IT, b.q[ST_IT], ga + ST_INPUT, b.q[ST_INPUT], true, pf->it,
@@ -259,8 +260,8 @@ template <int MODE, typename HT, typename YT>
 __device__ __noinline__ void fix_out_unit(const HT* __restrict__ h, const int8_t* __restrict__ c4, YT* __restrict__ y,
                                           const YT* __restrict__ bias, const Geo& g, const Bits& b, const Acc* acc,
                                           const PlanF64* __restrict__ pf, int t, int k, uint32_t plane) {
-  const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
-  const int ty = tile / g.tw, tx = tile % g.tw;
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_OUT].r, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
   const double scale = ga[ST_OUT].scale;
@@ -321,9 +322,9 @@ __global__ void __launch_bounds__(256) in_a_kernel(const int8_t* __restrict__ c0
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = idx < (uint32_t)g.T * (uint32_t)g.C;
   const uint32_t id = active ? idx : 0u;
-  const int c = (int)(id % (uint32_t)g.C), t = (int)(id / (uint32_t)g.C);
-  const int n = t / g.TP, tile = t % g.TP;
-  const int grp = n / g.ipg;
+  const int c = (int)g.fC.mod(id), t = (int)g.fC.div(id);
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int grp = (int)g.fipg.div((unsigned)n);
   float X[6][6];
   C0Win(c0, g, n, tile, c, LD).load(X);
   constexpr int st = MODE == 0 ? ST_IT : ST_IBC;
@@ -347,9 +348,9 @@ __global__ void __launch_bounds__(256, WL_MINB) in_b_kernel(const int8_t* __rest
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = idx < (uint32_t)g.T * (uint32_t)g.C;
   const uint32_t id = active ? idx : 0u;
-  const int c = (int)(id % (uint32_t)g.C), t = (int)(id / (uint32_t)g.C);
-  const int n = t / g.TP, tile = t % g.TP;
-  const int grp = n / g.ipg;
+  const int c = (int)g.fC.mod(id), t = (int)g.fC.div(id);
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int grp = (int)g.fipg.div((unsigned)n);
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_IBC].r, thr = ga[ST_IBC].thr, ef = ga[ST_IBC].ef;
   constexpr uint32_t plane = LD;
@@ -391,13 +392,13 @@ __global__ void __launch_bounds__(256, WL_MINB) in_b_kernel(const int8_t* __rest
 // V codes.  Canonical: from c0 through B^T.  Legendre: from the stored c1 through B_P^T.
 template <int MODE, int LD>
 __global__ void __launch_bounds__(256, WL_MINB) in_c_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
-                                                   int8_t* __restrict__ V, Geo g, Bits b, Acc* __restrict__ acc,
+                                                   int8_t* __restrict__ V, const __grid_constant__ Geo g, const __grid_constant__ Bits b, Acc* __restrict__ acc,
                                                    const PlanF64* __restrict__ pf, FixList fl) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (uint32_t)g.T * (uint32_t)g.C) return;
-  const int c = (int)(idx % (uint32_t)g.C), t = (int)(idx / (uint32_t)g.C);
-  const int n = t / g.TP, tile = t % g.TP;
-  const int grp = n / g.ipg;
+  const int c = (int)g.fC.mod(idx), t = (int)g.fC.div(idx);
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int grp = (int)g.fipg.div((unsigned)n);
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_IT].r, thr = ga[ST_IT].thr, ef = ga[ST_IT].ef;
   constexpr uint32_t plane = LD;
@@ -421,15 +422,15 @@ __global__ void __launch_bounds__(256, WL_MINB) in_c_kernel(const int8_t* __rest
   }
   sandwich_cols<LIT>(X, store);
   const bool want = dmax > thr;
-  if (want && !defer_fix(fl, FIX_IT, idx, want)) fix_it_unit<MODE>(c0, c1, V, g, b, acc, pf, t, c, LD);
+  if (want && !defer_fix(fl, FIX_IT, idx, want)) fix_it_unit<MODE>(c0, c1, dst, LD, g, b, acc, pf, t, c, LD);
 }
 
 // Exact recomputation of one input-side unit: local exact max and fp64 max_abs of its argmax.
 template <int MODE, int STAGE>
 __device__ void exact_input_unit(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1, const Geo& g,
                                  const Bits& b, Acc* acc, const PlanF64* pf, int t, int c) {
-  const int n = t / g.TP, tile = t % g.TP;
-  const int grp = n / g.ipg;
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int grp = (int)g.fipg.div((unsigned)n);
   Acc* ga = acc + (size_t)grp * ST_COUNT;
   int Xi[6][6];
   long long T[6][6];
@@ -482,7 +483,7 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
     if (e < nent) {
       const float v = __uint_as_float(table[e]);
       const int t = (int)(e / CB);
-      const int grp = (t / g.TP) / g.ipg;
+      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)t));
       const Acc& a = acc[(size_t)grp * ST_COUNT + STAGE];
       const float mf = __uint_as_float(a.MF);
       pass = v > 0.f && v >= mf - 2.f * stage_error(a, rowsum);
@@ -508,10 +509,10 @@ __global__ void __launch_bounds__(256) out_a_kernel(const HT* __restrict__ h, Ge
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = idx < (uint32_t)g.T * (uint32_t)g.K;
   const uint32_t id = active ? idx : 0u;
-  const int k = (int)(id % (uint32_t)g.K), t = (int)(id / (uint32_t)g.K);
-  const int n = t / g.TP, tile = t % g.TP;
-  const int grp = n / g.ipg;
-  const int ty = tile / g.tw, tx = tile % g.tw;
+  const int k = (int)g.fK.mod(id), t = (int)g.fK.div(id);
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int grp = (int)g.fipg.div((unsigned)n);
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
   float X[6][6];
   load_planes(h, (uint32_t)LD, (uint32_t)t * 36u * LD + k, X);
   float m = 0.f, tm = 0.f;
@@ -539,9 +540,9 @@ __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restric
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = idx < (uint32_t)g.T * (uint32_t)g.K;
   const uint32_t id = active ? idx : 0u;
-  const int k = (int)(id % (uint32_t)g.K), t = (int)(id / (uint32_t)g.K);
-  const int n = t / g.TP, tile = t % g.TP;
-  const int grp = n / g.ipg;
+  const int k = (int)g.fK.mod(id), t = (int)g.fK.div(id);
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int grp = (int)g.fipg.div((unsigned)n);
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr, ef = ga[ST_OBC].ef;
   constexpr uint32_t plane = LD;
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restric
       for (int e = 0; e < 36; ++e) K4[e / 6][e % 6] = (float)dst[e * plane];
     }
   }
-  const int ty = tile / g.tw, tx = tile % g.tw;
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
   float m = 0.f, tm = 0.f;
   sandwich_cols<tab::Leg_OT>(K4, [&](int j, const float (&col)[4]) {
 #pragma unroll
@@ -587,15 +588,15 @@ __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restric
 // fp32 (YT = float, dequant table optional) or in the reference's fp64 (YT = double, quantize.py:120-125).
 template <int MODE, typename HT, int LD, typename YT = float>
 __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4,
-                                                    YT* __restrict__ y, const YT* __restrict__ bias, Geo g,
-                                                    Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
+                                                    YT* __restrict__ y, const YT* __restrict__ bias, const __grid_constant__ Geo g,
+                                                    const __grid_constant__ Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                                     const float* __restrict__ otab, FixList fl) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (uint32_t)g.T * (uint32_t)g.K) return;
-  const int k = (int)(idx % (uint32_t)g.K), t = (int)(idx / (uint32_t)g.K);
-  const int n = t / g.TP, tile = t % g.TP;
-  const int ty = tile / g.tw, tx = tile % g.tw;
-  const int grp = n / g.ipg;
+  const int k = (int)g.fK.mod(idx), t = (int)g.fK.div(idx);
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
+  const int grp = (int)g.fipg.div((unsigned)n);
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_OUT].r, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
   const double scale = ga[ST_OUT].scale;
@@ -648,9 +649,9 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
 template <int MODE, int STAGE, typename HT>
 __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __restrict__ c4, const Geo& g, const Bits& b,
                                   Acc* acc, const PlanF64* pf, int t, int k) {
-  const int n = t / g.TP, tile = t % g.TP;
-  const int ty = tile / g.tw, tx = tile % g.tw;
-  const int grp = n / g.ipg;
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
+  const int grp = (int)g.fipg.div((unsigned)n);
   Acc* ga = acc + (size_t)grp * ST_COUNT;
   int Xi[6][6];
   if (MODE == 1 && STAGE == ST_OBC) {
@@ -716,7 +717,7 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
     if (e < nent) {
       const float v = __uint_as_float(table[e]);
       const int t = (int)(e / KB);
-      const int grp = (t / g.TP) / g.ipg;
+      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)t));
       const Acc& a = acc[(size_t)grp * ST_COUNT + STAGE];
       const float mf = __uint_as_float(a.MF);
       pass = v > 0.f && v >= mf - 2.f * stage_error(a, rowsum);
@@ -749,7 +750,7 @@ __global__ void finalize_hadamard_kernel(const int8_t* __restrict__ U, const int
     if (e < nent) {
       const unsigned v = table[e];
       const int t = (int)((e / nchunk) % g.T);
-      const int grp = (t / g.TP) / g.ipg;
+      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)t));
       pass = v != 0 && (unsigned long long)v == acc[(size_t)grp * ST_COUNT + ST_HAD].M;
     }
     unsigned mask = __ballot_sync(0xffffffffu, pass);
@@ -759,7 +760,7 @@ __global__ void finalize_hadamard_kernel(const int8_t* __restrict__ U, const int
       const long long ee = base + l;
       const int chunk = (int)(ee % nchunk);
       const int t = (int)((ee / nchunk) % g.T), xi = (int)(ee / nchunk / g.T);
-      const int grp = (t / g.TP) / g.ipg;
+      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)t));
       Acc* ga = acc + (size_t)grp * ST_COUNT;
       const long long M = (long long)ga[ST_HAD].M;
       const int8_t* vrow = V + ((size_t)t * 36 + xi) * g.Cp;
@@ -788,8 +789,8 @@ __global__ void __launch_bounds__(128) fixup_ibc_kernel(FixList fl, const int8_t
   const uint32_t plane = (uint32_t)g.Cp;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const unsigned u = fl.items[i];
-    const int c = (int)(u % (unsigned)g.C), t = (int)(u / (unsigned)g.C);
-    const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
+    const int c = (int)g.fC.mod(u), t = (int)g.fC.div(u);
+    const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
     const Acc* ga = acc + (size_t)grp * ST_COUNT;
     const float r = ga[ST_IBC].r, thr = ga[ST_IBC].thr, ef = ga[ST_IBC].ef;
     int8_t* dst = c1 + ((size_t)t * 36 * plane + c);
@@ -810,13 +811,14 @@ __global__ void __launch_bounds__(128) fixup_ibc_kernel(FixList fl, const int8_t
 
 template <int MODE>
 __global__ void __launch_bounds__(128) fixup_it_kernel(FixList fl, const int8_t* __restrict__ c0,
-                                                       const int8_t* __restrict__ c1, int8_t* __restrict__ V, Geo g,
-                                                       Bits b, const Acc* __restrict__ acc,
+                                                       const int8_t* __restrict__ c1, int8_t* __restrict__ V, const __grid_constant__ Geo g,
+                                                       const __grid_constant__ Bits b, const Acc* __restrict__ acc,
                                                        const PlanF64* __restrict__ pf) {
   const unsigned cnt = fix_count(fl, FIX_IT);
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const unsigned u = fl.items[i];
-    fix_it_unit<MODE>(c0, c1, V, g, b, acc, pf, (int)(u / (unsigned)g.C), (int)(u % (unsigned)g.C), (uint32_t)g.Cp);
+    const int t = (int)g.fC.div(u), c = (int)g.fC.mod(u);
+    fix_it_unit<MODE>(c0, c1, V + ((size_t)t * 36 * g.Cp + c), (uint32_t)g.Cp, g, b, acc, pf, t, c, (uint32_t)g.Cp);
   }
 }
 
@@ -829,9 +831,9 @@ __global__ void __launch_bounds__(128) fixup_obc_kernel(FixList fl, const HT* __
   const uint32_t plane = (uint32_t)g.Kp;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const unsigned u = fl.items[i];
-    const int k = (int)(u % (unsigned)g.K), t = (int)(u / (unsigned)g.K);
-    const int n = t / g.TP, tile = t % g.TP, grp = n / g.ipg;
-    const int ty = tile / g.tw, tx = tile % g.tw;
+    const int k = (int)g.fK.mod(u), t = (int)g.fK.div(u);
+    const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
+    const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
     const Acc* ga = acc + (size_t)grp * ST_COUNT;
     const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr, ef = ga[ST_OBC].ef;
     const uint32_t off = (uint32_t)t * 36u * plane + (uint32_t)k;
@@ -855,12 +857,12 @@ __global__ void __launch_bounds__(128) fixup_obc_kernel(FixList fl, const HT* __
 template <int MODE, typename HT, typename YT>
 __global__ void __launch_bounds__(128) fixup_out_kernel(FixList fl, const HT* __restrict__ h,
                                                         const int8_t* __restrict__ c4, YT* __restrict__ y,
-                                                        const YT* __restrict__ bias, Geo g, Bits b,
+                                                        const YT* __restrict__ bias, const __grid_constant__ Geo g, const __grid_constant__ Bits b,
                                                         const Acc* __restrict__ acc, const PlanF64* __restrict__ pf) {
   const unsigned cnt = fix_count(fl, FIX_OUT);
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const unsigned u = fl.items[i];
-    fix_out_unit<MODE, HT, YT>(h, c4, y, bias, g, b, acc, pf, (int)(u / (unsigned)g.K), (int)(u % (unsigned)g.K),
+    fix_out_unit<MODE, HT, YT>(h, c4, y, bias, g, b, acc, pf, (int)g.fK.div(u), (int)g.fK.mod(u),
                                (uint32_t)g.Kp);
   }
 }
