@@ -399,6 +399,31 @@ __device__ __forceinline__ void sandwich_cols(const float (&X)[L::C][L::C], F&& 
   });
 }
 
+// Rounding depth of the fp32 second half per element (sandwich_cols / lapply): a chain of n fmas
+// rounds n times; a row pair rounds max(n_even, n_odd) times and once more in e +- o.  The fast path
+// certifies |error| <= depth * 2^-24 * rowsum * max|tmp| (plus a 0.5 margin in stage_params_kernel).
+template <class L>
+__host__ __device__ constexpr int chain_depth() {
+  int d = 0;
+  for (int i = 0; i < L::R; ++i) {
+    const int p = row_partner<L>(i);
+    int ne = 0, no = 0, nz = 0;
+    for (int l = 0; l < L::C; ++l) {
+      const int a = L::e(i, l);
+      if (a != 0) {
+        ++nz;
+        if (p >= 0 && a == L::e(p, l))
+          ++ne;
+        else if (p >= 0)
+          ++no;
+      }
+    }
+    const int di = p >= 0 ? (ne > no ? ne : no) + 1 : nz;
+    d = di > d ? di : d;
+  }
+  return d;
+}
+
 // Largest row abs-sum of L (the per-column band uses it for every row of the column).
 template <class L>
 __host__ __device__ constexpr float max_row_abs_sum() {

@@ -488,6 +488,18 @@ static void gemm_tiles(const Geo& g, int* bn, int* sw) {
 
 // Max row abs-sum of each stage's integer matrix: with the group's max |first-half value| it bounds
 // the fp32 error of the second half (stage_error in wl_kernels2.cuh).
+// fp32 second-half rounding depth of each transform stage (the fast path's certified band)
+static float stage_depth(int mode, int stage) {
+  const bool leg = mode == WL_LEGENDRE;
+  switch (stage) {
+    case ST_IBC: return (float)chain_depth<tab::Leg_IBC>();
+    case ST_IT: return leg ? (float)chain_depth<tab::Leg_IT>() : (float)chain_depth<tab::Can_IT>();
+    case ST_OBC: return (float)chain_depth<tab::Leg_OBC>();
+    case ST_OUT: return leg ? (float)chain_depth<tab::Leg_OT>() : (float)chain_depth<tab::Can_OT>();
+    default: return 6.f;
+  }
+}
+
 static StageE stage_rowsums(int mode) {
   auto rowsum = [](auto tag, int R, int C) {
     using M = decltype(tag);
@@ -795,7 +807,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         auto ka = sin_a_kernel<0, LDs>;
         sin_a_kernel<0, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
         finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
         if (staged_c) {
           auto kc = sin_c_kernel<0, LDs>;
@@ -808,13 +820,13 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         auto ka = sin_a_kernel<1, LDs>;
         sin_a_kernel<1, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
         finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC], stage_depth(plan->mode, ST_IBC));
         prof_mark("input_base_change_max", st);
         auto kb = sin_b_kernel<LDs>;
         sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM_OUT, iters), S::THREADS, S::SMEM_OUT, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs, fl);
         fixup_ibc_kernel<<<fix_blocks, 128, 0, st>>>(fl, c0, c1, g, b, acc, plan->d_pf, tabs);
         finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
         if (staged_c) {
           auto kc = sin_c_kernel<1, LDs>;
@@ -828,7 +840,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
       if (!leg) {
         in_a_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
         finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
         in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
         fixup_it_kernel<0><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
@@ -836,12 +848,12 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
       } else {
         in_a_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
         finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC], stage_depth(plan->mode, ST_IBC));
         prof_mark("input_base_change_max", st);
         in_b_kernel<LD><<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs, fl);
         fixup_ibc_kernel<<<fix_blocks, 128, 0, st>>>(fl, c0, c1, g, b, acc, plan->d_pf, tabs);
         finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
         in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
         fixup_it_kernel<1><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
@@ -871,7 +883,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     if (rc) return rc;
     finalize_hadamard_kernel<<<fin_blocks, 256, 0, st>>>(U, V, g, acc, wh->wacc, wstage, qu, b.q[ST_IT],
                                                          tabs.t[ST_HAD], L.bn);
-    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_HAD, b.q[ST_HAD], 0.f);
+    stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_HAD, b.q[ST_HAD], 0.f, 0.f);
     prof_mark("gemm_hadamard_max", st);
   }
   if (L.hbytes == 1) {
@@ -924,7 +936,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         auto ka = sout_a_kernel<0, HT, LDs>;
         sout_a_kernel<0, HT, LDs><<<staged_grid(ka, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, g, acc, tabs);
         finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
         out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
@@ -934,13 +946,13 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         auto ka = sout_a_kernel<1, HT, LDs>;
         sout_a_kernel<1, HT, LDs><<<staged_grid(ka, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, g, acc, tabs);
         finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC], stage_depth(plan->mode, ST_OBC));
         prof_mark("output_base_change_max", st);
         auto kb = sout_b_kernel<HT, LDs>;
         sout_b_kernel<HT, LDs><<<staged_grid(kb, SH::THREADS, SH::SMEM_OUT, iters), SH::THREADS, SH::SMEM_OUT, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
         fixup_obc_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, g, b, acc, plan->d_pf, tabs);
         finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
         out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
@@ -951,7 +963,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
       if (!leg) {
         out_a_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
         finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
         out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
@@ -960,12 +972,12 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
       } else {
         out_a_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
         finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC], stage_depth(plan->mode, ST_OBC));
         prof_mark("output_base_change_max", st);
         out_b_kernel<HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
         fixup_obc_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, g, b, acc, plan->d_pf, tabs);
         finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
-        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT]);
+        stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
         out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);

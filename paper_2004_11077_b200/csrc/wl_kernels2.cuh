@@ -129,16 +129,15 @@ struct SrcPlanes {  // [T][36][LD] codes
   __device__ void load(XT (&X)[6][6]) const { load_planes(p, plane, off, X); }
 };
 
-// Exact code of element (i, j) of stage L . X . L^T, X reloaded from src; ties replayed in fp64.
-template <class L, class Src>
-__device__ __noinline__ int exact_elem(Src src, int i, int j, const Acc* a_stage, int qmax, const Acc* a_in,
+// Exact code of element (i, j) of stage L . X . L^T from the unit's input codes xc (row-major 6x6,
+// loaded once by fix_unit); ties replayed in fp64.
+template <class L>
+__device__ __noinline__ int exact_elem(const int* xc, int i, int j, const Acc* a_stage, int qmax, const Acc* a_in,
                                        int qmax_in, bool in_float, const double* __restrict__ Lf) {
-  int X[6][6];
-  src.load(X);
   long long T = 0;
   for (int l = 0; l < L::C; ++l) {
-    long long tmp = 0;
-    for (int l2 = 0; l2 < L::C; ++l2) tmp += (long long)X[l][l2] * L::e(j, l2);
+    int tmp = 0;  // first half |.| <= qmax_in * rowsum(L) < 2^31
+    for (int l2 = 0; l2 < L::C; ++l2) tmp += xc[l * 6 + l2] * L::e(j, l2);
     T += (long long)L::e(i, l) * tmp;
   }
   const StageQ q = load_int_stage(*a_stage, qmax);
@@ -146,8 +145,6 @@ __device__ __noinline__ int exact_elem(Src src, int i, int j, const Acc* a_stage
   int code = rq(T, q, tie);
   if (tie) {
     const StageQ qin = in_float ? load_float_stage(*a_in, qmax_in) : load_int_stage(*a_in, qmax_in);
-    int xc[36];
-    for (int e = 0; e < 36; ++e) xc[e] = X[e / 6][e % 6];
     code = code_of(replay_sandwich(Lf, L::R, L::C, xc, qin.qmax, qin.maxabs, qin.scale, i, j), q);
   }
   return code;
@@ -170,13 +167,21 @@ template <class L, class Src, class Out>
 __device__ __noinline__ void fix_unit(Src src, float r, float thr, float ef, const Acc* a_stage, int qmax,
                                       const Acc* a_in, int qmax_in, bool in_float, const double* __restrict__ Lf,
                                       Out out) {
+  int xc[36];  // the unit's codes, loaded once (the exact path reuses them)
+  {
+    int Xi[6][6];
+    src.load(Xi);
+#pragma unroll
+    for (int e = 0; e < 36; ++e) xc[e] = Xi[e / 6][e % 6];
+  }
   float X[6][6];
-  src.load(X);
+#pragma unroll
+  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = (float)xc[e];
   sandwich_cols<L>(X, [&](int j, const float (&col)[L::R], float cm) {
     for (int i = 0; i < L::R; ++i) {
       const float y = fmaf(col[i], r, kMagic), k = y - kMagic;
       if (fabsf(fmaf(col[i], r, -k)) + ef * cm * row_abs_sum<L>(i) > thr)
-        out(i, j, exact_elem<L>(src, i, j, a_stage, qmax, a_in, qmax_in, in_float, Lf));
+        out(i, j, exact_elem<L>(xc, i, j, a_stage, qmax, a_in, qmax_in, in_float, Lf));
     }
   });
 }
@@ -285,7 +290,7 @@ __device__ __noinline__ void fix_out_unit(const HT* __restrict__ h, const int8_t
 }
 
 // r, threshold and reference scale of one stage for every group, once its M and F are final.
-__global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage, int qmax, float rowsum) {
+__global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage, int qmax, float rowsum, float depth) {
   const int gi = blockIdx.x * blockDim.x + threadIdx.x;
   if (gi >= groups) return;
   Acc& a = acc[(size_t)gi * ST_COUNT + stage];
@@ -296,7 +301,7 @@ __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage
   (void)E;
   // per-element band = ef * rowsum_i * max|tmp col j| (the element's fp32 error E_ij times qmax/M);
   // slack for r = fl(qmax/M) (relative 2^-24 on a value <= qmax) and the fma rounding of d
-  a.ef = M ? (float)((double)qmax * 6.5 * 5.9604644775390625e-8 / (double)M) : 0.f;
+  a.ef = M ? (float)((double)qmax * ((double)depth + 0.5) * 5.9604644775390625e-8 / (double)M) : 0.f;
   a.thr = M ? 0.5f - (float)((qmax + 1) * 1.25 * 5.9604644775390625e-8) : 1.f;
   a.scale = maxabs > 0.0 ? maxabs / (double)qmax : 1.0;
 }
