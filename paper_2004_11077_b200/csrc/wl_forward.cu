@@ -997,6 +997,15 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
   WL_CUDA(cudaGetLastError());
   if (g_debug_fail) return fail(WL_ERR_CUDA, "kernel group '%s' failed: %s", g_debug_fail,
                                 cudaGetErrorString(cudaGetLastError()));
+  if (getenv("WL_FIX_STATS")) {  // debug: deferred-fix list lengths (IBC, IT, OBC, OUT) of this call
+    unsigned cnt[kFixLists];
+    WL_CUDA(cudaMemcpyAsync(cnt, fl.count, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+    WL_CUDA(cudaStreamSynchronize(st));
+    const double units_in = (double)g.T * g.C, units_out = (double)g.T * g.K;
+    fprintf(stderr, "wl fix lists: ibc %u (%.3f%%) it %u (%.3f%%) obc %u (%.3f%%) out %u (%.3f%%) cap %u\n", cnt[0],
+            100.0 * cnt[0] / units_in, cnt[1], 100.0 * cnt[1] / units_in, cnt[2], 100.0 * cnt[2] / units_out, cnt[3],
+            100.0 * cnt[3] / units_out, fl.cap);
+  }
   return WL_OK;
 }
 

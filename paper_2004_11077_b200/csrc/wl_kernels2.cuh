@@ -477,29 +477,31 @@ template <int MODE, int STAGE>
 __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1, Geo g, Bits b,
                                       Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                       const unsigned* __restrict__ table, float rowsum) {
-  const int CB = (g.C + 31) >> 5;
-  const long long nent = (long long)g.T * CB;
+  // thread per tile row t (group data loaded once), walking the row's CB entries; a warp's 32
+  // consecutive rows read contiguous table segments.  Entries within 2E of the group's fp32 max are
+  // recomputed exactly by the whole warp (lane per channel).
+  const int NB = (g.C + 31) >> 5;
   const int lane = threadIdx.x & 31;
-  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long base = wid * 32; base < nent; base += nw * 32) {
-    const long long e = base + lane;
-    bool pass = false;
-    if (e < nent) {
-      const float v = __uint_as_float(table[e]);
-      const int t = (int)(e / CB);
-      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)t));
+  const unsigned T = (unsigned)g.T;
+  const unsigned nthr = gridDim.x * blockDim.x;
+  for (unsigned t0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; t0 < T; t0 += nthr) {
+    const unsigned t = t0 + lane;
+    const bool valid = t < T;
+    float lim = 3.4e38f;
+    if (valid) {
+      const int grp = (int)g.fipg.div(g.fTP.div(t));
       const Acc& a = acc[(size_t)grp * ST_COUNT + STAGE];
-      const float mf = __uint_as_float(a.MF);
-      pass = v > 0.f && v >= mf - 2.f * stage_error(a, rowsum);
+      lim = __uint_as_float(a.MF) - 2.f * stage_error(a, rowsum);
     }
-    unsigned mask = __ballot_sync(0xffffffffu, pass);
-    while (mask) {
-      const int l = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const long long ee = base + l;
-      const int t = (int)(ee / CB), c = (int)(ee % CB) * 32 + lane;
-      if (c < g.C) exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, t, c);
+    for (int cb = 0; cb < NB; ++cb) {
+      const float v = valid ? __uint_as_float(table[(size_t)t * NB + cb]) : 0.f;
+      unsigned mask = __ballot_sync(0xffffffffu, v > 0.f && v >= lim);
+      while (mask) {
+        const int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int tl = (int)t0 + l, ch = cb * 32 + lane;
+        if (ch < g.C) exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, tl, ch);
+      }
     }
   }
 }
@@ -711,29 +713,31 @@ template <int MODE, int STAGE, typename HT>
 __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4, Geo g, Bits b,
                                        Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                        const unsigned* __restrict__ table, float rowsum) {
-  const int KB = (g.K + 31) >> 5;
-  const long long nent = (long long)g.T * KB;
+  // thread per tile row t (group data loaded once), walking the row's KB entries; a warp's 32
+  // consecutive rows read contiguous table segments.  Entries within 2E of the group's fp32 max are
+  // recomputed exactly by the whole warp (lane per channel).
+  const int NB = (g.K + 31) >> 5;
   const int lane = threadIdx.x & 31;
-  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long base = wid * 32; base < nent; base += nw * 32) {
-    const long long e = base + lane;
-    bool pass = false;
-    if (e < nent) {
-      const float v = __uint_as_float(table[e]);
-      const int t = (int)(e / KB);
-      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)t));
+  const unsigned T = (unsigned)g.T;
+  const unsigned nthr = gridDim.x * blockDim.x;
+  for (unsigned t0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; t0 < T; t0 += nthr) {
+    const unsigned t = t0 + lane;
+    const bool valid = t < T;
+    float lim = 3.4e38f;
+    if (valid) {
+      const int grp = (int)g.fipg.div(g.fTP.div(t));
       const Acc& a = acc[(size_t)grp * ST_COUNT + STAGE];
-      const float mf = __uint_as_float(a.MF);
-      pass = v > 0.f && v >= mf - 2.f * stage_error(a, rowsum);
+      lim = __uint_as_float(a.MF) - 2.f * stage_error(a, rowsum);
     }
-    unsigned mask = __ballot_sync(0xffffffffu, pass);
-    while (mask) {
-      const int l = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const long long ee = base + l;
-      const int t = (int)(ee / KB), k = (int)(ee % KB) * 32 + lane;
-      if (k < g.K) exact_output_unit<MODE, STAGE, HT>(h, c4, g, b, acc, pf, t, k);
+    for (int cb = 0; cb < NB; ++cb) {
+      const float v = valid ? __uint_as_float(table[(size_t)t * NB + cb]) : 0.f;
+      unsigned mask = __ballot_sync(0xffffffffu, v > 0.f && v >= lim);
+      while (mask) {
+        const int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int tl = (int)t0 + l, ch = cb * 32 + lane;
+        if (ch < g.K) exact_output_unit<MODE, STAGE, HT>(h, c4, g, b, acc, pf, tl, ch);
+      }
     }
   }
 }
@@ -744,41 +748,43 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
 __global__ void finalize_hadamard_kernel(const int8_t* __restrict__ U, const int8_t* __restrict__ V, Geo g,
                                          Acc* __restrict__ acc, const Acc* __restrict__ wacc, int wstage, int qmax_u,
                                          int qmax_v, const unsigned* __restrict__ table, int bn) {
+  // table[(xi * T + t) * nchunk + chunk]: each thread owns one tile row t (its group max loaded once)
+  // and walks its 36 * nchunk entries; a warp's 32 consecutive rows read contiguous table segments.
+  // An entry equal to the group's exact max is recomputed by the whole warp (rare).
   const int nchunk = g.Kp / bn;
-  const long long nent = (long long)36 * g.T * nchunk;
   const int lane = threadIdx.x & 31;
-  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long base = wid * 32; base < nent; base += nw * 32) {
-    const long long e = base + lane;
-    bool pass = false;
-    if (e < nent) {
-      const unsigned v = table[e];
-      const int t = (int)((e / nchunk) % g.T);
-      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)t));
-      pass = v != 0 && (unsigned long long)v == acc[(size_t)grp * ST_COUNT + ST_HAD].M;
-    }
-    unsigned mask = __ballot_sync(0xffffffffu, pass);
-    while (mask) {
-      const int l = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const long long ee = base + l;
-      const int chunk = (int)(ee % nchunk);
-      const int t = (int)((ee / nchunk) % g.T), xi = (int)(ee / nchunk / g.T);
-      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)t));
-      Acc* ga = acc + (size_t)grp * ST_COUNT;
-      const long long M = (long long)ga[ST_HAD].M;
-      const int8_t* vrow = V + ((size_t)t * 36 + xi) * g.Cp;
-      double f = 0.0;
-      for (int k = chunk * bn + lane; k < min(chunk * bn + bn, g.K); k += 32) {
-        const int8_t* urow = U + ((size_t)k * 36 + xi) * g.Cp;
-        long long s = 0;
-        for (int c = 0; c < g.C; ++c) s += (int)urow[c] * (int)vrow[c];
-        if ((s < 0 ? -s : s) == M)
-          f = fmax(f, fabs(replay_hadamard(urow, vrow, g.C, load_int_stage(wacc[wstage], qmax_u),
-                                           load_int_stage(ga[ST_IT], qmax_v))));
+  const unsigned T = (unsigned)g.T;
+  const unsigned nthr = gridDim.x * blockDim.x;
+  for (unsigned t0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; t0 < T; t0 += nthr) {
+    const unsigned t = t0 + lane;
+    const bool valid = t < T;
+    const int grp = valid ? (int)g.fipg.div(g.fTP.div(t)) : 0;
+    const unsigned long long M = valid ? acc[(size_t)grp * ST_COUNT + ST_HAD].M : 0ull;
+    for (int xi = 0; xi < 36; ++xi) {
+      const unsigned* row = table + ((size_t)xi * T + t) * nchunk;
+      for (int chunk = 0; chunk < nchunk; ++chunk) {
+        const unsigned v = valid ? row[chunk] : 0u;
+        unsigned mask = __ballot_sync(0xffffffffu, v != 0 && (unsigned long long)v == M);
+        while (mask) {
+          const int l = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int tl = (int)t0 + l;
+          const int gl = __shfl_sync(0xffffffffu, grp, l);
+          Acc* ga = acc + (size_t)gl * ST_COUNT;
+          const long long Ml = (long long)ga[ST_HAD].M;
+          const int8_t* vrow = V + ((size_t)tl * 36 + xi) * g.Cp;
+          double f = 0.0;
+          for (int k = chunk * bn + lane; k < min(chunk * bn + bn, g.K); k += 32) {
+            const int8_t* urow = U + ((size_t)k * 36 + xi) * g.Cp;
+            long long sdot = 0;
+            for (int c = 0; c < g.C; ++c) sdot += (int)urow[c] * (int)vrow[c];
+            if ((sdot < 0 ? -sdot : sdot) == Ml)
+              f = fmax(f, fabs(replay_hadamard(urow, vrow, g.C, load_int_stage(wacc[wstage], qmax_u),
+                                               load_int_stage(ga[ST_IT], qmax_v))));
+          }
+          if (f > 0.0) atomicMax(&ga[ST_HAD].F, dbits(f));
+        }
       }
-      if (f > 0.0) atomicMax(&ga[ST_HAD].F, dbits(f));
     }
   }
 }
