@@ -924,6 +924,32 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     const long long n = (long long)L.groups * (2 * b.q[ST_OUT] + 1);
     out_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(acc, L.groups, b.q[ST_OUT], otab);
   };
+  // output code pass: the staged kernel (coalesced y rows) for fp32 outputs, else the plain grid
+  const bool staged_oc = sizeof(YT) == 4 && !getenv("WL_PLAIN_OUT_C");
+  auto out_codes = [&](auto mode_c, auto ht, auto plain) -> int {
+    constexpr int MODE = decltype(mode_c)::value;
+    using HT = decltype(ht);
+    const HT* hh = reinterpret_cast<const HT*>(h);
+    if constexpr (sizeof(YT) == 4) {
+      if (staged_oc) {
+        using STT = std::conditional_t<MODE == 0, HT, int8_t>;
+        CUtensorMap om;
+        const void* src = MODE == 0 ? (const void*)hh : (const void*)c4;
+        if (!make_tmap_3d_plain(&om, src, (int)sizeof(STT), (uint64_t)g.Kp, 36, (uint64_t)g.T, StagedOut::KB, 36,
+                                StagedOut::TPB))
+          return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled (output codes) failed");
+        constexpr int smem = StagedOut::smem<STT>();
+        const long long iters = (long long)((g.T + StagedOut::TPB - 1) / StagedOut::TPB) * ((g.K + StagedOut::KB - 1) / StagedOut::KB);
+        auto kern = sout_c_kernel<MODE, HT>;
+        sout_c_kernel<MODE, HT><<<staged_grid(kern, StagedOut::THREADS, smem, iters), StagedOut::THREADS, smem, st>>>(
+            om, hh, c4, reinterpret_cast<float*>(y), reinterpret_cast<const float*>(bias), g, b, acc, plan->d_pf, otab, fl);
+        return 0;
+      }
+    }
+    plain();
+    return 0;
+  };
+  int oc_rc = 0;
   auto run_out = [&](auto ldc, auto ht) {
     constexpr int LD = decltype(ldc)::value;
     using HT = decltype(ht);
@@ -939,7 +965,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
+        oc_rc = out_codes(IntC<0>{}, HT{}, [&] { out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl); });
         fixup_out_kernel<0, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       } else {
@@ -955,7 +981,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
+        oc_rc = out_codes(IntC<1>{}, HT{}, [&] { out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl); });
         fixup_out_kernel<1, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       }
@@ -966,7 +992,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
+        oc_rc = out_codes(IntC<0>{}, HT{}, [&] { out_c_kernel<0, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl); });
         fixup_out_kernel<0, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       } else {
@@ -980,7 +1006,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
-        out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl);
+        oc_rc = out_codes(IntC<1>{}, HT{}, [&] { out_c_kernel<1, HT, LD, YT><<<ogrid, tb, 0, st>>>(hh, c4, y, bias, g, b, acc, plan->d_pf, otab, fl); });
         fixup_out_kernel<1, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       }
@@ -993,6 +1019,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
       run_out(ldc, int16_t{});
   });
   if (rc) return rc;
+  if (oc_rc) return oc_rc;
 
   WL_CUDA(cudaGetLastError());
   if (g_debug_fail) return fail(WL_ERR_CUDA, "kernel group '%s' failed: %s", g_debug_fail,

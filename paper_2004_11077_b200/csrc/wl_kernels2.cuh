@@ -260,13 +260,13 @@ __device__ __noinline__ void fix_it_unit(const int8_t* __restrict__ c0, const in
   }
 }
 
-// Exact fix of one output unit: flagged elements of y rewritten (dequantised, + bias, cropped).
-template <int MODE, typename HT, typename YT>
-__device__ __noinline__ void fix_out_unit(const HT* __restrict__ h, const int8_t* __restrict__ c4, YT* __restrict__ y,
-                                          const YT* __restrict__ bias, const Geo& g, const Bits& b, const Acc* acc,
-                                          const PlanF64* __restrict__ pf, int t, int k, uint32_t plane) {
-  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
-  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
+// Exact fix of one output unit: every flagged element (i, j) is handed to put(i, j, value) as its
+// dequantised value + bias (crop not applied: the caller decides where the value goes).
+template <int MODE, typename HT, typename YT, class Put>
+__device__ __noinline__ void fix_out_unit_to(const HT* __restrict__ h, const int8_t* __restrict__ c4,
+                                             const YT* __restrict__ bias, const Geo& g, const Bits& b, const Acc* acc,
+                                             const PlanF64* __restrict__ pf, int t, int k, uint32_t plane, Put put) {
+  const int n = (int)g.fTP.div((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
   const Acc* ga = acc + (size_t)grp * ST_COUNT;
   const float r = ga[ST_OUT].r, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
   const double scale = ga[ST_OUT].scale;
@@ -275,11 +275,8 @@ __device__ __noinline__ void fix_out_unit(const HT* __restrict__ h, const int8_t
   const YT bk = bias ? bias[k] : (YT)0;
   const uint32_t off = (uint32_t)t * 36u * plane + (uint32_t)k;
   auto fix = [&](int i, int j, int code) {
-    const int rr = 4 * ty + i, cc = 4 * tx + j;
-    if (rr < g.Ho && cc < g.Wo) {
-      const YT v = code == qo ? (YT)maxabs : (code == -qo ? (YT)-maxabs : (YT)((double)code * scale));
-      y[(((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + cc] = v + bk;
-    }
+    const YT v = code == qo ? (YT)maxabs : (code == -qo ? (YT)-maxabs : (YT)((double)code * scale));
+    put(i, j, v + bk);
   };
   if constexpr (MODE == 0)
     fix_unit<tab::Can_OT>(SrcPlanes<HT>{h, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_HAD, b.q[ST_HAD], false,
@@ -287,6 +284,20 @@ __device__ __noinline__ void fix_out_unit(const HT* __restrict__ h, const int8_t
   else
     fix_unit<tab::Leg_OT>(SrcPlanes<int8_t>{c4, plane, off}, r, thr, ef, ga + ST_OUT, qo, ga + ST_OBC, b.q[ST_OBC],
                           false, pf->ot, fix);
+}
+
+// Exact fix of one output unit: flagged elements of y rewritten (dequantised, + bias, cropped).
+template <int MODE, typename HT, typename YT>
+__device__ __forceinline__ void fix_out_unit(const HT* __restrict__ h, const int8_t* __restrict__ c4,
+                                             YT* __restrict__ y, const YT* __restrict__ bias, const Geo& g,
+                                             const Bits& b, const Acc* acc, const PlanF64* __restrict__ pf, int t,
+                                             int k, uint32_t plane) {
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
+  fix_out_unit_to<MODE, HT, YT>(h, c4, bias, g, b, acc, pf, t, k, plane, [&](int i, int j, YT v) {
+    const int rr = 4 * ty + i, cc = 4 * tx + j;
+    if (rr < g.Ho && cc < g.Wo) y[(((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + cc] = v;
+  });
 }
 
 // r, threshold and reference scale of one stage for every group, once its M and F are final.

@@ -275,4 +275,122 @@ __global__ void __launch_bounds__(Staged<LD, sizeof(HT)>::THREADS, WL_MINB)
   }, c4);
 }
 
+// Output code pass (y), staged both ways.  A work item is TPB=8 consecutive tiles x KB=32 output
+// channels: one 3-D TMA box {32 channels, 36 elements, 8 tiles} of the [T][36][Kp] codes (c4, or h
+// for canonical) lands as [tile][36][32]; warp w computes tile w, lane = channel (conflict-free byte
+// reads).  The 4x4 dequantised outputs go to a padded shared block [channel][tile][4][4(+pad)] and
+// leave as float4 rows, tile fastest, so a warp stores 4 rows x 8 tiles = 4 contiguous 128-byte
+// runs of y instead of 32 scattered 16-byte pieces (the plain out_c_kernel's lg_throttle).
+struct StagedOut {
+  static constexpr int TPB = 8, KB = 32, THREADS = 256;
+  static constexpr int OT = 20;             // floats per tile (16 + 4 pad)
+  static constexpr int OK = TPB * OT + 4;   // floats per channel (bank offset 4 words per channel)
+  static constexpr int OUT_BYTES = KB * OK * 4;
+  template <typename ST>
+  static constexpr int in_bytes() { return TPB * 36 * KB * (int)sizeof(ST); }
+  template <typename ST>
+  static constexpr int smem() { return 2 * in_bytes<ST>() + OUT_BYTES + 16; }
+};
+
+template <int MODE, typename HT>
+__global__ void __launch_bounds__(StagedOut::THREADS, 3)
+    sout_c_kernel(const __grid_constant__ CUtensorMap srcmap, const HT* __restrict__ h,
+                  const int8_t* __restrict__ c4, float* __restrict__ y, const float* __restrict__ bias,
+                  const __grid_constant__ Geo g, const __grid_constant__ Bits b, const Acc* __restrict__ acc,
+                  const PlanF64* __restrict__ pf, const float* __restrict__ otab, FixList fl) {
+  using S = StagedOut;
+  using ST = std::conditional_t<MODE == 0, HT, int8_t>;  // staged code type
+  constexpr int IN_TILE = 36 * S::KB * (int)sizeof(ST);
+  constexpr int IN_BYTES = S::in_bytes<ST>();
+  extern __shared__ __align__(128) uint8_t wl_stage_smem[];
+  uint8_t* sm = wl_stage_smem;
+  float* so = reinterpret_cast<float*>(sm + 2 * IN_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 2 * IN_BYTES + S::OUT_BYTES);
+  const int nkb = (g.K + S::KB - 1) / S::KB;
+  const int niter = ((g.T + S::TPB - 1) / S::TPB) * nkb;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qo = b.q[ST_OUT];
+  using LOT = std::conditional_t<MODE == 0, tab::Can_OT, tab::Leg_OT>;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&srcmap);
+  }
+  __syncthreads();
+  auto issue = [&](int it, int s) {
+    const int tg = it / nkb, kb = it - tg * nkb;
+    mbar_arrive_expect_tx(&bar[s], (uint32_t)IN_BYTES);
+    tma_load_3d(sm + s * IN_BYTES, &srcmap, &bar[s], kb * S::KB, 0, tg * S::TPB);
+  };
+  if (threadIdx.x == 0 && (int)blockIdx.x < niter) issue(blockIdx.x, 0);
+  int kk = 0;
+  for (int it = blockIdx.x; it < niter; it += gridDim.x, ++kk) {
+    const int s = kk & 1;
+    if (threadIdx.x == 0 && it + (int)gridDim.x < niter) issue(it + gridDim.x, s ^ 1);
+    const int tg = it / nkb, kb = it - tg * nkb;
+    const int t0 = tg * S::TPB, k0 = kb * S::KB;
+    mbar_wait(&bar[s], (uint32_t)((kk >> 1) & 1));
+    {
+      const int t = t0 + w, k = k0 + lane;
+      const bool active = t < g.T && k < g.K;
+      const int tt = active ? t : 0;
+      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)tt));
+      const Acc* ga = acc + (size_t)grp * ST_COUNT;
+      // inactive lanes (padded channels hold arbitrary codes) requantise with r = 0 -> code 0
+      const float r = active ? ga[ST_OUT].r : 0.f, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
+      const float* tabg = otab ? otab + (size_t)grp * (2 * qo + 1) + qo : nullptr;
+      const double scale = ga[ST_OUT].scale;
+      const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
+      auto deqf = [=](int code) -> float {
+        if (tabg) return __ldg(tabg + code);
+        return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+      };
+      const float bk = (bias && active) ? __ldg(&bias[k]) : 0.f;
+      float X[6][6];
+      {
+        const ST* p = reinterpret_cast<const ST*>(sm + s * IN_BYTES + w * IN_TILE) + lane;
+#pragma unroll
+        for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = to_x<float>((int)p[e * S::KB]);
+      }
+      float* o = so + lane * S::OK + w * S::OT;
+      float dmax = 0.f, kd;
+      sandwich_cols<LOT>(X, [&](int j, const float (&col)[4], float cm) {
+        float dcol = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[4 * i + j] = deqf(rq_col(col[i], r, kd, dcol)) + bk;
+        dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<LOT>(), dcol));
+      });
+      const bool want = dmax > thr && active;
+      if (want && !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want))
+        fix_out_unit_to<MODE, HT, float>(h, c4, bias, g, b, acc, pf, t, k, (uint32_t)g.Kp,
+                                         [o](int i, int j, float v) { o[4 * i + j] = v; });
+    }
+    __syncthreads();
+    // store phase: piece q = (channel kq, row i, tile tq), tile fastest
+#pragma unroll
+    for (int rep = 0; rep < (S::KB * 4 * S::TPB) / S::THREADS; ++rep) {
+      const int q = rep * S::THREADS + threadIdx.x;
+      const int tq = q & (S::TPB - 1), i = (q / S::TPB) & 3, kq = q / (4 * S::TPB);
+      const int t = t0 + tq, k = k0 + kq;
+      if (t >= g.T || k >= g.K) continue;
+      const int n = (int)g.fTP.div((unsigned)t), tile = t - n * g.TP;
+      const int ty = (int)g.ftw.div((unsigned)tile), tx = tile - ty * g.tw;
+      const int rr = 4 * ty + i;
+      if (rr >= g.Ho) continue;
+      const float4 v = *reinterpret_cast<const float4*>(so + kq * S::OK + tq * S::OT + 4 * i);
+      float* row = y + (((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + 4 * tx;
+      if ((g.Wo & 3) == 0) {
+        __stcs(reinterpret_cast<float4*>(row), v);
+      } else {
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (4 * tx + j < g.Wo) row[j] = vv[j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace wl
