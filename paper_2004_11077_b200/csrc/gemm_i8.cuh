@@ -183,12 +183,14 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // tile -> (xi, m-block, n-block); consecutive tiles of a CTA share xi where possible (U reuse in L2)
+  // tile -> (xi, n-block, m-block), xi fastest: the CTAs in flight together cover all 36 elements of a
+  // few m-blocks, i.e. whole contiguous [128 rows][36][C] regions of V and h (DRAM page locality);
+  // U (36 x Kp x Cp bytes) stays L2-resident whatever the order.
   auto decode = [&](int tile, int& xi, int& mb, int& nb) {
-    nb = tile % nblocks;
-    const int r = tile / nblocks;
-    mb = r % mblocks;
-    xi = r / mblocks;
+    xi = tile % 36;
+    const int r = tile / 36;
+    nb = r % nblocks;
+    mb = r / nblocks;
   };
 
   if (warp == 0) {

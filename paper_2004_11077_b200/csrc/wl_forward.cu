@@ -766,7 +766,11 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
       WL_CUDA(cudaFuncSetAttribute(quant_input_kernel<XT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       qattr = true;
     }
-    quant_input_kernel<XT><<<dim3(g.H, g.N), 256, qsm, st>>>(x, c0, g, b, acc, qrow);
+    if (sizeof(XT) == 4 && (g.W & 3) == 0 && g.W <= 64 && !getenv("WL_GENERIC_QUANT"))
+      quant_input_w64_kernel<<<dim3(g.H, g.N), 256, (size_t)g.W * (g.Cp + 4), st>>>(
+          reinterpret_cast<const float*>(x), c0, g, b, acc);
+    else
+      quant_input_kernel<XT><<<dim3(g.H, g.N), 256, qsm, st>>>(x, c0, g, b, acc, qrow);
     prof_mark("quant_input", st);
   }
   int8_t* c1 = reinterpret_cast<int8_t*>(ws + L.off_c1);
@@ -783,7 +787,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
   fl.items = reinterpret_cast<unsigned*>(ws + L.off_fix + 64);
   fl.cap = L.fix_cap;
   WL_CUDA(cudaMemsetAsync(fl.count, 0, 64, st));
-  const int fix_blocks = 2 * 148;
+  const int fix_blocks = 16 * 148;  // one wave covers every deferred unit of config-4-sized calls (latency-bound per unit)
 
   const long long tc = (long long)g.T * g.C;
   const int tb = 256;
@@ -940,9 +944,17 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
           return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled (output codes) failed");
         constexpr int smem = StagedOut::smem<STT>();
         const long long iters = (long long)((g.T + StagedOut::TPB - 1) / StagedOut::TPB) * ((g.K + StagedOut::KB - 1) / StagedOut::KB);
-        auto kern = sout_c_kernel<MODE, HT>;
-        sout_c_kernel<MODE, HT><<<staged_grid(kern, StagedOut::THREADS, smem, iters), StagedOut::THREADS, smem, st>>>(
-            om, hh, c4, reinterpret_cast<float*>(y), reinterpret_cast<const float*>(bias), g, b, acc, plan->d_pf, otab, fl);
+        auto launch = [&](auto tabc) {
+          constexpr bool TAB = decltype(tabc)::value;
+          auto kern = sout_c_kernel<MODE, HT, TAB>;
+          sout_c_kernel<MODE, HT, TAB><<<staged_grid(kern, StagedOut::THREADS, smem, iters), StagedOut::THREADS, smem,
+                                         st>>>(om, hh, c4, reinterpret_cast<float*>(y),
+                                               reinterpret_cast<const float*>(bias), g, b, acc, plan->d_pf, otab, fl);
+        };
+        if (otab)
+          launch(std::true_type{});
+        else
+          launch(std::false_type{});
         return 0;
       }
     }

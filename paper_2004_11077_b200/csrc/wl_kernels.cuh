@@ -111,6 +111,15 @@ __device__ __forceinline__ int quant_code(float v, float rc, float thr, double s
   c = c > qmax ? qmax : c;
   return v < 0.f ? -c : c;
 }
+// Fast path of quant_code: the fp32 magic-number code, `bad` set when the exact path must decide.
+__device__ __forceinline__ int quant_fast(float v, float rc, float thr, int qmax, bool& bad) {
+  const float a = fabsf(v);
+  const float y = fmaf(a, rc, kMagic);
+  const float k = y - kMagic;
+  bad |= fabsf(fmaf(a, rc, -k)) > thr;
+  const int c = min(__float_as_int(y) - 0x4B400000, qmax);
+  return v < 0.f ? -c : c;
+}
 __device__ __forceinline__ int quant_code(double v, float, float, double scale, int qmax) {
   double d = rint(__ddiv_rn(v, scale));  // quantize.py:118-119 in the reference's own precision
   d = d > qmax ? qmax : d;
@@ -164,6 +173,64 @@ __global__ void __launch_bounds__(256) quant_input_kernel(const XT* __restrict__
       dst[i] = *reinterpret_cast<const int4*>(srow + w * ld + 16 * j);
     }
     __syncthreads();
+  }
+}
+
+// fp32 input, W % 4 == 0, W <= 64: block = (row h, image n); thread = (4-pixel chunk w4 = tid & 15,
+// channel group of 4).  Each thread quantises a 4x4 (channel x pixel) block from 4 coalesced float4
+// loads, transposes it in registers into one 32-bit word per pixel (4 channels, PRMT) and stores the
+// words into a [W][Cp + 4] shared row (2-way bank conflicts at worst); the row leaves as coalesced
+// 32-bit words.  ~12 instructions per element (the generic kernel's per-item division and byte
+// stores cost ~30).
+__global__ void __launch_bounds__(256) quant_input_w64_kernel(const float* __restrict__ x, int8_t* __restrict__ c0,
+                                                              Geo g, Bits b, const Acc* __restrict__ acc) {
+  extern __shared__ __align__(16) int8_t srow[];
+  const int h = blockIdx.x, n = blockIdx.y;
+  const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
+  const float rc = q.maxabs > 0.0 ? (float)((double)q.qmax / q.maxabs) : 0.f;
+  const float thr = 0.5f - (float)((q.qmax + 1) * 1.25 * 5.9604644775390625e-8);
+  const int ld = g.Cp + 4;
+  const int w4n = g.W >> 2, ncg = g.Cp >> 2;
+  const int w4 = threadIdx.x & 15;
+  if (w4 < w4n) {
+    const size_t cstride = (size_t)g.H * g.W;
+    const float* xb = x + ((size_t)n * g.C * g.H + h) * g.W + 4 * w4;
+#pragma unroll 2
+    for (int cg = threadIdx.x >> 4; cg < ncg; cg += blockDim.x >> 4) {
+      // all four loads first (clamped channel, discarded below) so they are in flight together
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = __ldg(reinterpret_cast<const float4*>(xb + (size_t)min(4 * cg + u, g.C - 1) * cstride));
+      uint32_t wd[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (4 * cg + u < g.C) {
+          bool bad = false;
+          int k0 = quant_fast(v[u].x, rc, thr, q.qmax, bad), k1 = quant_fast(v[u].y, rc, thr, q.qmax, bad);
+          int k2 = quant_fast(v[u].z, rc, thr, q.qmax, bad), k3 = quant_fast(v[u].w, rc, thr, q.qmax, bad);
+          if (bad) {  // some element within the fp32 band of a half-integer: the exact path decides
+            k0 = quant_code(v[u].x, rc, thr, q.scale, q.qmax), k1 = quant_code(v[u].y, rc, thr, q.scale, q.qmax);
+            k2 = quant_code(v[u].z, rc, thr, q.scale, q.qmax), k3 = quant_code(v[u].w, rc, thr, q.scale, q.qmax);
+          }
+          // byte u of word p <- low byte of code k_p
+          constexpr uint32_t kSel[4] = {0x3214u, 0x3240u, 0x3410u, 0x4210u};
+          wd[0] = __byte_perm(wd[0], (uint32_t)k0, kSel[u]);
+          wd[1] = __byte_perm(wd[1], (uint32_t)k1, kSel[u]);
+          wd[2] = __byte_perm(wd[2], (uint32_t)k2, kSel[u]);
+          wd[3] = __byte_perm(wd[3], (uint32_t)k3, kSel[u]);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(srow + (4 * w4 + p) * ld + 4 * cg) = wd[p];
+    }
+  }
+  __syncthreads();
+  uint32_t* dst = reinterpret_cast<uint32_t*>(c0 + ((size_t)n * g.H + h) * g.W * g.Cp);
+  const int wpr = g.Cp >> 2, lw = __ffs(wpr) - 1;  // 32-bit words per pixel (a power of two)
+  for (int i = threadIdx.x; i < g.W * wpr; i += blockDim.x) {
+    const int w = i >> lw, j = i & (wpr - 1);
+    dst[i] = *reinterpret_cast<const uint32_t*>(srow + w * ld + 4 * j);
   }
 }
 

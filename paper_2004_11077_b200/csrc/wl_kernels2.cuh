@@ -161,29 +161,47 @@ __device__ __forceinline__ int rq_nb(float T, float r, float band, float& k, flo
 }
 
 // Rare path for a unit whose fast path came within the band of a half-integer: redo the fp32
-// sandwich (deterministic, same values), and for every flagged element compute the exact code and
-// hand it to out(i, j, code), which overwrites what the fast path stored.
+// sandwich (deterministic, same values) to find the flagged elements (per-row band), then compute
+// the unit's exact integer stage values once (int32 first half, int64 second, compile-time
+// indices: no local-memory tables) and hand every flagged element's exact code to out(i, j, code),
+// which overwrites what the fast path stored; exact ties are replayed in fp64.
 template <class L, class Src, class Out>
 __device__ __noinline__ void fix_unit(Src src, float r, float thr, float ef, const Acc* a_stage, int qmax,
                                       const Acc* a_in, int qmax_in, bool in_float, const double* __restrict__ Lf,
                                       Out out) {
-  int xc[36];  // the unit's codes, loaded once (the exact path reuses them)
-  {
-    int Xi[6][6];
-    src.load(Xi);
-#pragma unroll
-    for (int e = 0; e < 36; ++e) xc[e] = Xi[e / 6][e % 6];
-  }
+  int Xi[6][6];  // the unit's codes, loaded once (the exact path reuses them)
+  src.load(Xi);
   float X[6][6];
 #pragma unroll
-  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = (float)xc[e];
+  for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = (float)Xi[e / 6][e % 6];
+  unsigned long long mask = 0;
   sandwich_cols<L>(X, [&](int j, const float (&col)[L::R], float cm) {
+#pragma unroll
     for (int i = 0; i < L::R; ++i) {
       const float y = fmaf(col[i], r, kMagic), k = y - kMagic;
-      if (fabsf(fmaf(col[i], r, -k)) + ef * cm * row_abs_sum<L>(i) > thr)
-        out(i, j, exact_elem<L>(xc, i, j, a_stage, qmax, a_in, qmax_in, in_float, Lf));
+      if (fabsf(fmaf(col[i], r, -k)) + ef * cm * row_abs_sum<L>(i) > thr) mask |= 1ull << (i * 6 + j);
     }
   });
+  if (!mask) return;
+  long long T[L::R][L::R];
+  sandwich<L>(Xi, T);
+  const StageQ q = load_int_stage(*a_stage, qmax);
+#pragma unroll
+  for (int e = 0; e < L::R * L::R; ++e) {
+    const int i = e / L::R, j = e % L::R;
+    if ((mask >> (i * 6 + j)) & 1ull) {
+      bool tie = false;
+      int code = rq(T[i][j], q, tie);
+      if (tie) {
+        int xc[36];
+#pragma unroll
+        for (int u = 0; u < 36; ++u) xc[u] = Xi[u / 6][u % 6];
+        const StageQ qin = in_float ? load_float_stage(*a_in, qmax_in) : load_int_stage(*a_in, qmax_in);
+        code = code_of(replay_sandwich(Lf, L::R, L::C, xc, qin.qmax, qin.maxabs, qin.scale, i, j), q);
+      }
+      out(i, j, code);
+    }
+  }
 }
 
 // Per-column fast-path requantisation: code from the magic-number rounding, float code k, and the
@@ -756,45 +774,56 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
 // Hadamard: table[(xi*T + t)*nchunk + chunk] = exact max |I| over the row chunk (written by the GEMM
 // max epilogue).  Entries equal to the group maximum are recomputed on CUDA cores (lane per column)
 // and their maxima replayed in fp64.
-__global__ void finalize_hadamard_kernel(const int8_t* __restrict__ U, const int8_t* __restrict__ V, Geo g,
+__global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __restrict__ U, const int8_t* __restrict__ V, Geo g,
                                          Acc* __restrict__ acc, const Acc* __restrict__ wacc, int wstage, int qmax_u,
                                          int qmax_v, const unsigned* __restrict__ table, int bn) {
-  // table[(xi * T + t) * nchunk + chunk]: each thread owns one tile row t (its group max loaded once)
-  // and walks its 36 * nchunk entries; a warp's 32 consecutive rows read contiguous table segments.
-  // An entry equal to the group's exact max is recomputed by the whole warp (rare).
+  // Flat, fully parallel scan: thread per (xi, t) table row (nchunk <= 4 entries, one 16-byte load
+  // when nchunk == 4); consecutive threads read consecutive rows.  An entry equal to its group's exact
+  // max is recomputed by the whole warp (rare): lanes over the entry's output columns.
   const int nchunk = g.Kp / bn;
   const int lane = threadIdx.x & 31;
   const unsigned T = (unsigned)g.T;
-  const unsigned nthr = gridDim.x * blockDim.x;
-  for (unsigned t0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; t0 < T; t0 += nthr) {
-    const unsigned t = t0 + lane;
-    const bool valid = t < T;
-    const int grp = valid ? (int)g.fipg.div(g.fTP.div(t)) : 0;
+  const unsigned long long rows = 36ull * T;
+  const unsigned long long nthr = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long r0 = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; r0 < rows;
+       r0 += nthr) {
+    const unsigned long long r = r0 + lane;
+    const bool valid = r < rows;
+    const unsigned xi = valid ? (unsigned)(r / T) : 0u;
+    const unsigned t = valid ? (unsigned)(r - (unsigned long long)xi * T) : 0u;
+    const int grp = (int)g.fipg.div(g.fTP.div(t));
     const unsigned long long M = valid ? acc[(size_t)grp * ST_COUNT + ST_HAD].M : 0ull;
-    for (int xi = 0; xi < 36; ++xi) {
-      const unsigned* row = table + ((size_t)xi * T + t) * nchunk;
-      for (int chunk = 0; chunk < nchunk; ++chunk) {
-        const unsigned v = valid ? row[chunk] : 0u;
-        unsigned mask = __ballot_sync(0xffffffffu, v != 0 && (unsigned long long)v == M);
-        while (mask) {
-          const int l = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const int tl = (int)t0 + l;
-          const int gl = __shfl_sync(0xffffffffu, grp, l);
-          Acc* ga = acc + (size_t)gl * ST_COUNT;
-          const long long Ml = (long long)ga[ST_HAD].M;
-          const int8_t* vrow = V + ((size_t)tl * 36 + xi) * g.Cp;
-          double f = 0.0;
-          for (int k = chunk * bn + lane; k < min(chunk * bn + bn, g.K); k += 32) {
-            const int8_t* urow = U + ((size_t)k * 36 + xi) * g.Cp;
-            long long sdot = 0;
-            for (int c = 0; c < g.C; ++c) sdot += (int)urow[c] * (int)vrow[c];
-            if ((sdot < 0 ? -sdot : sdot) == Ml)
-              f = fmax(f, fabs(replay_hadamard(urow, vrow, g.C, load_int_stage(wacc[wstage], qmax_u),
-                                               load_int_stage(ga[ST_IT], qmax_v))));
-          }
-          if (f > 0.0) atomicMax(&ga[ST_HAD].F, dbits(f));
+    unsigned v[4] = {0u, 0u, 0u, 0u};
+    if (valid) {
+      if (nchunk == 4) {
+        const uint4 q = *reinterpret_cast<const uint4*>(table + r * 4);
+        v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+      } else {
+        for (int c = 0; c < nchunk && c < 4; ++c) v[c] = table[r * nchunk + c];
+      }
+    }
+    for (int chunk = 0; chunk < nchunk; ++chunk) {
+      const unsigned vc = chunk < 4 ? v[chunk & 3] : (valid ? table[r * nchunk + chunk] : 0u);
+      unsigned mask = __ballot_sync(0xffffffffu, valid && vc != 0 && (unsigned long long)vc == M);
+      while (mask) {
+        const int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int tl = (int)__shfl_sync(0xffffffffu, t, l);
+        const int xl = (int)__shfl_sync(0xffffffffu, xi, l);
+        const int gl = __shfl_sync(0xffffffffu, grp, l);
+        Acc* ga = acc + (size_t)gl * ST_COUNT;
+        const long long Ml = (long long)ga[ST_HAD].M;
+        const int8_t* vrow = V + ((size_t)tl * 36 + xl) * g.Cp;
+        double f = 0.0;
+        for (int k = chunk * bn + lane; k < min(chunk * bn + bn, g.K); k += 32) {
+          const int8_t* urow = U + ((size_t)k * 36 + xl) * g.Cp;
+          long long sdot = 0;
+          for (int c = 0; c < g.C; ++c) sdot += (int)urow[c] * (int)vrow[c];
+          if ((sdot < 0 ? -sdot : sdot) == Ml)
+            f = fmax(f, fabs(replay_hadamard(urow, vrow, g.C, load_int_stage(wacc[wstage], qmax_u),
+                                             load_int_stage(ga[ST_IT], qmax_v))));
         }
+        if (f > 0.0) atomicMax(&ga[ST_HAD].F, dbits(f));
       }
     }
   }

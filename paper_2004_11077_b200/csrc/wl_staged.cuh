@@ -292,7 +292,7 @@ struct StagedOut {
   static constexpr int smem() { return 2 * in_bytes<ST>() + OUT_BYTES + 16; }
 };
 
-template <int MODE, typename HT>
+template <int MODE, typename HT, bool TAB>
 __global__ void __launch_bounds__(StagedOut::THREADS, 3)
     sout_c_kernel(const __grid_constant__ CUtensorMap srcmap, const HT* __restrict__ h,
                   const int8_t* __restrict__ c4, float* __restrict__ y, const float* __restrict__ bias,
@@ -306,10 +306,13 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
   uint8_t* sm = wl_stage_smem;
   float* so = reinterpret_cast<float*>(sm + 2 * IN_BYTES);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 2 * IN_BYTES + S::OUT_BYTES);
+  __shared__ long long ybase[S::TPB];  // y offset of (n, k0, 4*ty, 4*tx) per tile of the item, -1 if t >= T
+  __shared__ int yrows[S::TPB];        // rows of the tile inside Ho
   const int nkb = (g.K + S::KB - 1) / S::KB;
   const int niter = ((g.T + S::TPB - 1) / S::TPB) * nkb;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qo = b.q[ST_OUT];
+  const long long plane = (long long)g.Ho * g.Wo;
   using LOT = std::conditional_t<MODE == 0, tab::Can_OT, tab::Leg_OT>;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -330,6 +333,19 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
     if (threadIdx.x == 0 && it + (int)gridDim.x < niter) issue(it + gridDim.x, s ^ 1);
     const int tg = it / nkb, kb = it - tg * nkb;
     const int t0 = tg * S::TPB, k0 = kb * S::KB;
+    if (threadIdx.x < S::TPB) {
+      const int t = t0 + threadIdx.x;
+      long long base = -1;
+      int rows = 0;
+      if (t < g.T) {
+        const int n = (int)g.fTP.div((unsigned)t), tile = t - n * g.TP;
+        const int ty = (int)g.ftw.div((unsigned)tile), tx = tile - ty * g.tw;
+        base = ((long long)n * g.K + k0) * plane + (long long)(4 * ty) * g.Wo + 4 * tx;
+        rows = min(4, g.Ho - 4 * ty);
+      }
+      ybase[threadIdx.x] = base;
+      yrows[threadIdx.x] = rows;
+    }
     mbar_wait(&bar[s], (uint32_t)((kk >> 1) & 1));
     {
       const int t = t0 + w, k = k0 + lane;
@@ -339,12 +355,14 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
       const Acc* ga = acc + (size_t)grp * ST_COUNT;
       // inactive lanes (padded channels hold arbitrary codes) requantise with r = 0 -> code 0
       const float r = active ? ga[ST_OUT].r : 0.f, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
-      const float* tabg = otab ? otab + (size_t)grp * (2 * qo + 1) + qo : nullptr;
+      const float* tabg = TAB ? otab + (size_t)grp * (2 * qo + 1) + qo : nullptr;
       const double scale = ga[ST_OUT].scale;
       const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
       auto deqf = [=](int code) -> float {
-        if (tabg) return __ldg(tabg + code);
-        return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+        if constexpr (TAB)
+          return __ldg(tabg + code);
+        else
+          return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
       };
       const float bk = (bias && active) ? __ldg(&bias[k]) : 0.f;
       float X[6][6];
@@ -362,7 +380,7 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
         dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<LOT>(), dcol));
       });
       const bool want = dmax > thr && active;
-      if (want && !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want))
+      if (__any_sync(0xffffffffu, want) && want && !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want))
         fix_out_unit_to<MODE, HT, float>(h, c4, bias, g, b, acc, pf, t, k, (uint32_t)g.Kp,
                                          [o](int i, int j, float v) { o[4 * i + j] = v; });
     }
@@ -372,21 +390,18 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
     for (int rep = 0; rep < (S::KB * 4 * S::TPB) / S::THREADS; ++rep) {
       const int q = rep * S::THREADS + threadIdx.x;
       const int tq = q & (S::TPB - 1), i = (q / S::TPB) & 3, kq = q / (4 * S::TPB);
-      const int t = t0 + tq, k = k0 + kq;
-      if (t >= g.T || k >= g.K) continue;
-      const int n = (int)g.fTP.div((unsigned)t), tile = t - n * g.TP;
-      const int ty = (int)g.ftw.div((unsigned)tile), tx = tile - ty * g.tw;
-      const int rr = 4 * ty + i;
-      if (rr >= g.Ho) continue;
+      const long long base = ybase[tq];
+      if (base < 0 || k0 + kq >= g.K || i >= yrows[tq]) continue;
       const float4 v = *reinterpret_cast<const float4*>(so + kq * S::OK + tq * S::OT + 4 * i);
-      float* row = y + (((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + 4 * tx;
+      float* row = y + base + kq * plane + (long long)i * g.Wo;
       if ((g.Wo & 3) == 0) {
         __stcs(reinterpret_cast<float4*>(row), v);
       } else {
+        const int cols = g.Wo - (int)((base % g.Wo));
         const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (4 * tx + j < g.Wo) row[j] = vv[j];
+          if (j < cols) row[j] = vv[j];
       }
     }
     __syncthreads();
