@@ -130,25 +130,31 @@ namespace wl {
 // BN-column accumulators so the 8 epilogue warps drain tile i while the MMA warp fills tile i+1 and
 // the TMA warp streams tile i+2's operands.  Barriers: smem ring full/empty[STAGES], accumulator
 // full[2] (tcgen05.commit) / empty[2] (8 epilogue-warp arrivals).
-constexpr int kEpiGroups = 4;                          // column groups per TMEM lane quarter
-constexpr int kEpiWarps = 4 * kEpiGroups;              // 16 epilogue warps
-constexpr int kGemmPThreads = 64 + 32 * kEpiWarps;     // w0 TMA, w1 MMA + TMEM owner, w2.. epilogue
+// Column groups per TMEM lane quarter are the epilogue's choice (Epi::kGroups): 4 (16 epilogue
+// warps) for the light max pass; 2 (8 warps, no spills under the register cap) for requantisation.
+template <int G>
+struct EpiShape {
+  static constexpr int kGroups = G;
+  static constexpr int kWarps = 4 * G;
+  static constexpr int kThreads = 64 + 32 * kWarps;  // w0 TMA, w1 MMA + TMEM owner, w2.. epilogue
+};
 
-template <int BN, int SW, int STAGES, int EPI_STAGE = 0>
+template <int BN, int SW, int STAGES, int EPI_STAGE = 0, int EPI_WARPS = 16>
 struct GemmPSmem {
   static constexpr int kA = 128 * SW;
   static constexpr int kB = BN * SW;
-  static constexpr int kEpi = kEpiWarps * EPI_STAGE;  // per-epilogue-warp staging bytes
+  static constexpr int kEpi = EPI_WARPS * EPI_STAGE;  // per-epilogue-warp staging bytes
   static constexpr int kBytes = 1024 + STAGES * (kA + kB) + 512 + kEpi;
 };
 
 template <int BN, int SW, int STAGES, class Epi>
-__global__ void __launch_bounds__(kGemmPThreads, 1)
+__global__ void __launch_bounds__(EpiShape<Epi::kGroups>::kThreads, 1)
     gemm_i8_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int T,
                        int Kout, int Cpad, int Kpad, Epi epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  using L = GemmPSmem<BN, SW, STAGES, Epi::kStageBytes>;
+  constexpr int kEpiGroups = Epi::kGroups, kEpiWarps = 4 * kEpiGroups;
+  using L = GemmPSmem<BN, SW, STAGES, Epi::kStageBytes, kEpiWarps>;
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * L::kA;
   uint8_t* sEpi = sB + STAGES * L::kB;  // kEpiWarps x Epi::kStageBytes (16-byte aligned)
@@ -249,12 +255,13 @@ __global__ void __launch_bounds__(kGemmPThreads, 1)
       decode(tile, xi, mb, nb);
       const int a = local & 1;
       const uint32_t aph = (local >> 1) & 1;
+      const int row = mb * 128 + 32 * q + lane;
+      // per-row parameters (global loads) before the wait: their latency overlaps the MMA
+      epi.begin(xi, row, row < T);
       mbar_wait(&accfull[a], aph);
       tc_fence_after();
-      const int row = mb * 128 + 32 * q + lane;
       const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + (uint32_t)(a * BN + half * HC);
       const int n0 = nb * BN + half * HC;
-      epi.begin(xi, row, row < T);
       static_assert(HC % 16 == 0, "epilogue column group must be a multiple of 16");
 #pragma unroll 1
       for (int c = 0; c < HC; c += 32) {

@@ -215,7 +215,7 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   o = align256(o + (size_t)36 * g.T * g.Cp);
   L->off_c4 = o;
   o = align256(o + (size_t)36 * g.T * g.Kp);
-  L->bn = (g.Kp >= 256 ? 256 : g.Kp) / kEpiGroups;  // table chunk = one epilogue warp's columns
+  L->bn = (g.Kp >= 256 ? 256 : g.Kp) / 4;  // table chunk = one max-pass epilogue warp's columns (EpiHadMax::kGroups)
   const size_t CB = (g.C + 31) / 32, KB = (g.K + 31) / 32;
   const size_t ents[kNumTables] = {g.T * CB, g.T * CB, (size_t)36 * g.T * (g.Kp / L->bn), g.T * KB, g.T * KB};
   for (int i = 0; i < kNumTables; ++i) {
@@ -304,6 +304,7 @@ static int dispatch_ld_out(int ld, F&& f) {
 // reduced in place (atomicMax) and units that may hold the argmax are pushed as candidates for the
 // fp64 replay in finalize_hadamard_kernel.
 struct EpiHadMax {
+  static constexpr int kGroups = 4;
   static constexpr int kStageBytes = 0;
   Acc* acc;
   unsigned* table;
@@ -345,6 +346,43 @@ struct EpiHadMax {
   }
 };
 
+// Exact requantisation of 8 Hadamard accumulators of one row (rare path: the fp32 bracket split for
+// some element of the chunk): int64 rounding, fp64 replay of exact ties.  Returns the packed codes
+// (int8: 2 words, int16: 4 words).  A free function taking values, so the epilogue functor and its
+// arrays stay in registers.
+struct HadRqCtx {
+  const Acc* acc;
+  const Acc* wacc;
+  const int8_t* U;
+  const int8_t* V;
+  int C, Cp, grp, wstage, qmax_u, qmax_v, qmax_h, xi, row;
+};
+template <typename HT>
+static __device__ __noinline__ uint4 had_rq_slow8(HadRqCtx cx, uint4 va, uint4 vb, int col, int n) {
+  const StageQ q = load_int_stage(cx.acc[(size_t)cx.grp * ST_COUNT + ST_HAD], cx.qmax_h);
+  const uint32_t v[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    bool tie = false;
+    int code = rq((long long)(int)v[j], q, tie);
+    if (tie && j < n) {
+      const StageQ qu = load_int_stage(cx.wacc[cx.wstage], cx.qmax_u);
+      const StageQ qv = load_int_stage(cx.acc[(size_t)cx.grp * ST_COUNT + ST_IT], cx.qmax_v);
+      code = code_of(replay_hadamard(cx.U + ((size_t)(col + j) * 36 + cx.xi) * cx.Cp,
+                                     cx.V + ((size_t)cx.row * 36 + cx.xi) * cx.Cp, cx.C, qu, qv),
+                     q);
+    }
+    c[j] = (uint32_t)code;
+  }
+  if constexpr (sizeof(HT) == 1)
+    return make_uint4(__byte_perm(__byte_perm(c[0], c[1], 0x0040), __byte_perm(c[2], c[3], 0x0040), 0x5410),
+                      __byte_perm(__byte_perm(c[4], c[5], 0x0040), __byte_perm(c[6], c[7], 0x0040), 0x5410), 0u, 0u);
+  else
+    return make_uint4(__byte_perm(c[0], c[1], 0x5410), __byte_perm(c[2], c[3], 0x5410), __byte_perm(c[4], c[5], 0x5410),
+                      __byte_perm(c[6], c[7], 0x5410));
+}
+
 // Requantisation pass: h = rhe(qmax_h * I / M) with the fp32 magic-number fast path (I is exact and
 // |I| < 2^24, so the only inexactness is the product by qmax/M); near half-integers the exact int64
 // decision, and exact ties are replayed in fp64 from the U and V codes.
@@ -352,8 +390,9 @@ template <typename HT>
 struct EpiHadRq {
   // each epilogue warp stages its 32 rows x 128 columns of codes (swizzled 16-byte slots) and
   // writes them back as whole row segments
-  static constexpr int kStageBytes = 32 * 64 * (int)sizeof(HT);
-  static constexpr int kRowBytes = 64 * (int)sizeof(HT);
+  static constexpr int kGroups = 2;
+  static constexpr int kStageBytes = 32 * (256 / kGroups) * (int)sizeof(HT);
+  static constexpr int kRowBytes = (256 / kGroups) * (int)sizeof(HT);
   static constexpr int kSwz = kRowBytes / 16 - 1;  // XOR swizzle of the 16-byte slots within a row
   uint8_t* stage;
   int hc;  // columns per epilogue warp (half the N tile)
@@ -372,6 +411,7 @@ struct EpiHadRq {
   float r_lo, r_hi;
   int grp;
   bool small;  // |I| < 2^22: int -> float by the magic-number add instead of I2F
+  bool dummy;  // experiment switch (WL_DUMMY_EPI): skip the requantisation arithmetic
   __device__ __forceinline__ void begin(int, int row, bool valid) {
     grp = valid ? (int)g.fipg.div(g.fTP.div((unsigned)row)) : 0;
     const Acc& a = acc[(size_t)grp * ST_COUNT + ST_HAD];
@@ -386,39 +426,59 @@ struct EpiHadRq {
     small = (long long)g.C * qmax_u * qmax_v < (1LL << 22);
   }
   __device__ __forceinline__ void apply(int xi, int row, int col, const uint32_t* v, int n) {
-    HT out[16];
-    uint32_t diff = 0;
+    // y[j] = 0x4B400000 + code: its low byte / half-word is the two's-complement code
+    uint32_t y[16];
+    uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;  // independent chains (ILP)
+    if (dummy) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float fi = small ? __int_as_float((int)v[j] + 0x4B400000) - kMagic : (float)(int)v[j];
-      const uint32_t y1 = __float_as_uint(fmaf(fi, r_lo, kMagic));
-      const uint32_t y2 = __float_as_uint(fmaf(fi, r_hi, kMagic));
-      diff |= y1 ^ y2;
-      out[j] = (HT)(int)y1;  // low byte / half-word of 0x4B400000 + code is the two's-complement code
-    }
-    if (diff != 0) {
-      const StageQ q = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h);
+      for (int j = 0; j < 16; ++j) y[j] = v[j];
+    } else if (small) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        bool tie = false;
-        int code = rq((long long)(int)v[j], q, tie);
-        if (tie && j < n) {
-          const StageQ qu = load_int_stage(wacc[wstage], qmax_u);
-          const StageQ qv = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_IT], qmax_v);
-          code = code_of(replay_hadamard(U + ((size_t)(col + j) * 36 + xi) * g.Cp,
-                                         V + ((size_t)row * 36 + xi) * g.Cp, g.C, qu, qv), q);
-        }
-        out[j] = (HT)code;
+        const float fi = __int_as_float((int)v[j] + 0x4B400000) - kMagic;
+        y[j] = __float_as_uint(fmaf(fi, r_lo, kMagic));
+        const uint32_t d = y[j] ^ __float_as_uint(fmaf(fi, r_hi, kMagic));
+        if ((j & 3) == 0) d0 |= d; else if ((j & 3) == 1) d1 |= d; else if ((j & 3) == 2) d2 |= d; else d3 |= d;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float fi = (float)(int)v[j];
+        y[j] = __float_as_uint(fmaf(fi, r_lo, kMagic));
+        const uint32_t d = y[j] ^ __float_as_uint(fmaf(fi, r_hi, kMagic));
+        if ((j & 3) == 0) d0 |= d; else if ((j & 3) == 1) d1 |= d; else if ((j & 3) == 2) d2 |= d; else d3 |= d;
       }
     }
-    // stage: row `lane` of this warp, 16-byte slot (column offset within the half / 16 bytes)
+    const bool exact = ((d0 | d1) | (d2 | d3)) != 0;  // rare: some element's bracket split
     const int lane = threadIdx.x & 31;
     const int slot0 = ((col % hc) * (int)sizeof(HT)) >> 4;
+    const uint32_t rbase = smem_u32(stage) + lane * kRowBytes;
+    const HadRqCtx cx{acc, wacc, U, V, g.C, g.Cp, grp, wstage, qmax_u, qmax_v, qmax_h, xi, row};
+    if constexpr (sizeof(HT) == 1) {
+      uint32_t w[4];
 #pragma unroll
-    for (int v = 0; v < (int)sizeof(HT); ++v) {
-      const int slot = slot0 + v;
-      *reinterpret_cast<int4*>(stage + lane * kRowBytes + ((slot ^ (lane & kSwz)) << 4)) =
-          reinterpret_cast<const int4*>(out)[v];
+      for (int q = 0; q < 4; ++q)
+        w[q] = __byte_perm(__byte_perm(y[4 * q], y[4 * q + 1], 0x0040), __byte_perm(y[4 * q + 2], y[4 * q + 3], 0x0040),
+                           0x5410);
+      if (exact) {
+        const uint4 lo = had_rq_slow8<HT>(cx, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]), col, n);
+        const uint4 hi = had_rq_slow8<HT>(cx, make_uint4(v[8], v[9], v[10], v[11]), make_uint4(v[12], v[13], v[14], v[15]),
+                                          col + 8, n - 8);
+        w[0] = lo.x, w[1] = lo.y, w[2] = hi.x, w[3] = hi.y;
+      }
+      st_shared_v4(rbase + ((slot0 ^ (lane & kSwz)) << 4), w[0], w[1], w[2], w[3]);
+    } else {
+      uint32_t w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = __byte_perm(y[2 * q], y[2 * q + 1], 0x5410);
+      if (exact) {
+        const uint4 lo = had_rq_slow8<HT>(cx, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]), col, n);
+        const uint4 hi = had_rq_slow8<HT>(cx, make_uint4(v[8], v[9], v[10], v[11]), make_uint4(v[12], v[13], v[14], v[15]),
+                                          col + 8, n - 8);
+        w[0] = lo.x, w[1] = lo.y, w[2] = lo.z, w[3] = lo.w, w[4] = hi.x, w[5] = hi.y, w[6] = hi.z, w[7] = hi.w;
+      }
+      st_shared_v4(rbase + ((slot0 ^ (lane & kSwz)) << 4), w[0], w[1], w[2], w[3]);
+      st_shared_v4(rbase + (((slot0 + 1) ^ (lane & kSwz)) << 4), w[4], w[5], w[6], w[7]);
     }
   }
   __device__ __forceinline__ void finish_chunk(int, int, bool, int) {}
@@ -432,7 +492,7 @@ struct EpiHadRq {
       const int r = r0 + lane / kSlots, sl = lane % kSlots;
       const int row = row0 + r;
       if (row < T && sl * 16 < nbytes) {
-        const int4 v = *reinterpret_cast<const int4*>(stage + r * kRowBytes + ((sl ^ (r & kSwz)) << 4));
+        const int4 v = ld_shared_v4(smem_u32(stage) + r * kRowBytes + ((sl ^ (r & kSwz)) << 4));
         *reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(h + ((size_t)row * 36 + xi) * g.Kp + n0) + sl * 16) = v;
       }
     }
@@ -454,7 +514,7 @@ static int num_sms() {
 template <int BN, int SW, class Epi>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo& g, const Epi& e, cudaStream_t st) {
   constexpr int STAGES = Epi::kStageBytes > 0 ? 3 : 4;
-  using L = GemmPSmem<BN, SW, STAGES, Epi::kStageBytes>;
+  using L = GemmPSmem<BN, SW, STAGES, Epi::kStageBytes, 4 * Epi::kGroups>;
   auto kern = gemm_i8_persistent<BN, SW, STAGES, Epi>;
   static bool attr_set = false;  // per instantiation; idempotent
   if (!attr_set) {
@@ -463,7 +523,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo& 
   }
   const int ntiles = 36 * ((g.T + 127) / 128) * (g.Kp / BN);
   const int grid = std::min(ntiles, num_sms());
-  kern<<<grid, kGemmPThreads, L::kBytes, st>>>(ta, tb, g.T, g.K, g.Cp, g.Kp, e);
+  kern<<<grid, EpiShape<Epi::kGroups>::kThreads, L::kBytes, st>>>(ta, tb, g.T, g.K, g.Cp, g.Kp, e);
   WL_CUDA(cudaGetLastError());
   return WL_OK;
 }
@@ -480,7 +540,7 @@ static int dispatch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo
 }
 
 // N tile = whole padded Kout up to 256 (2 TMEM accumulators of BN columns); the max tables hold one
-// entry per epilogue warp's column group (BN / kEpiGroups columns).
+// entry per max-pass epilogue warp column group (BN / EpiHadMax::kGroups columns).
 static void gemm_tiles(const Geo& g, int* bn, int* sw) {
   *bn = g.Kp >= 256 ? 256 : g.Kp;  // must match Layout::bn
   *sw = g.Cp % 128 == 0 ? 128 : (g.Cp % 64 == 0 ? 64 : 32);
@@ -902,6 +962,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     e.qmax_u = qu;
     e.qmax_v = b.q[ST_IT];
     e.qmax_h = b.q[ST_HAD];
+    e.dummy = getenv("WL_DUMMY_EPI") != nullptr;
     rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
   } else {
     EpiHadRq<int16_t> e;
@@ -915,6 +976,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     e.qmax_u = qu;
     e.qmax_v = b.q[ST_IT];
     e.qmax_h = b.q[ST_HAD];
+    e.dummy = getenv("WL_DUMMY_EPI") != nullptr;
     rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
   }
   if (rc) return rc;

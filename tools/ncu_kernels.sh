@@ -3,7 +3,7 @@
 # details page and the condensed summary to gpurun_out/ (the .ncu-rep stays in /tmp: too large).
 RX=${1:-gemm}; N=${2:-256}; TAG=${3:-k}
 python tools/prof_forward.py --n $N --iters 1 > gpurun_out/plain_$TAG.log 2>&1 || exit 1
-ncu --set full --clock-control none --import-source on -k regex:"$RX" -c 6 -o /tmp/prof_$TAG \
+ncu -f --set full --clock-control none --import-source on -k regex:"$RX" -c 6 -o /tmp/prof_$TAG \
     python tools/prof_forward.py --n $N --iters 1 > gpurun_out/ncu_$TAG.log 2>&1
 ncu -i /tmp/prof_$TAG.ncu-rep --page details > gpurun_out/details_$TAG.txt 2>&1
 python tools/ncu_summary.py /tmp/prof_$TAG.ncu-rep gpurun_out/summary_$TAG.csv > /dev/null
