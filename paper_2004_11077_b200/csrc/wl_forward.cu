@@ -152,7 +152,7 @@ static const int kTableStage[kNumTables] = {ST_IBC, ST_IT, ST_HAD, ST_OBC, ST_OU
 
 struct Layout {
   Geo g;
-  size_t off_acc, off_c0, off_v, off_h, off_c1, off_c4, off_tab[kNumTables], tab_bytes[kNumTables], off_otab, off_fix,
+  size_t off_acc, off_c0, off_v, off_h, off_c1, off_c4, off_t4, off_e4, off_tab[kNumTables], tab_bytes[kNumTables], off_otab, off_fix,
       total;
   unsigned fix_cap;
   int groups, hbytes, bn;
@@ -215,6 +215,11 @@ static int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L) {
   o = align256(o + (size_t)36 * g.T * g.Cp);
   L->off_c4 = o;
   o = align256(o + (size_t)36 * g.T * g.Kp);
+  // Legendre fp32-output path: output-stage fast-path values T4 [T][16][Kp] and error factors [T][Kp]
+  L->off_t4 = o;
+  o = align256(o + (size_t)16 * g.T * g.Kp * sizeof(float));
+  L->off_e4 = o;
+  o = align256(o + (size_t)g.T * g.Kp * sizeof(float));
   L->bn = (g.Kp >= 256 ? 256 : g.Kp) / 4;  // table chunk = one max-pass epilogue warp's columns (EpiHadMax::kGroups)
   const size_t CB = (g.C + 31) / 32, KB = (g.K + 31) / 32;
   const size_t ents[kNumTables] = {g.T * CB, g.T * CB, (size_t)36 * g.T * (g.Kp / L->bn), g.T * KB, g.T * KB};
@@ -835,6 +840,10 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
   }
   int8_t* c1 = reinterpret_cast<int8_t*>(ws + L.off_c1);
   int8_t* c4 = reinterpret_cast<int8_t*>(ws + L.off_c4);
+  float* t4 = reinterpret_cast<float*>(ws + L.off_t4);
+  float* e4 = reinterpret_cast<float*>(ws + L.off_e4);
+  // Legendre, fp32 output, staged output side: store T4 instead of c4 (WL_NO_T4 = the c4 path)
+  const bool t4path = leg && sizeof(YT) == 4 && g.Kp <= 256 && !getenv("WL_NO_T4");
   Tables tabs;
   for (int i = 0; i < ST_COUNT; ++i) tabs.t[i] = nullptr;
   for (int i = 0; i < kNumTables; ++i) {
@@ -1048,6 +1057,43 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC], stage_depth(plan->mode, ST_OBC));
         prof_mark("output_base_change_max", st);
+        if (t4path) {
+          // T4 path: the output stage's fp32 values + error factors are stored instead of c4
+          using ST4 = StagedT4<LDs, sizeof(HT)>;
+          auto kbt = sout_bt_kernel<HT, LDs>;
+          sout_bt_kernel<HT, LDs><<<staged_grid(kbt, ST4::THREADS, ST4::SMEM, iters), ST4::THREADS, ST4::SMEM, st>>>(
+              hh, t4, e4, g, b, acc, plan->d_pf, tabs, fl);
+          fixup_obct_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, t4, e4, g, b, acc, plan->d_pf, tabs);
+          finalize_output_kernel<1, ST_OUT, HT, true><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+          stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
+          prof_mark("output_max", st);
+          make_otab();
+          if (sizeof(YT) == 4) {
+            CUtensorMap tm4, em4;
+            if (!make_tmap_3d_plain(&tm4, t4, 4, (uint64_t)g.Kp, 16, (uint64_t)g.T, StagedOut::KB, 16, StagedOut::TPB) ||
+                !make_tmap_3d_plain(&em4, e4, 4, (uint64_t)g.Kp, 1, (uint64_t)g.T, StagedOut::KB, 1, StagedOut::TPB)) {
+              oc_rc = fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled (T4) failed");
+              return;
+            }
+            constexpr int smem = 2 * (StagedOut::TPB * 17 * StagedOut::KB * 4) + StagedOut::OUT_BYTES + 16;
+            const long long oiters = (long long)((g.T + StagedOut::TPB - 1) / StagedOut::TPB) * ((g.K + StagedOut::KB - 1) / StagedOut::KB);
+            auto launch = [&](auto tabc) {
+              constexpr bool TAB = decltype(tabc)::value;
+              auto kern = sout_ct_kernel<HT, TAB>;
+              sout_ct_kernel<HT, TAB><<<staged_grid(kern, StagedOut::THREADS, smem, oiters), StagedOut::THREADS, smem, st>>>(
+                  tm4, em4, hh, reinterpret_cast<float*>(y), reinterpret_cast<const float*>(bias), g, b, acc, plan->d_pf,
+                  otab, fl);
+            };
+            if (otab)
+              launch(std::true_type{});
+            else
+              launch(std::false_type{});
+            fixup_outt_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, reinterpret_cast<float*>(y),
+                                                              reinterpret_cast<const float*>(bias), g, b, acc, plan->d_pf);
+          }
+          prof_mark("output_write", st);
+          return;
+        }
         auto kb = sout_b_kernel<HT, LDs>;
         sout_b_kernel<HT, LDs><<<staged_grid(kb, SH::THREADS, SH::SMEM_OUT, iters), SH::THREADS, SH::SMEM_OUT, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
         fixup_obc_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, g, b, acc, plan->d_pf, tabs);

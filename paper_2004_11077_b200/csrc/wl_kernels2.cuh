@@ -682,7 +682,32 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
     fix_out_unit<MODE, HT, YT>(h, c4, y, bias, g, b, acc, pf, t, k, plane);
 }
 
-template <int MODE, int STAGE, typename HT>
+// Exact c4 codes of one unit from its h codes (int64 sandwich, ties replayed in fp64); these are the
+// codes the fast path produces after its certified fixes.
+template <typename HT>
+__device__ __forceinline__ void exact_c4_from_h(const HT* __restrict__ h, uint32_t plane, uint32_t off, const Acc* ga,
+                                                const Bits& b, const PlanF64* __restrict__ pf, int (&c4)[6][6]) {
+  int Xi[6][6];
+  load_planes(h, plane, off, Xi);
+  long long T3[6][6];
+  sandwich<tab::Leg_OBC>(Xi, T3);
+  const StageQ q = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
+#pragma unroll
+  for (int e = 0; e < 36; ++e) {
+    bool tie = false;
+    int code = rq(T3[e / 6][e % 6], q, tie);
+    if (tie) {
+      int xc[36];
+#pragma unroll
+      for (int u = 0; u < 36; ++u) xc[u] = Xi[u / 6][u % 6];
+      const StageQ qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
+      code = code_of(replay_sandwich(pf->obc, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6), q);
+    }
+    c4[e / 6][e % 6] = code;
+  }
+}
+
+template <int MODE, int STAGE, typename HT, bool FROM_H = false>
 __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __restrict__ c4, const Geo& g, const Bits& b,
                                   Acc* acc, const PlanF64* pf, int t, int k) {
   const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
@@ -718,7 +743,10 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
     for (int e = 0; e < 16; ++e) Y[e / 4][e % 4] = Y32[e / 4][e % 4];
     qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
   } else {
-    load_planes(c4, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
+    if constexpr (FROM_H)
+      exact_c4_from_h<HT>(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + (uint32_t)k, ga, b, pf, Xi);
+    else
+      load_planes(c4, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
     sandwich<tab::Leg_OT>(Xi, Y);
     qin = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
   }
@@ -738,7 +766,7 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
   atomicMax(&ga[ST_OUT].F, dbits(f));
 }
 
-template <int MODE, int STAGE, typename HT>
+template <int MODE, int STAGE, typename HT, bool FROM_H = false>
 __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4, Geo g, Bits b,
                                        Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
                                        const unsigned* __restrict__ table, float rowsum) {
@@ -765,7 +793,7 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
         const int l = __ffs(mask) - 1;
         mask &= mask - 1;
         const int tl = (int)t0 + l, ch = cb * 32 + lane;
-        if (ch < g.K) exact_output_unit<MODE, STAGE, HT>(h, c4, g, b, acc, pf, tl, ch);
+        if (ch < g.K) exact_output_unit<MODE, STAGE, HT, FROM_H>(h, c4, g, b, acc, pf, tl, ch);
       }
     }
   }

@@ -408,4 +408,349 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
   }
 }
 
+
+// ------------------------------------------------------------------ Legendre output stage via T4
+// With fp32 outputs the Legendre output side stores the output stage's fp32 fast-path values
+// T4 = A_P^T c4 A_P (16 floats per unit, [T][16][Kp]) plus the unit's error factor
+// e4 = rowsum(A_P) * max_j |first-half column j| ([T][Kp]) instead of the 36 c4 codes: the final
+// pass then reads 68 bytes per unit and only requantises (no second A_P sandwich).  c4 stays
+// implicit: any unit whose decision needs exact values recomputes c4 exactly from h.
+
+// Exact output codes of one unit (all 16 elements) from h: c4 exactly, then A_P^T c4 A_P in int64,
+// ties replayed in fp64 from c4.  put(i, j, code).
+template <typename HT, class Put>
+__device__ __noinline__ void exact_out_from_h(const HT* __restrict__ h, const Geo& g, const Bits& b, const Acc* acc,
+                                              const PlanF64* __restrict__ pf, int t, int k, Put put) {
+  const int n = (int)g.fTP.div((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
+  const Acc* ga = acc + (size_t)grp * ST_COUNT;
+  int c4[6][6];
+  exact_c4_from_h<HT>(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + (uint32_t)k, ga, b, pf, c4);
+  long long Y[4][4];
+  sandwich<tab::Leg_OT>(c4, Y);
+  const StageQ q = load_int_stage(ga[ST_OUT], b.q[ST_OUT]);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    bool tie = false;
+    int code = rq(Y[e / 4][e % 4], q, tie);
+    if (tie) {
+      int xc[36];
+#pragma unroll
+      for (int u = 0; u < 36; ++u) xc[u] = c4[u / 6][u % 6];
+      const StageQ qin = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
+      code = code_of(replay_sandwich(pf->ot, 4, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 4, e % 4), q);
+    }
+    put(e / 4, e % 4, code);
+  }
+}
+
+// Exact output values (dequantised + bias) of one unit into o[4 * i + j] (shared staging); tabg is the
+// group's dequant table (or null: fp64 formula).  No closures: every argument by value.
+template <typename HT>
+__device__ __noinline__ void exact_out_to(const HT* __restrict__ h, const Geo& g, const Bits& b, const Acc* acc,
+                                          const PlanF64* __restrict__ pf, int t, int k, float* o,
+                                          const float* __restrict__ tabg, float bk) {
+  const int n = (int)g.fTP.div((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
+  const Acc* ga = acc + (size_t)grp * ST_COUNT;
+  const int qo = b.q[ST_OUT];
+  const double scale = ga[ST_OUT].scale;
+  const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
+  int codes[16];
+  exact_out_from_h<HT>(h, g, b, acc, pf, t, k, [&codes](int i, int j, int code) { codes[4 * i + j] = code; });
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int code = codes[e];
+    const float v = tabg ? tabg[code]
+                         : (code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale)));
+    o[e] = v + bk;
+  }
+}
+
+// T4 (fp32 fast path) + error factor of one unit from its float c4 codes; returns the cropped max and
+// the first-half max through m / tm.
+__device__ __forceinline__ void t4_of_unit(const float (&K4)[6][6], int ty, int tx, const Geo& g, float* ot, int ostride,
+                                           float& efac, float& m, float& tm) {
+  float cmax = 0.f;
+  m = 0.f;
+  tm = 0.f;
+  sandwich_cols<tab::Leg_OT>(K4, [&](int j, const float (&col)[4], float cm) {
+    cmax = fmaxf(cmax, cm);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ot[(4 * i + j) * ostride] = col[i];
+      if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[i]));
+    }
+  }, &tm);
+  efac = cmax * max_row_abs_sum<tab::Leg_OT>();
+}
+
+// Rare inline fallback of sout_bt (fix list full): exact c4 from h, then T4 / e4 of the unit written
+// to ot / oe; returns (cropped max, first-half max).  Out of line so the fast path keeps its registers.
+template <typename HT>
+__device__ __noinline__ float2 exact_t4_unit(const HT* __restrict__ h, const Geo& g, const Bits& b, const Acc* ga,
+                                             const PlanF64* __restrict__ pf, int t, int k, int ty, int tx, float* ot,
+                                             int ostride, float* oe) {
+  int c4[6][6];
+  exact_c4_from_h<HT>(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + (uint32_t)k, ga, b, pf, c4);
+  float K4[6][6];
+#pragma unroll
+  for (int e = 0; e < 36; ++e) K4[e / 6][e % 6] = (float)c4[e / 6][e % 6];
+  float m, tm, efac;
+  t4_of_unit(K4, ty, tx, g, ot, ostride, efac, m, tm);
+  *oe = efac;
+  return make_float2(m, tm);
+}
+
+template <int LD, int EB>
+struct StagedT4 {
+  static_assert(LD <= 256, "staged path handles up to 256 padded channels");
+  static constexpr int TPB = 256 / LD;
+  static constexpr int THREADS = TPB * LD;
+  static constexpr int TILE_BYTES = 36 * LD * EB;
+  static constexpr int STAGE_BYTES = TPB * TILE_BYTES;
+  static constexpr int T4_TILE = 16 * LD * 4;
+  static constexpr int E_TILE = LD * 4;
+  static constexpr int OUT_BYTES = TPB * (T4_TILE + E_TILE);
+  static constexpr int SMEM = 2 * STAGE_BYTES + 2 * OUT_BYTES + 16;
+};
+
+// Legendre output_base_change codes (kept in registers) -> T4 / e4 stored, output max recorded.
+template <typename HT, int LD>
+__global__ void __launch_bounds__(StagedT4<LD, sizeof(HT)>::THREADS, WL_MINB)
+    sout_bt_kernel(const HT* __restrict__ h, float* __restrict__ t4, float* __restrict__ e4, Geo g, Bits b,
+                   Acc* __restrict__ acc, const PlanF64* __restrict__ pf, Tables tabs, FixList fl) {
+  using S = StagedT4<LD, sizeof(HT)>;
+  extern __shared__ __align__(128) uint8_t wl_stage_smem[];
+  uint8_t* sm = wl_stage_smem;
+  uint8_t* osm = sm + 2 * S::STAGE_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(osm + 2 * S::OUT_BYTES);
+  const int niter = (g.T + S::TPB - 1) / S::TPB;
+  const int tl = threadIdx.x / LD, k = threadIdx.x % LD;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int it, int s) {
+    const int t0 = it * S::TPB;
+    const int nt = min(S::TPB, g.T - t0);
+    mbar_arrive_expect_tx(&bar[s], (uint32_t)(nt * S::TILE_BYTES));
+    bulk_g2s(sm + s * S::STAGE_BYTES, reinterpret_cast<const uint8_t*>(h) + (size_t)t0 * S::TILE_BYTES,
+             (uint32_t)(nt * S::TILE_BYTES), &bar[s]);
+  };
+  if (threadIdx.x == 0 && (int)blockIdx.x < niter) issue(blockIdx.x, 0);
+  int kk = 0;
+  for (int it = blockIdx.x; it < niter; it += gridDim.x, ++kk) {
+    const int s = kk & 1;
+    if (threadIdx.x == 0 && it + (int)gridDim.x < niter) issue(it + gridDim.x, s ^ 1);
+    mbar_wait(&bar[s], (uint32_t)((kk >> 1) & 1));
+    const int t = it * S::TPB + tl;
+    const bool active = t < g.T && k < g.K;
+    const int tt = active ? t : 0;
+    const int n = (int)g.fTP.div((unsigned)tt), tile = (int)g.fTP.mod((unsigned)tt), grp = (int)g.fipg.div((unsigned)n);
+    const Acc* ga = acc + (size_t)grp * ST_COUNT;
+    const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr, ef = ga[ST_OBC].ef;
+    const uint8_t* st = sm + s * S::STAGE_BYTES + tl * S::TILE_BYTES;
+    float* ot = reinterpret_cast<float*>(osm + s * S::OUT_BYTES) + tl * 16 * LD + k;
+    float* oe = reinterpret_cast<float*>(osm + s * S::OUT_BYTES + S::TPB * S::T4_TILE) + tl * LD + k;
+    float K4[6][6];
+    bool deferred = false, inline_fix = false;
+    {
+      float X[6][6];
+      stage_x<LD, HT>(st, k, X);
+      float dmax = 0.f;
+      sandwich_cols<tab::Leg_OBC>(X, [&](int j, const float (&col)[6], float cm) {
+        float dcol = 0.f;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) rq_col(col[i], r, K4[i][j], dcol);
+        dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<tab::Leg_OBC>(), dcol));
+      });
+      const bool want = dmax > thr && active;
+      deferred = defer_fix(fl, FIX_OBC, (unsigned)tt * (unsigned)g.K + (unsigned)k, want);
+      inline_fix = want && !deferred;
+    }
+    const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
+    float m, tm, efac;
+    if (inline_fix) {
+      const float2 mm = exact_t4_unit<HT>(h, g, b, ga, pf, tt, k, ty, tx, ot, LD, oe);
+      m = mm.x, tm = mm.y;
+    } else {
+      t4_of_unit(K4, ty, tx, g, ot, LD, efac, m, tm);
+      *oe = efac;
+    }
+    if (deferred) m = tm = 0.f;  // recorded by fixup_obct_kernel from the exact codes
+    record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], tt, k, g.K);
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) bulk_wait_read<0>();  // the store issued last iteration has read buffer s^1
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int t0 = it * S::TPB, nt = min(S::TPB, g.T - t0);
+      bulk_s2g(t4 + (size_t)t0 * 16 * LD, osm + s * S::OUT_BYTES, (uint32_t)(nt * S::T4_TILE));
+      bulk_s2g(e4 + (size_t)t0 * LD, osm + s * S::OUT_BYTES + S::TPB * S::T4_TILE, (uint32_t)(nt * S::E_TILE));
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all<0>();
+}
+
+// Deferred output_base_change units: exact c4 from h, T4 / e4 rewritten, output max recorded.
+template <typename HT>
+__global__ void __launch_bounds__(128) fixup_obct_kernel(FixList fl, const HT* __restrict__ h, float* __restrict__ t4,
+                                                         float* __restrict__ e4, const __grid_constant__ Geo g,
+                                                         const __grid_constant__ Bits b, Acc* __restrict__ acc,
+                                                         const PlanF64* __restrict__ pf, Tables tabs) {
+  const unsigned cnt = fix_count(fl, FIX_OBC);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const unsigned u = fl.items[i];
+    const int t = (int)g.fK.div(u), k = (int)g.fK.mod(u);
+    const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
+    const Acc* ga = acc + (size_t)grp * ST_COUNT;
+    int c4[6][6];
+    exact_c4_from_h<HT>(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + (uint32_t)k, ga, b, pf, c4);
+    float K4[6][6];
+#pragma unroll
+    for (int e = 0; e < 36; ++e) K4[e / 6][e % 6] = (float)c4[e / 6][e % 6];
+    const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
+    float m, tm, efac;
+    t4_of_unit(K4, ty, tx, g, t4 + (size_t)t * 16 * g.Kp + k, g.Kp, efac, m, tm);
+    e4[(size_t)t * g.Kp + k] = efac;
+    record_unit_single(m, tm, grp, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K);
+  }
+}
+
+// Final output pass from T4 / e4 (Legendre, fp32 output).  Work item = 8 tiles x 32 channels: TMA
+// boxes {32, 16, 8} of T4 and {32, 1, 8} of e4; warp = tile, lane = channel; outputs staged and
+// stored as in sout_c_kernel.
+template <typename HT, bool TAB>
+__global__ void __launch_bounds__(StagedOut::THREADS, 4)
+    sout_ct_kernel(const __grid_constant__ CUtensorMap t4map, const __grid_constant__ CUtensorMap e4map,
+                   const HT* __restrict__ h, float* __restrict__ y, const float* __restrict__ bias,
+                   const __grid_constant__ Geo g, const __grid_constant__ Bits b, const Acc* __restrict__ acc,
+                   const PlanF64* __restrict__ pf, const float* __restrict__ otab, FixList fl) {
+  using S = StagedOut;
+  constexpr int T4B = S::TPB * 16 * S::KB * 4, EB = S::TPB * S::KB * 4, IN_BYTES = T4B + EB;
+  extern __shared__ __align__(128) uint8_t wl_stage_smem[];
+  uint8_t* sm = wl_stage_smem;
+  float* so = reinterpret_cast<float*>(sm + 2 * IN_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 2 * IN_BYTES + S::OUT_BYTES);
+  __shared__ long long ybase[S::TPB];
+  __shared__ int yrows[S::TPB];
+  const int nkb = (g.K + S::KB - 1) / S::KB;
+  const int niter = ((g.T + S::TPB - 1) / S::TPB) * nkb;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qo = b.q[ST_OUT];
+  const long long plane = (long long)g.Ho * g.Wo;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&t4map);
+    tma_prefetch_desc(&e4map);
+  }
+  __syncthreads();
+  auto issue = [&](int it, int s) {
+    const int tg = it / nkb, kb = it - tg * nkb;
+    mbar_arrive_expect_tx(&bar[s], (uint32_t)IN_BYTES);
+    tma_load_3d(sm + s * IN_BYTES, &t4map, &bar[s], kb * S::KB, 0, tg * S::TPB);
+    tma_load_3d(sm + s * IN_BYTES + T4B, &e4map, &bar[s], kb * S::KB, 0, tg * S::TPB);
+  };
+  if (threadIdx.x == 0 && (int)blockIdx.x < niter) issue(blockIdx.x, 0);
+  int kk = 0;
+  for (int it = blockIdx.x; it < niter; it += gridDim.x, ++kk) {
+    const int s = kk & 1;
+    if (threadIdx.x == 0 && it + (int)gridDim.x < niter) issue(it + gridDim.x, s ^ 1);
+    const int tg = it / nkb, kb = it - tg * nkb;
+    const int t0 = tg * S::TPB, k0 = kb * S::KB;
+    if (threadIdx.x < S::TPB) {
+      const int t = t0 + threadIdx.x;
+      long long base = -1;
+      int rows = 0;
+      if (t < g.T) {
+        const int n = (int)g.fTP.div((unsigned)t), tile = t - n * g.TP;
+        const int ty = (int)g.ftw.div((unsigned)tile), tx = tile - ty * g.tw;
+        base = ((long long)n * g.K + k0) * plane + (long long)(4 * ty) * g.Wo + 4 * tx;
+        rows = min(4, g.Ho - 4 * ty);
+      }
+      ybase[threadIdx.x] = base;
+      yrows[threadIdx.x] = rows;
+    }
+    mbar_wait(&bar[s], (uint32_t)((kk >> 1) & 1));
+    {
+      const int t = t0 + w, k = k0 + lane;
+      const bool active = t < g.T && k < g.K;
+      const int tt = active ? t : 0;
+      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)tt));
+      const Acc* ga = acc + (size_t)grp * ST_COUNT;
+      const float r = active ? ga[ST_OUT].r : 0.f, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
+      const float* tabg = TAB ? otab + (size_t)grp * (2 * qo + 1) + qo : nullptr;
+      const double scale = ga[ST_OUT].scale;
+      const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
+      auto deqf = [=](int code) -> float {
+        if constexpr (TAB)
+          return __ldg(tabg + code);
+        else
+          return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+      };
+      const float bk = (bias && active) ? __ldg(&bias[k]) : 0.f;
+      const float* p = reinterpret_cast<const float*>(sm + s * IN_BYTES) + w * 16 * S::KB + lane;
+      const float efac = reinterpret_cast<const float*>(sm + s * IN_BYTES + T4B)[w * S::KB + lane];
+      float* o = so + lane * S::OK + w * S::OT;
+      float dmax = 0.f, kd;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) o[e] = deqf(rq_col(active ? p[e * S::KB] : 0.f, r, kd, dmax)) + bk;
+      const bool want = fmaf(ef, efac, dmax) > thr && active;
+      if (__any_sync(0xffffffffu, want) && want &&
+          !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want))
+        exact_out_to<HT>(h, g, b, acc, pf, t, k, o, tabg, bk);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rep = 0; rep < (S::KB * 4 * S::TPB) / S::THREADS; ++rep) {
+      const int q = rep * S::THREADS + threadIdx.x;
+      const int tq = q & (S::TPB - 1), i = (q / S::TPB) & 3, kq = q / (4 * S::TPB);
+      const long long base = ybase[tq];
+      if (base < 0 || k0 + kq >= g.K || i >= yrows[tq]) continue;
+      const float4 v = *reinterpret_cast<const float4*>(so + kq * S::OK + tq * S::OT + 4 * i);
+      float* row = y + base + kq * plane + (long long)i * g.Wo;
+      if ((g.Wo & 3) == 0) {
+        __stcs(reinterpret_cast<float4*>(row), v);
+      } else {
+        const int cols = g.Wo - (int)((base % g.Wo));
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < cols) row[j] = vv[j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Deferred final-output units of the T4 path: exact from h, written to y.
+template <typename HT>
+__global__ void __launch_bounds__(128) fixup_outt_kernel(FixList fl, const HT* __restrict__ h, float* __restrict__ y,
+                                                         const float* __restrict__ bias, const __grid_constant__ Geo g,
+                                                         const __grid_constant__ Bits b, const Acc* __restrict__ acc,
+                                                         const PlanF64* __restrict__ pf) {
+  const unsigned cnt = fix_count(fl, FIX_OUT);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const unsigned u = fl.items[i];
+    const int t = (int)g.fK.div(u), k = (int)g.fK.mod(u);
+    const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
+    const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
+    const Acc* ga = acc + (size_t)grp * ST_COUNT;
+    const int qo = b.q[ST_OUT];
+    const double scale = ga[ST_OUT].scale;
+    const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
+    const float bk = bias ? bias[k] : 0.f;
+    exact_out_from_h<HT>(h, g, b, acc, pf, t, k, [&](int ii, int jj, int code) {
+      const int rr = 4 * ty + ii, cc = 4 * tx + jj;
+      if (rr < g.Ho && cc < g.Wo) {
+        const float v = code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+        y[(((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + cc] = v + bk;
+      }
+    });
+  }
+}
+
 }  // namespace wl

@@ -56,7 +56,7 @@ inline bool make_tmap_i8_4d(CUtensorMap* map, const void* base, uint64_t d0, uin
   return r == CUDA_SUCCESS;
 }
 
-// 3-D tensor [d2][d1][d0] of 1- or 2-byte elements (d0 contiguous), box {b0, b1, b2}, no swizzle,
+// 3-D tensor [d2][d1][d0] of 1-, 2- or 4-byte elements (d0 contiguous), box {b0, b1, b2}, no swizzle,
 // out-of-bounds boxes zero-filled (the smem box is dense [b2][b1][b0]).
 inline bool make_tmap_3d_plain(CUtensorMap* map, const void* base, int elem_bytes, uint64_t d0, uint64_t d1,
                                uint64_t d2, uint32_t b0, uint32_t b1, uint32_t b2) {
@@ -66,7 +66,10 @@ inline bool make_tmap_3d_plain(CUtensorMap* map, const void* base, int elem_byte
   cuuint64_t strides[2] = {d0 * elem_bytes, d0 * d1 * elem_bytes};
   cuuint32_t box[3] = {b0, b1, b2};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 3,
+  const CUtensorMapDataType dt = elem_bytes == 4   ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                 : elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                                   : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  CUresult r = enc(map, dt, 3,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
