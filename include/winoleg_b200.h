@@ -94,6 +94,14 @@ int wl_backward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const 
                 const void* fwd_workspace, float* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
                 void* stream);
 
+/* Float (unquantized) Winograd correlation in fp32 — the reference's conv2d_winograd(x, w, plan,
+ * mode) (pipeline.py:161-164: run_pipeline with the identity cast), with the same batch, padding,
+ * crop and bias conventions as wl_forward.  w is [c_out][c_in][3][3] fp32 (no cache: the weight
+ * transform runs every call).  Accuracy: fp32 arithmetic (tolerance stated in tests/test_gpu_float.py). */
+int wl_float_workspace_size(const wl_plan* plan, const wl_shape* s, size_t* bytes);
+int wl_forward_float(const wl_plan* plan, const wl_shape* s, const float* x, const float* w, const float* bias, float* y,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
 /* Per-group StageStat rows [n/images_per_group][nstages] after wl_forward (synchronises stream). */
 int wl_num_stages(const wl_plan* plan);
 int wl_read_stats(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, const void* cache,

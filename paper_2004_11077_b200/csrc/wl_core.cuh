@@ -19,6 +19,10 @@ enum StageId { ST_INPUT = 0, ST_WEIGHTS, ST_WT, ST_WBC, ST_IBC, ST_IT, ST_HAD, S
 
 // Per (group, stage) reduction slot: M = max |T| (integer stages) or fp32 bits of max |x| (input /
 // weights); F = fp64 bits of the reference's max_abs (positive doubles order like uint64).
+struct PlanF64 {  // fp64 left matrices (nearest doubles of the exact rationals, construct.py:191-208)
+  double wt[6 * 3], wbc[36], ibc[36], it[36], obc[36], ot[4 * 6];
+};
+
 struct Acc {
   unsigned long long M;   // exact integer max |T| (fp64 bits of max|x| for input / weights)
   unsigned long long F;   // fp64 bits of the reference max_abs

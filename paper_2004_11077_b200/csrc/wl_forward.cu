@@ -17,6 +17,7 @@
 #include "../../include/winoleg_b200.h"
 #include "gemm_i8.cuh"
 #include "wl_backward.h"
+#include "wl_float.h"
 #include "wl_kernels2.cuh"
 #include "wl_staged.cuh"
 #include "wl_tmap.h"
@@ -691,6 +692,42 @@ int wl_plan_destroy(wl_plan* plan) {
 }
 
 int wl_plan_mode(const wl_plan* plan) { return plan ? plan->mode : WL_ERR_ARG; }
+
+// ------------------------------------------------------------------ float (unquantized) path
+static int float_geo(const wl_shape* s, FGeo* g) {
+  if (!s) return fail(WL_ERR_ARG, "shape is NULL");
+  if (s->n < 1 || s->c_in < 1 || s->c_out < 1 || s->pad < 0)
+    return fail(WL_ERR_ARG, "bad shape n=%d c_in=%d c_out=%d pad=%d", s->n, s->c_in, s->c_out, s->pad);
+  const int Hp = s->h + 2 * s->pad, Wp = s->w + 2 * s->pad;
+  if (Hp < 3 || Wp < 3) return fail(WL_ERR_ARG, "input %dx%d is smaller than the 3x3 kernel", Hp, Wp);
+  g->N = s->n, g->C = s->c_in, g->K = s->c_out, g->H = s->h, g->W = s->w, g->pad = s->pad;
+  g->Ho = Hp - 2, g->Wo = Wp - 2, g->th = (g->Ho + 3) / 4, g->tw = (g->Wo + 3) / 4, g->TP = g->th * g->tw;
+  g->T = g->N * g->TP;
+  if ((unsigned long long)36 * g->T * std::max(g->C, g->K) >= (1ULL << 31))
+    return fail(WL_ERR_ARG, "problem too large for one float call (split the batch)");
+  return WL_OK;
+}
+
+int wl_float_workspace_size(const wl_plan* plan, const wl_shape* s, size_t* bytes) {
+  if (!plan || !bytes) return fail(WL_ERR_ARG, "NULL argument");
+  FGeo g;
+  if (int rc = float_geo(s, &g)) return rc;
+  *bytes = wl_float_workspace_bytes(g);
+  return WL_OK;
+}
+
+int wl_forward_float(const wl_plan* plan, const wl_shape* s, const float* x, const float* w, const float* bias, float* y,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (!plan || !x || !w || !y || !workspace) return fail(WL_ERR_ARG, "NULL argument");
+  FGeo g;
+  if (int rc = float_geo(s, &g)) return rc;
+  if (workspace_bytes < wl_float_workspace_bytes(g))
+    return fail(WL_ERR_WORKSPACE, "workspace needs %zu bytes", wl_float_workspace_bytes(g));
+  std::string err;
+  if (wl_float_run(plan->mode == WL_LEGENDRE, plan->d_pf, g, x, w, bias, y, workspace, (cudaStream_t)stream, &err))
+    return fail(WL_ERR_CUDA, "float path: %s", err.c_str());
+  return WL_OK;
+}
 
 int wl_num_stages(const wl_plan* plan) { return plan ? (plan->mode == WL_LEGENDRE ? 9 : 6) : WL_ERR_ARG; }
 

@@ -39,9 +39,6 @@ struct Bits {
   int q[ST_COUNT];  // qmax per stage id
 };
 
-struct PlanF64 {  // fp64 left matrices (nearest doubles of the exact rationals, construct.py:191-208)
-  double wt[6 * 3], wbc[36], ibc[36], it[36], obc[36], ot[4 * 6];
-};
 
 __device__ __forceinline__ int group_of_image(int n, const Geo& g) { return (int)g.fipg.div((unsigned)n); }
 

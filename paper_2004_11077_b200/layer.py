@@ -422,5 +422,48 @@ def conv2d_winograd_quantized(x, w, plan: WinogradPlan, mode: str, qconfig: Quan
     return y, stats
 
 
+def conv2d_winograd(x, w, plan: WinogradPlan, mode: str = "canonical", padding: int = 0, bias=None):
+    """Float (unquantized) Winograd correlation on the GPU in fp32: the reference's
+    ``conv2d_winograd`` (pipeline.py:161-164, run_pipeline with the identity cast), SURVEY §8f row 2.
+
+    x: [c_in, H, W] or [N, c_in, H, W]; w: [c_out, c_in, 3, 3]; CUDA tensors or numpy arrays
+    (numpy in -> numpy out, like the reference; computed in fp32 either way).  Zero padding and bias
+    follow ``conv2d_winograd_quantized``."""
+    _require_mode(plan, mode)
+    as_numpy = isinstance(x, np.ndarray) or isinstance(w, np.ndarray)
+    dev = torch.device("cuda", torch.cuda.current_device()) if as_numpy else x.device
+    x = torch.as_tensor(np.asarray(x) if as_numpy else x, device=dev).float().contiguous()
+    w = torch.as_tensor(np.asarray(w) if as_numpy else w, device=dev).float().contiguous()
+    single = x.dim() == 3
+    if single:
+        x = x.unsqueeze(0)
+    _check_conv_args(x, w)
+    if w.shape[2] != 3:
+        raise DimensionError(f"plan is for k=3, weights have k={w.shape[2]}")
+    n, cin, h, wd = (int(v) for v in x.shape)
+    cout = int(w.shape[0])
+    shape = _lib.wl_shape(n, cin, cout, h, wd, int(padding), 1)
+    ho, wo = h + 2 * padding - 2, wd + 2 * padding - 2
+    if ho < 1 or wo < 1:
+        raise DimensionError(f"input {h}x{wd} (pad {padding}) is smaller than the 3x3 kernel")
+    if bias is not None:
+        bias = torch.as_tensor(np.asarray(bias) if isinstance(bias, np.ndarray) else bias, device=dev).float().contiguous()
+        if bias.shape != (cout,):
+            raise DimensionError(f"bias must be [{cout}], got {tuple(bias.shape)}")
+    dplan = DevicePlan.get(plan, mode, dev)
+    nbytes = ctypes.c_size_t()
+    _lib.check(_lib.lib().wl_float_workspace_size(dplan.handle, ctypes.byref(shape), ctypes.byref(nbytes)),
+               "wl_float_workspace_size")
+    ws = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    y = torch.empty((n, cout, ho, wo), dtype=torch.float32, device=dev)
+    _lib.check(_lib.lib().wl_forward_float(
+        dplan.handle, ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+        ctypes.c_void_p(bias.data_ptr() if bias is not None else 0), ctypes.c_void_p(y.data_ptr()),
+        ctypes.c_void_p(ws.data_ptr()), nbytes.value, _stream_ptr()), "wl_forward_float")
+    if single:
+        y = y[0]
+    return y.cpu().numpy() if as_numpy else y
+
+
 def default_plan(use_legendre: bool = True) -> WinogradPlan:
     return build_plan(4, 3, use_legendre=use_legendre)

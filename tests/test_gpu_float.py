@@ -1,0 +1,60 @@
+"""GPU: the fp32 float (unquantized) Winograd path, §8f row 2 — the reference's conv2d_winograd
+(pipeline.py:161-164) — against the reference's fp64 outputs (golden) and the fp64 oracle.
+
+Tolerance (fp32 arithmetic, stated): max |y_gpu - y_ref| <= 2e-5 * max(1, max |y_ref|) per image,
+for both bases; the fp64 reference itself agrees with direct correlation to 1e-10."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2004_11077_b200 as W
+from oracle import float_ref as F
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "float_cases.npz")
+TOL = 2e-5
+
+
+def _err(got, ref):
+    return float(np.max(np.abs(got.astype(np.float64) - ref)) / max(1.0, float(np.max(np.abs(ref)))))
+
+
+@pytest.mark.parametrize("mode", ["canonical", "legendre"])
+def test_float_winograd_vs_reference_golden(mode):
+    z = np.load(GOLD, allow_pickle=False)
+    plan = W.build_plan(4, 3, use_legendre=True)
+    for m in json.loads(str(z["meta"])):
+        n, pad = m["name"], m["pad"]
+        y = W.conv2d_winograd(z[f"{n}_x"], z[f"{n}_w"], plan, mode, padding=pad)
+        ref = z[f"{n}_wino_{mode}"]
+        assert y.shape == ref.shape
+        e = _err(y, ref)
+        print(f"{n} {mode}: rel err {e:.3e}")
+        assert e <= TOL, (n, e)
+
+
+def test_float_winograd_batched_padding_bias():
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((4, 24, 13, 18)).astype(np.float32)
+    w = (rng.standard_normal((20, 24, 3, 3)) * np.sqrt(2 / 216)).astype(np.float32)
+    b = rng.standard_normal(20).astype(np.float32)
+    plan = W.build_plan(4, 3, use_legendre=True)
+    for mode in ("canonical", "legendre"):
+        y = W.conv2d_winograd(torch.as_tensor(x, device="cuda"), torch.as_tensor(w, device="cuda"), plan, mode,
+                              padding=1, bias=torch.as_tensor(b, device="cuda")).cpu().numpy()
+        assert y.shape == (4, 20, 13, 18)
+        for i in range(4):
+            ref = F.winograd_float(np.pad(x[i].astype(np.float64), ((0, 0), (1, 1), (1, 1))), w, mode) + b[:, None, None]
+            assert _err(y[i], ref) <= TOL
+
+
+def test_float_winograd_errors():
+    with pytest.raises(W.DimensionError):
+        W.conv2d_winograd(np.zeros((2, 2, 2), np.float32), np.zeros((1, 2, 3, 3), np.float32),
+                          W.build_plan(4, 3, use_legendre=True), "canonical")
+    with pytest.raises(ValueError):
+        W.conv2d_winograd(np.zeros((2, 6, 6), np.float32), np.zeros((1, 2, 3, 3), np.float32),
+                          W.build_plan(4, 3, use_legendre=True), "chebyshev")
