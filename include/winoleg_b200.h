@@ -102,6 +102,18 @@ int wl_float_workspace_size(const wl_plan* plan, const wl_shape* s, size_t* byte
 int wl_forward_float(const wl_plan* plan, const wl_shape* s, const float* x, const float* w, const float* bias, float* y,
                      void* workspace, size_t workspace_bytes, void* stream);
 
+/* Quantized direct-convolution baseline — the reference's conv2d_direct_quantized(x, w, qconfig)
+ * (quantize.py:151-160): fake-quantise x per scale group at input_bits and w at weight_bits, fp64
+ * direct correlation in the reference's order (_kernels.py:53-66), fake-quantise the result per
+ * group at output_transform_bits.  Computed in fp64 exactly as the reference does, so the f64 entry
+ * point is bit-identical to the reference and the fp32 one is that result rounded to fp32.  x is
+ * [n][c_in][h][w] with zero padding `pad`, w [c_out][c_in][3][3], y [n][c_out][h+2pad-2][w+2pad-2];
+ * only input_bits, weight_bits and output_transform_bits of q are used (each in [2, 53]). */
+int wl_direct_workspace_size(const wl_shape* s, size_t* bytes);
+int wl_direct_quantized(const wl_qcfg* q, const wl_shape* s, const float* x, const float* w, float* y,
+                        void* workspace, size_t workspace_bytes, void* stream);
+int wl_direct_quantized_f64(const wl_qcfg* q, const wl_shape* s, const double* x, const double* w, double* y,
+                            void* workspace, size_t workspace_bytes, void* stream);
 /* Per-group StageStat rows [n/images_per_group][nstages] after wl_forward (synchronises stream). */
 int wl_num_stages(const wl_plan* plan);
 int wl_read_stats(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, const void* cache,

@@ -17,6 +17,7 @@
 #include "../../include/winoleg_b200.h"
 #include "gemm_i8.cuh"
 #include "wl_backward.h"
+#include "wl_direct.h"
 #include "wl_float.h"
 #include "wl_kernels2.cuh"
 #include "wl_staged.cuh"
@@ -727,6 +728,65 @@ int wl_forward_float(const wl_plan* plan, const wl_shape* s, const float* x, con
   if (wl_float_run(plan->mode == WL_LEGENDRE, plan->d_pf, g, x, w, bias, y, workspace, (cudaStream_t)stream, &err))
     return fail(WL_ERR_CUDA, "float path: %s", err.c_str());
   return WL_OK;
+}
+
+static int direct_geo(const wl_shape* s, DGeo* g) {
+  if (!s) return fail(WL_ERR_ARG, "shape is NULL");
+  if (s->n < 1 || s->c_in < 1 || s->c_out < 1 || s->pad < 0 || s->images_per_group < 1 ||
+      s->n % s->images_per_group != 0)
+    return fail(WL_ERR_ARG, "bad shape n=%d c_in=%d c_out=%d pad=%d images_per_group=%d", s->n, s->c_in, s->c_out,
+                s->pad, s->images_per_group);
+  const int Hp = s->h + 2 * s->pad, Wp = s->w + 2 * s->pad;
+  if (Hp < 3 || Wp < 3) return fail(WL_ERR_ARG, "input %dx%d is smaller than the 3x3 kernel", Hp, Wp);
+  g->N = s->n, g->C = s->c_in, g->K = s->c_out, g->H = s->h, g->W = s->w, g->pad = s->pad;
+  g->Ho = Hp - 2, g->Wo = Wp - 2, g->ipg = s->images_per_group;
+  return WL_OK;
+}
+
+static int direct_bits(const wl_qcfg* q) {
+  if (!q) return fail(WL_ERR_ARG, "qconfig is NULL");
+  if (q->input_bits < 2 || q->input_bits > 53 || q->weight_bits < 2 || q->weight_bits > 53 ||
+      q->output_transform_bits < 2 || q->output_transform_bits > 53)
+    return fail(WL_ERR_BITS, "direct baseline widths must be in [2, 53]");
+  return WL_OK;
+}
+
+int wl_direct_workspace_size(const wl_shape* s, size_t* bytes) {
+  if (!bytes) return fail(WL_ERR_ARG, "NULL argument");
+  DGeo g;
+  if (int rc = direct_geo(s, &g)) return rc;
+  *bytes = wl_direct_workspace_bytes(g);
+  return WL_OK;
+}
+
+}  // extern "C"
+
+template <typename T>
+static int direct_impl(const wl_qcfg* q, const wl_shape* s, const T* x, const T* w, T* y, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (!x || !w || !y || !workspace) return fail(WL_ERR_ARG, "NULL argument");
+  DGeo g;
+  if (int rc = direct_geo(s, &g)) return rc;
+  if (int rc = direct_bits(q)) return rc;
+  if (workspace_bytes < wl_direct_workspace_bytes(g))
+    return fail(WL_ERR_WORKSPACE, "workspace needs %zu bytes", wl_direct_workspace_bytes(g));
+  std::string err;
+  if (wl_direct_run<T>(g, q->input_bits, q->weight_bits, q->output_transform_bits, x, w, y, workspace,
+                       (cudaStream_t)stream, &err))
+    return fail(WL_ERR_CUDA, "direct baseline: %s", err.c_str());
+  return WL_OK;
+}
+
+extern "C" {
+
+int wl_direct_quantized(const wl_qcfg* q, const wl_shape* s, const float* x, const float* w, float* y,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  return direct_impl<float>(q, s, x, w, y, workspace, workspace_bytes, stream);
+}
+
+int wl_direct_quantized_f64(const wl_qcfg* q, const wl_shape* s, const double* x, const double* w, double* y,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+  return direct_impl<double>(q, s, x, w, y, workspace, workspace_bytes, stream);
 }
 
 int wl_num_stages(const wl_plan* plan) { return plan ? (plan->mode == WL_LEGENDRE ? 9 : 6) : WL_ERR_ARG; }

@@ -465,5 +465,52 @@ def conv2d_winograd(x, w, plan: WinogradPlan, mode: str = "canonical", padding: 
     return y.cpu().numpy() if as_numpy else y
 
 
+def conv2d_direct_quantized(x, w, qconfig: QuantConfig | None = None, padding: int = 0,
+                            scale_groups: str = "image"):
+    """Quantized direct-convolution baseline on the GPU: the reference's ``conv2d_direct_quantized``
+    (quantize.py:151-160), SURVEY §8f row 3 — fake-quantise x (input_bits) and w (weight_bits),
+    correlate in fp64 in the reference's order, fake-quantise the result (output_transform_bits).
+
+    fp64 operands (and numpy arrays, copied to fp64 like the reference) run ``wl_direct_quantized_f64``
+    and return the reference's output bit for bit; fp32 CUDA tensors run ``wl_direct_quantized`` (the
+    same fp64 computation, result rounded to fp32).  Shapes, padding and ``scale_groups`` follow
+    ``conv2d_winograd_quantized``."""
+    if qconfig is None:
+        qconfig = QuantConfig()
+    if scale_groups not in ("image", "batch"):
+        raise ValueError(f"scale_groups must be 'image' or 'batch', got {scale_groups!r}")
+    as_numpy = isinstance(x, np.ndarray) or isinstance(w, np.ndarray)
+    if as_numpy:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        x = torch.as_tensor(np.asarray(x, dtype=np.float64), device=dev)
+        w = torch.as_tensor(np.asarray(w, dtype=np.float64), device=dev)
+    single = x.dim() == 3
+    if single:
+        x = x.unsqueeze(0)
+    _check_conv_args(x, w)
+    if w.shape[2] != 3:
+        raise DimensionError(f"the direct baseline is 3x3, weights have k={w.shape[2]}")
+    f64 = x.dtype == torch.float64 or w.dtype == torch.float64
+    dt = torch.float64 if f64 else torch.float32
+    x, w = x.to(dt).contiguous(), w.to(dt).contiguous()
+    n, cin, h, wd = (int(v) for v in x.shape)
+    cout = int(w.shape[0])
+    ho, wo = h + 2 * padding - 2, wd + 2 * padding - 2
+    if padding < 0 or ho < 1 or wo < 1:
+        raise DimensionError(f"input {h}x{wd} (pad {padding}) is smaller than the 3x3 kernel")
+    shape = _lib.wl_shape(n, cin, cout, h, wd, int(padding), 1 if scale_groups == "image" else n)
+    nbytes = ctypes.c_size_t()
+    _lib.check(_lib.lib().wl_direct_workspace_size(ctypes.byref(shape), ctypes.byref(nbytes)), "wl_direct_workspace_size")
+    ws = torch.empty(nbytes.value, dtype=torch.uint8, device=x.device)
+    y = torch.empty((n, cout, ho, wo), dtype=dt, device=x.device)
+    fn = _lib.lib().wl_direct_quantized_f64 if f64 else _lib.lib().wl_direct_quantized
+    _lib.check(fn(ctypes.byref(qcfg_struct(qconfig)), ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()),
+                  ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                  nbytes.value, _stream_ptr()), "wl_direct_quantized")
+    if single:
+        y = y[0]
+    return y.cpu().numpy() if as_numpy else y
+
+
 def default_plan(use_legendre: bool = True) -> WinogradPlan:
     return build_plan(4, 3, use_legendre=use_legendre)
