@@ -112,6 +112,10 @@ int wl_forward_float(const wl_plan* plan, const wl_shape* s, const float* x, con
 int wl_direct_workspace_size(const wl_shape* s, size_t* bytes);
 int wl_direct_quantized(const wl_qcfg* q, const wl_shape* s, const float* x, const float* w, float* y,
                         void* workspace, size_t workspace_bytes, void* stream);
+/* The unquantized fp64 direct correlation, the reference's conv2d_direct (reference.py:34-39,
+ * _kernels.py:53-66), same shapes and padding; bit-identical to the reference (its operation order). */
+int wl_direct_f64(const wl_shape* s, const double* x, const double* w, double* y, void* workspace,
+                  size_t workspace_bytes, void* stream);
 int wl_direct_quantized_f64(const wl_qcfg* q, const wl_shape* s, const double* x, const double* w, double* y,
                             void* workspace, size_t workspace_bytes, void* stream);
 /* Per-group StageStat rows [n/images_per_group][nstages] after wl_forward (synchronises stream). */

@@ -6,7 +6,8 @@ hand-written CUDA kernels (csrc/, include/winoleg_b200.h) and a PyTorch-facing A
 """
 
 from .errors import CudaLayerError, DimensionError, InvalidPointsError
-from .layer import (BASE_MODES, QuantWinogradConv, WinogradAwareConv2d, conv2d_direct_quantized, conv2d_winograd,
+from .layer import (BASE_MODES, QuantWinogradConv, WinogradAwareConv2d, conv2d_direct, conv2d_direct_quantized,
+                    conv2d_winograd,
                     conv2d_winograd_quantized,
                     default_plan, winograd_conv2d)
 from .plan import (BaseChange, InterpolationPoints, Rational, WinogradPlan, build_base_change, build_plan,
@@ -16,7 +17,8 @@ from .quantize import STAGE_BITS, STAGE_ORDER, QuantConfig, QuantParams, StageSt
 __version__ = "0.1.0"
 
 __all__ = [
-    "BASE_MODES", "QuantWinogradConv", "WinogradAwareConv2d", "conv2d_direct_quantized", "conv2d_winograd",
+    "BASE_MODES", "QuantWinogradConv", "WinogradAwareConv2d", "conv2d_direct", "conv2d_direct_quantized",
+    "conv2d_winograd",
     "conv2d_winograd_quantized",
     "default_plan",
     "winograd_conv2d",

@@ -40,7 +40,7 @@ EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_mode", "wl_weight_cache
            "wl_weight_transform_f64", "wl_workspace_size", "wl_forward", "wl_forward_f64", "wl_num_stages", "wl_read_stats", "wl_debug_layout",
            "wl_forward_launches", "wl_profile_enable", "wl_profile_read", "wl_backward_workspace_size",
            "wl_backward", "wl_float_workspace_size", "wl_forward_float", "wl_direct_workspace_size",
-           "wl_direct_quantized", "wl_direct_quantized_f64", "wl_last_error")
+           "wl_direct_quantized", "wl_direct_quantized_f64", "wl_direct_f64", "wl_last_error")
 
 
 def lib():
@@ -72,6 +72,7 @@ def lib():
     L.wl_direct_workspace_size.argtypes = [P(wl_shape), P(S)]
     L.wl_direct_quantized.argtypes = [P(wl_qcfg), P(wl_shape), VP, VP, VP, VP, S, VP]
     L.wl_direct_quantized_f64.argtypes = [P(wl_qcfg), P(wl_shape), VP, VP, VP, VP, S, VP]
+    L.wl_direct_f64.argtypes = [P(wl_shape), VP, VP, VP, VP, S, VP]
     L.wl_profile_enable.argtypes = [I]
     L.wl_profile_read.argtypes = [P(ctypes.c_char_p), P(ctypes.c_double), I, P(I), P(I)]
     L.wl_last_error.restype = ctypes.c_char_p

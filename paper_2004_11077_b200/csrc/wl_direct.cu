@@ -48,9 +48,10 @@ __global__ void absmax_kernel(const T* __restrict__ x, long long total, long lon
 }
 
 // fake_quant (quantize.py:111-126): scale = M/qmax, codes = clip(rint(v/scale)), out = codes*scale,
-// codes == +-qmax snapped to +-M; M == 0 leaves the (all-zero) tensor unchanged.
+// codes == +-qmax snapped to +-M; M == 0 leaves the (all-zero) tensor unchanged (and, with no
+// absmax pass, makes the cast the identity: the unquantized conv2d_direct).
 __device__ __forceinline__ double fake_quant1(double v, double M, double qmax) {
-  if (M == 0.0) return v;
+  if (M == 0.0 || qmax == 0.0) return v;  // qmax 0: identity cast (width 0)
   const double scale = __ddiv_rn(M, qmax);
   double c = rint(__ddiv_rn(v, scale));
   c = fmin(fmax(c, -qmax), qmax);
@@ -143,12 +144,14 @@ int wl_direct_run(const DGeo& g, int in_bits, int w_bits, int out_bits, const T*
   const long long ny = (long long)g.N * g.K * g.Ho * g.Wo, per_y = (long long)g.ipg * g.K * g.Ho * g.Wo;
   const int tb = 256;
   cudaMemsetAsync(gx, 0, (size_t)(2 * groups + 1) * 8, st);
-  dq::absmax_kernel<T><<<grid_for(nx, tb), tb, 0, st>>>(x, nx, per_x, gx);
-  dq::absmax_kernel<T><<<grid_for(nw, tb), tb, 0, st>>>(w, nw, nw, gw);
-  dq::quant_kernel<T><<<grid_for(nx, tb), tb, 0, st>>>(x, xq, nx, per_x, gx, (double)((1 << (in_bits - 1)) - 1));
-  dq::quant_kernel<T><<<grid_for(nw, tb), tb, 0, st>>>(w, wq, nw, nw, gw, (double)((1 << (w_bits - 1)) - 1));
+  // width 0 = identity cast: the group maximum stays 0 and fake_quant1 passes the value through
+  auto qmax = [](int bits) { return bits > 0 ? (double)((1LL << (bits - 1)) - 1) : 0.0; };
+  if (in_bits > 0) dq::absmax_kernel<T><<<grid_for(nx, tb), tb, 0, st>>>(x, nx, per_x, gx);
+  if (w_bits > 0) dq::absmax_kernel<T><<<grid_for(nw, tb), tb, 0, st>>>(w, nw, nw, gw);
+  dq::quant_kernel<T><<<grid_for(nx, tb), tb, 0, st>>>(x, xq, nx, per_x, gx, qmax(in_bits));
+  dq::quant_kernel<T><<<grid_for(nw, tb), tb, 0, st>>>(w, wq, nw, nw, gw, qmax(w_bits));
   dq::direct_kernel<<<grid_for(ny, tb), tb, 0, st>>>(xq, wq, z, g, gz);
-  dq::out_kernel<T><<<grid_for(ny, tb), tb, 0, st>>>(z, y, ny, per_y, gz, (double)((1LL << (out_bits - 1)) - 1));
+  dq::out_kernel<T><<<grid_for(ny, tb), tb, 0, st>>>(z, y, ny, per_y, gz, qmax(out_bits));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);

@@ -784,6 +784,21 @@ int wl_direct_quantized(const wl_qcfg* q, const wl_shape* s, const float* x, con
   return direct_impl<float>(q, s, x, w, y, workspace, workspace_bytes, stream);
 }
 
+int wl_direct_f64(const wl_shape* s, const double* x, const double* w, double* y, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  const wl_qcfg none = {0, 0, 0, 0, 0, 0, 0};  // identity casts
+  if (!x || !w || !y || !workspace) return fail(WL_ERR_ARG, "NULL argument");
+  DGeo g;
+  if (int rc = direct_geo(s, &g)) return rc;
+  if (workspace_bytes < wl_direct_workspace_bytes(g))
+    return fail(WL_ERR_WORKSPACE, "workspace needs %zu bytes", wl_direct_workspace_bytes(g));
+  std::string err;
+  if (wl_direct_run<double>(g, none.input_bits, none.weight_bits, none.output_transform_bits, x, w, y, workspace,
+                            (cudaStream_t)stream, &err))
+    return fail(WL_ERR_CUDA, "direct correlation: %s", err.c_str());
+  return WL_OK;
+}
+
 int wl_direct_quantized_f64(const wl_qcfg* q, const wl_shape* s, const double* x, const double* w, double* y,
                             void* workspace, size_t workspace_bytes, void* stream) {
   return direct_impl<double>(q, s, x, w, y, workspace, workspace_bytes, stream);

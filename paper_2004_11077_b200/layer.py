@@ -512,5 +512,37 @@ def conv2d_direct_quantized(x, w, qconfig: QuantConfig | None = None, padding: i
     return y.cpu().numpy() if as_numpy else y
 
 
+def conv2d_direct(x, w, padding: int = 0):
+    """fp64 direct correlation on the GPU: the reference's ``conv2d_direct`` (reference.py:34-39),
+    bit-identical to it (same operation order, _kernels.py:53-66).  The ground truth of the error
+    experiment.  x [c_in,H,W] or [N,c_in,H,W], w [c_out,c_in,3,3]; numpy in -> numpy out."""
+    as_numpy = isinstance(x, np.ndarray) or isinstance(w, np.ndarray)
+    dev = torch.device("cuda", torch.cuda.current_device()) if as_numpy else x.device
+    x = torch.as_tensor(np.asarray(x, dtype=np.float64) if as_numpy else x, device=dev).double().contiguous()
+    w = torch.as_tensor(np.asarray(w, dtype=np.float64) if as_numpy else w, device=dev).double().contiguous()
+    single = x.dim() == 3
+    if single:
+        x = x.unsqueeze(0)
+    _check_conv_args(x, w)
+    if w.shape[2] != 3:
+        raise DimensionError(f"the GPU direct correlation is 3x3, weights have k={w.shape[2]}")
+    n, cin, h, wd = (int(v) for v in x.shape)
+    cout = int(w.shape[0])
+    ho, wo = h + 2 * padding - 2, wd + 2 * padding - 2
+    if padding < 0 or ho < 1 or wo < 1:
+        raise DimensionError(f"input {h}x{wd} (pad {padding}) is smaller than the 3x3 kernel")
+    shape = _lib.wl_shape(n, cin, cout, h, wd, int(padding), 1)
+    nbytes = ctypes.c_size_t()
+    _lib.check(_lib.lib().wl_direct_workspace_size(ctypes.byref(shape), ctypes.byref(nbytes)), "wl_direct_workspace_size")
+    ws = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+    y = torch.empty((n, cout, ho, wo), dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().wl_direct_f64(ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                        ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()), nbytes.value,
+                                        _stream_ptr()), "wl_direct_f64")
+    if single:
+        y = y[0]
+    return y.cpu().numpy() if as_numpy else y
+
+
 def default_plan(use_legendre: bool = True) -> WinogradPlan:
     return build_plan(4, 3, use_legendre=use_legendre)

@@ -67,3 +67,12 @@ def test_direct_quantized_errors():
         W.conv2d_direct_quantized(np.zeros((2, 2, 2)), np.zeros((1, 2, 3, 3)))
     with pytest.raises(W.DimensionError):
         W.conv2d_direct_quantized(np.zeros((3, 6, 6)), np.zeros((1, 2, 3, 3)))
+
+
+def test_direct_f64_vs_reference_golden():
+    # the reference's conv2d_direct (reference.py:34-39), bit for bit, valid and padded
+    z = np.load(GOLD, allow_pickle=False)
+    for m in json.loads(str(z["meta"])):
+        n, pad = m["name"], m["pad"]
+        y = W.conv2d_direct(z[f"{n}_x"], z[f"{n}_w"], padding=pad)
+        assert np.array_equal(y, z[f"{n}_direct"]), n
