@@ -362,7 +362,8 @@ struct HadRqCtx {
   const Acc* wacc;
   const int8_t* U;
   const int8_t* V;
-  int C, Cp, grp, wstage, qmax_u, qmax_v, qmax_h, xi, row;
+  int C, Cp, Kp, grp, wstage, qmax_u, qmax_v, qmax_h, xi, row;
+  FixList fl;
 };
 template <typename HT>
 static __device__ __noinline__ uint4 had_rq_slow8(HadRqCtx cx, uint4 va, uint4 vb, int col, int n) {
@@ -373,7 +374,12 @@ static __device__ __noinline__ uint4 had_rq_slow8(HadRqCtx cx, uint4 va, uint4 v
   for (int j = 0; j < 8; ++j) {
     bool tie = false;
     int code = rq((long long)(int)v[j], q, tie);
-    if (tie && j < n) {
+    // exact ties are replayed in fp64 by fixup_had_kernel (one thread each, off the epilogue's
+    // critical path); only an overflowing list falls back to the inline replay
+    const bool want = tie && j < n;
+    const unsigned unit = ((unsigned)cx.row * 36u + (unsigned)cx.xi) * (unsigned)cx.Kp + (unsigned)(col + j);
+    if (defer_fix(cx.fl, FIX_HAD, unit, want)) {
+    } else if (want) {
       const StageQ qu = load_int_stage(cx.wacc[cx.wstage], cx.qmax_u);
       const StageQ qv = load_int_stage(cx.acc[(size_t)cx.grp * ST_COUNT + ST_IT], cx.qmax_v);
       code = code_of(replay_hadamard(cx.U + ((size_t)(col + j) * 36 + cx.xi) * cx.Cp,
@@ -393,11 +399,14 @@ static __device__ __noinline__ uint4 had_rq_slow8(HadRqCtx cx, uint4 va, uint4 v
 // Requantisation pass: h = rhe(qmax_h * I / M) with the fp32 magic-number fast path (I is exact and
 // |I| < 2^24, so the only inexactness is the product by qmax/M); near half-integers the exact int64
 // decision, and exact ties are replayed in fp64 from the U and V codes.
+#ifndef WL_RQ_GROUPS
+#define WL_RQ_GROUPS 2  // epilogue column groups of the requantisation pass (4 x groups epilogue warps)
+#endif
 template <typename HT>
 struct EpiHadRq {
   // each epilogue warp stages its 32 rows x 128 columns of codes (swizzled 16-byte slots) and
   // writes them back as whole row segments
-  static constexpr int kGroups = 2;
+  static constexpr int kGroups = WL_RQ_GROUPS;
   static constexpr int kStageBytes = 32 * (256 / kGroups) * (int)sizeof(HT);
   static constexpr int kRowBytes = (256 / kGroups) * (int)sizeof(HT);
   static constexpr int kSwz = kRowBytes / 16 - 1;  // XOR swizzle of the 16-byte slots within a row
@@ -413,12 +422,12 @@ struct EpiHadRq {
   const int8_t* V;
   HT* h;
   Geo g;
+  FixList fl;
   int wstage, qmax_u, qmax_v, qmax_h;
   StageF s;
   float r_lo, r_hi;
   int grp;
   bool small;  // |I| < 2^22: int -> float by the magic-number add instead of I2F
-  bool dummy;  // experiment switch (WL_DUMMY_EPI): skip the requantisation arithmetic
   __device__ __forceinline__ void begin(int, int row, bool valid) {
     grp = valid ? (int)g.fipg.div(g.fTP.div((unsigned)row)) : 0;
     const Acc& a = acc[(size_t)grp * ST_COUNT + ST_HAD];
@@ -436,10 +445,7 @@ struct EpiHadRq {
     // y[j] = 0x4B400000 + code: its low byte / half-word is the two's-complement code
     uint32_t y[16];
     uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;  // independent chains (ILP)
-    if (dummy) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) y[j] = v[j];
-    } else if (small) {
+    if (small) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float fi = __int_as_float((int)v[j] + 0x4B400000) - kMagic;
@@ -460,7 +466,7 @@ struct EpiHadRq {
     const int lane = threadIdx.x & 31;
     const int slot0 = ((col % hc) * (int)sizeof(HT)) >> 4;
     const uint32_t rbase = smem_u32(stage) + lane * kRowBytes;
-    const HadRqCtx cx{acc, wacc, U, V, g.C, g.Cp, grp, wstage, qmax_u, qmax_v, qmax_h, xi, row};
+    const HadRqCtx cx{acc, wacc, U, V, g.C, g.Cp, g.Kp, grp, wstage, qmax_u, qmax_v, qmax_h, xi, row, fl};
     if constexpr (sizeof(HT) == 1) {
       uint32_t w[4];
 #pragma unroll
@@ -506,6 +512,27 @@ struct EpiHadRq {
     __syncwarp();
   }
 };
+
+// Deferred exact ties of the requantisation pass: fp64 replay in the reference's order
+// (_kernels.py:99-104, c ascending), one thread per tie.
+template <typename HT>
+__global__ void __launch_bounds__(128) fixup_had_kernel(FixList fl, const int8_t* __restrict__ U,
+                                                        const int8_t* __restrict__ V, HT* __restrict__ h, Geo g,
+                                                        const Acc* __restrict__ acc, const Acc* __restrict__ wacc,
+                                                        int wstage, int qmax_u, int qmax_v, int qmax_h) {
+  const unsigned cnt = fix_count(fl, FIX_HAD);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const unsigned u = fl.items[i];
+    const unsigned rx = u / (unsigned)g.Kp, col = u - rx * (unsigned)g.Kp;
+    const unsigned row = rx / 36u, xi = rx - row * 36u;
+    const int grp = (int)g.fipg.div(g.fTP.div(row));
+    const StageQ q = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_HAD], qmax_h);
+    const StageQ qu = load_int_stage(wacc[wstage], qmax_u);
+    const StageQ qv = load_int_stage(acc[(size_t)grp * ST_COUNT + ST_IT], qmax_v);
+    const double t = replay_hadamard(U + ((size_t)col * 36 + xi) * g.Cp, V + ((size_t)row * 36 + xi) * g.Cp, g.C, qu, qv);
+    h[u] = (HT)code_of(t, q);
+  }
+}
 
 static int num_sms() {
   static int n = 0;
@@ -899,9 +926,9 @@ int wl_debug_layout(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, si
 int wl_forward_launches(const wl_plan* plan, const wl_shape*, const wl_qcfg* q) {
   if (!plan) return WL_ERR_ARG;
   // absmax, quant, [in_a|in_b(+fixup), finalize, params] x2|1, in_c, fixup, gemm max, finalize, params,
-  // gemm codes, [out_a|out_b(+fixup), finalize, params] x2|1, output table, out_c, fixup
+  // gemm codes, tie fixup, [out_a|out_b(+fixup), finalize, params] x2|1, output table, out_c, fixup
   const int otab = (q && q->output_transform_bits <= 12) ? 1 : 0;
-  return (plan->mode == WL_LEGENDRE ? 24 : 16) + otab;
+  return (plan->mode == WL_LEGENDRE ? 25 : 17) + otab;
 }
 
 }  // extern "C"
@@ -1079,12 +1106,15 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     e.V = V;
     e.h = reinterpret_cast<int8_t*>(h);
     e.g = g;
+    e.fl = fl;
     e.wstage = wstage;
     e.qmax_u = qu;
     e.qmax_v = b.q[ST_IT];
     e.qmax_h = b.q[ST_HAD];
-    e.dummy = getenv("WL_DUMMY_EPI") != nullptr;
     rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
+    if (!rc)
+      fixup_had_kernel<int8_t><<<fix_blocks, 128, 0, st>>>(fl, U, V, reinterpret_cast<int8_t*>(h), g, acc, wh->wacc, wstage,
+                                                          qu, b.q[ST_IT], b.q[ST_HAD]);
   } else {
     EpiHadRq<int16_t> e;
     e.acc = acc;
@@ -1093,12 +1123,15 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     e.V = V;
     e.h = reinterpret_cast<int16_t*>(h);
     e.g = g;
+    e.fl = fl;
     e.wstage = wstage;
     e.qmax_u = qu;
     e.qmax_v = b.q[ST_IT];
     e.qmax_h = b.q[ST_HAD];
-    e.dummy = getenv("WL_DUMMY_EPI") != nullptr;
     rc = dispatch_gemm(ta, tbm, g, bn, sw, e, st);
+    if (!rc)
+      fixup_had_kernel<int16_t><<<fix_blocks, 128, 0, st>>>(fl, U, V, reinterpret_cast<int16_t*>(h), g, acc, wh->wacc, wstage,
+                                                          qu, b.q[ST_IT], b.q[ST_HAD]);
   }
   if (rc) return rc;
   prof_mark("gemm_hadamard_codes", st);
@@ -1256,14 +1289,14 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
   WL_CUDA(cudaGetLastError());
   if (g_debug_fail) return fail(WL_ERR_CUDA, "kernel group '%s' failed: %s", g_debug_fail,
                                 cudaGetErrorString(cudaGetLastError()));
-  if (getenv("WL_FIX_STATS")) {  // debug: deferred-fix list lengths (IBC, IT, OBC, OUT) of this call
+  if (getenv("WL_FIX_STATS")) {  // debug: deferred-fix list lengths (IBC, IT, OBC, OUT, HAD) of this call
     unsigned cnt[kFixLists];
     WL_CUDA(cudaMemcpyAsync(cnt, fl.count, sizeof(cnt), cudaMemcpyDeviceToHost, st));
     WL_CUDA(cudaStreamSynchronize(st));
     const double units_in = (double)g.T * g.C, units_out = (double)g.T * g.K;
-    fprintf(stderr, "wl fix lists: ibc %u (%.3f%%) it %u (%.3f%%) obc %u (%.3f%%) out %u (%.3f%%) cap %u\n", cnt[0],
-            100.0 * cnt[0] / units_in, cnt[1], 100.0 * cnt[1] / units_in, cnt[2], 100.0 * cnt[2] / units_out, cnt[3],
-            100.0 * cnt[3] / units_out, fl.cap);
+    fprintf(stderr, "wl fix lists: ibc %u (%.3f%%) it %u (%.3f%%) obc %u (%.3f%%) out %u (%.3f%%) hadamard ties %u cap %u\n",
+            cnt[0], 100.0 * cnt[0] / units_in, cnt[1], 100.0 * cnt[1] / units_in, cnt[2], 100.0 * cnt[2] / units_out,
+            cnt[3], 100.0 * cnt[3] / units_out, cnt[FIX_HAD], fl.cap);
   }
   return WL_OK;
 }

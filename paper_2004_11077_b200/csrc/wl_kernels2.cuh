@@ -220,7 +220,7 @@ __device__ __forceinline__ int rq_col(float T, float r, float& k, float& dcol) {
 // of being fixed inline (which stalls its warp, and in the staged kernels the whole CTA at the next
 // barrier).  A follow-up kernel fixes the listed units one per thread before anything reads them.
 // If the list is full the producer fixes inline, so any capacity is correct.
-enum FixListId { FIX_IBC = 0, FIX_IT, FIX_OBC, FIX_OUT, kFixLists };
+enum FixListId { FIX_IBC = 0, FIX_IT, FIX_OBC, FIX_OUT, FIX_HAD, kFixLists };
 struct FixList {
   unsigned* count;  // [kFixLists]
   unsigned* items;  // unit ids t * nch + c, shared by the lists (producer/fixup pairs run in sequence)
