@@ -14,6 +14,7 @@ Prints one JSON line on rank 0 (see README/DESIGN for every key).
 from __future__ import annotations
 
 import argparse
+import csv
 import json
 import os
 import statistics
@@ -47,6 +48,43 @@ def layer_units(n, c, k, hw, pad):
     i8ops = 2 * 36 * T * c * k
     eff_ops = 2 * 9 * n * ho * ho * c * k
     return bytes_, i8ops, eff_ops, T
+
+
+# Forward kernels behind each wl_profile slot (wl_forward.cu prof_mark), for the DRAM traffic lookup
+SLOT_KERNELS = {
+    "absmax_input": ("absmax_input_kernel",),
+    "quant_input": ("quant_input",),
+    "input_base_change_max": ("sin_a_kernel", "finalize_input_kernel<1, 4>"),
+    "input_transform_max": ("sin_b_kernel", "fixup_ibc_kernel", "finalize_input_kernel<1, 5>"),
+    "input_transform_codes": ("sin_c_kernel", "fixup_it_kernel"),
+    "gemm_hadamard_max": ("gemm_i8_persistent<256, 128, 4, EpiHadMax>", "finalize_hadamard_kernel"),
+    "gemm_hadamard_codes": ("gemm_i8_persistent<256, 128, 3, EpiHadRq", "fixup_had_kernel"),
+    "output_base_change_max": ("sout_a_kernel", "finalize_output_kernel<1, 7"),
+    "output_max": ("sout_bt_kernel", "fixup_obct_kernel", "finalize_output_kernel<1, 8"),
+    "output_write": ("out_table_kernel", "sout_ct_kernel", "fixup_outt_kernel"),
+}
+NCU_FULL = os.path.join(ROOT, "profiles", "r01_ncu_full_cfg4.csv")
+
+
+def ncu_traffic(slot):
+    """DRAM bytes (read + write) per launch of a profile slot from the committed `ncu --set full` capture
+    of one config-4 forward (profiles/r01_ncu_full_cfg4.csv, tools/ncu_full_cfg4.sh), or None."""
+    try:
+        with open(NCU_FULL) as fh:
+            rows = list(csv.reader(fh))
+    except OSError:
+        return None
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    seen, total = set(), 0.0
+    for r in rows[1:]:
+        name = r[0]
+        if name in seen or not any(name.startswith(p) for p in SLOT_KERNELS.get(slot, ())):
+            continue
+        seen.add(name)  # first launch of each kernel (the capture holds two forwards)
+        for cell in (r[2], r[3]):
+            v, u = cell.split()
+            total += float(v) * unit[u]
+    return total if seen else None
 
 
 def kernel_units(name, n, c, k, hw, pad, hbytes=1):
@@ -295,7 +333,8 @@ def run_ours(args, rank, world, local_rank):
     else:
         roof = {"kernel": dom, "bound": "hbm", "achieved": kb / (dom_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = ncu_traffic(dom)
+    roof["traffic_source"] = "profiles/r01_ncu_full_cfg4.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
     roof["algorithmic_bytes_per_launch"] = kb
     roof["ms_per_launch"] = dom_ms
     roof["peak_source"] = peak_kind if roof["bound"] == "hbm" else ("torch._int_mm 8192^3 measured live" if i8_peak else "2x bf16 planning")

@@ -2,6 +2,7 @@
 efficiency and the top warp-stall reasons.  Usage: ncu_summary.py report.ncu-rep [out.csv]"""
 import csv
 import io
+import re
 import subprocess
 import sys
 
@@ -16,6 +17,8 @@ def main(rep, out=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
+    # tensor-pipe utilisation (tcgen05 kernels): every percent-of-peak metric of the tensor pipes
+    tkeys = [k for k in hdr if re.search(r"pipe_(tensor|tc|uma|imma)", k) and k.endswith("pct_of_peak_sustained_active")]
     lines = []
     for row in rows[2:]:
         d = dict(zip(hdr, row))
@@ -26,8 +29,9 @@ def main(rep, out=None):
                   and k.endswith("_per_issue_active.ratio") and v}
         top = sorted(stalls.items(), key=lambda x: -x[1])[:4]
         vals = {k: f"{d.get(k, '')} {u.get(k, '')}".strip() for k in KEYS}
-        lines.append([name] + [vals[k] for k in KEYS] + ["; ".join(f"{k}={v:.2f}" for k, v in top)])
-    head = ["kernel"] + KEYS + ["top_stalls(cycles/issue)"]
+        lines.append([name] + [vals[k] for k in KEYS] + ["; ".join(f"{k}={v:.2f}" for k, v in top)] +
+                     [d.get(k, "") for k in tkeys])
+    head = ["kernel"] + KEYS + ["top_stalls(cycles/issue)"] + tkeys
     buf = io.StringIO()
     w = csv.writer(buf)
     w.writerow(head)
