@@ -845,8 +845,19 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
         double f = 0.0;
         for (int k = chunk * bn + lane; k < min(chunk * bn + bn, g.K); k += 32) {
           const int8_t* urow = U + ((size_t)k * 36 + xl) * g.Cp;
-          long long sdot = 0;
-          for (int c = 0; c < g.C; ++c) sdot += (int)urow[c] * (int)vrow[c];
+          // exact integer dot over the zero-padded Cp channels: 16-byte loads, 4-way byte dot products
+          // (|sum| <= 127 * 255 * 512 < 2^31; channels >= C are zero in U and V)
+          const int4* u4 = reinterpret_cast<const int4*>(urow);
+          const int4* v4 = reinterpret_cast<const int4*>(vrow);
+          int s0 = 0, s1 = 0;
+          for (int c = 0; c < g.Cp / 16; ++c) {
+            const int4 a = __ldg(u4 + c), bb = __ldg(v4 + c);
+            s0 = __dp4a(a.x, bb.x, s0);
+            s1 = __dp4a(a.y, bb.y, s1);
+            s0 = __dp4a(a.z, bb.z, s0);
+            s1 = __dp4a(a.w, bb.w, s1);
+          }
+          const long long sdot = (long long)s0 + s1;
           if ((sdot < 0 ? -sdot : sdot) == Ml)
             f = fmax(f, fabs(replay_hadamard(urow, vrow, g.C, load_int_stage(wacc[wstage], qmax_u),
                                              load_int_stage(ga[ST_IT], qmax_v))));
