@@ -21,6 +21,7 @@
 #include "wl_float.h"
 #include "wl_kernels2.cuh"
 #include "wl_staged.cuh"
+#include "wl_tc.cuh"
 #include "wl_tmap.h"
 
 using namespace wl;
@@ -1029,8 +1030,23 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         fixup_it_kernel<0><<<fix_blocks, 128, 0, st>>>(fl, c0, c1, V, g, b, acc, plan->d_pf);
         prof_mark("input_transform_codes", st);
       } else {
-        auto ka = sin_a_kernel<1, LDs>;
-        sin_a_kernel<1, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
+        CUtensorMap amap;
+        // WL_TC_SIN_A=1: the tcgen05 Kronecker-digit pass (exact; measured 1.45 ms vs 0.67 ms for the
+        // CUDA-core pass on config 4: recombining three int32 digit accumulators per output costs as
+        // many instructions as the sparse P^-T sandwich itself — see DESIGN.md §4)
+        if ((g.Cp == 128 || g.Cp == 256) && getenv("WL_TC_SIN_A") &&
+            make_tmap_i8_4d_sw128(&amap, c0, g.Cp, g.W, g.H, g.N, 6, 6)) {
+          // tensor-core pass: one int8 MMA per (tile, 128 channels) against the Kronecker digits
+          static bool attr = false;
+          if (!attr) {
+            cudaFuncSetAttribute(tc::sin_a_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
+            attr = true;
+          }
+          tc::sin_a_tc_kernel<<<num_sms(), tc::THREADS, tc::SMEM, st>>>(amap, g, acc, tabs);
+        } else {
+          auto ka = sin_a_kernel<1, LDs>;
+          sin_a_kernel<1, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
+        }
         finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC], stage_depth(plan->mode, ST_IBC));
         prof_mark("input_base_change_max", st);

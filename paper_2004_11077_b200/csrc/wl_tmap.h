@@ -56,6 +56,22 @@ inline bool make_tmap_i8_4d(CUtensorMap* map, const void* base, uint64_t d0, uin
   return r == CUDA_SUCCESS;
 }
 
+// 4-D int8 tensor [d3][d2][d1][d0] (d0 contiguous), box {128, b1, b2, 1} with the 128-byte swizzle
+// (the MN-major SW128 operand layout of the tensor-core transforms), OOB -> zero.
+inline bool make_tmap_i8_4d_sw128(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                                  uint64_t d3, uint32_t b1, uint32_t b2) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {d0, d1, d2, d3};
+  cuuint64_t strides[3] = {d0, d0 * d1, d0 * d1 * d2};
+  cuuint32_t box[4] = {128, b1, b2, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 3-D tensor [d2][d1][d0] of 1-, 2- or 4-byte elements (d0 contiguous), box {b0, b1, b2}, no swizzle,
 // out-of-bounds boxes zero-filled (the smem box is dense [b2][b1][b0]).
 inline bool make_tmap_3d_plain(CUtensorMap* map, const void* base, int elem_bytes, uint64_t d0, uint64_t d1,
