@@ -247,3 +247,13 @@ def test_fp64_numpy_call_equals_oracle_single_image():
         yo, so = O.conv2d_winograd_quantized(x, w, mode, O.uniform_bits(8, 9))
         assert np.array_equal(y, yo)
         assert stats_tuples(st) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so]
+
+
+@pytest.mark.parametrize("cin,groups", [(128, "image"), (256, "batch"), (96, "image"), (200, "batch")])
+def test_tc_sin_a_opt_in_bit_exact(monkeypatch, cin, groups):
+    """The opt-in tcgen05 Kronecker-digit pass (WL_TC_SIN_A=1, Cp in {128, 256}) is bit-exact too."""
+    monkeypatch.setenv("WL_TC_SIN_A", "1")
+    rng = np.random.default_rng(cin)
+    x = rng.standard_normal((2, cin, 10, 13)).astype(np.float32)
+    w = _kaiming(rng, 72, cin)
+    _compare_with_oracle(x, w, "legendre", W.QuantConfig.uniform(8), 1, groups)

@@ -47,7 +47,9 @@ def _worker(rank, world, port, q):
         dist.all_gather(gathered, flat)
         same = all(torch.equal(gathered[0], g) for g in gathered)
         if rank == 0:
-            q.put({"shards": got, "tmax": float(t), "same": same, "params": flat})
+            # numpy pickles by value (a torch tensor would be shared through a file descriptor that
+            # disappears when this process exits before the parent reads it)
+            q.put({"shards": got, "tmax": float(t), "same": same, "params": flat.numpy().copy()})
     finally:
         dist.destroy_process_group()
 
@@ -79,7 +81,7 @@ def test_gloo_world2_sharding_timing_and_ddp_step():
     loss.backward()
     opt.step()
     flat = torch.cat([p.detach().flatten() for p in ref.parameters()])
-    assert torch.allclose(flat, res["params"], atol=1e-5, rtol=1e-4)
+    assert torch.allclose(flat, torch.from_numpy(res["params"]), atol=1e-5, rtol=1e-4)
 
 
 def test_shard_range_properties():
