@@ -924,12 +924,15 @@ int wl_debug_layout(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, si
   return WL_OK;
 }
 
-int wl_forward_launches(const wl_plan* plan, const wl_shape*, const wl_qcfg* q) {
+int wl_forward_launches(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q) {
   if (!plan) return WL_ERR_ARG;
+  // fp32 forward with per-image groups and W % 4 == 0, W, H <= 64: absmax + quant fused into one kernel
+  const int fused = (s && s->images_per_group == 1 && (s->w & 3) == 0 && s->w <= 64 && s->h <= 64 &&
+                     getenv("WL_FUSED_QUANT")) ? 1 : 0;
   // absmax, quant, [in_a|in_b(+fixup), finalize, params] x2|1, in_c, fixup, gemm max, finalize, params,
   // gemm codes, tie fixup, [out_a|out_b(+fixup), finalize, params] x2|1, output table, out_c, fixup
   const int otab = (q && q->output_transform_bits <= 12) ? 1 : 0;
-  return (plan->mode == WL_LEGENDRE ? 25 : 17) + otab;
+  return (plan->mode == WL_LEGENDRE ? 25 : 17) + otab - fused;
 }
 
 }  // extern "C"
@@ -961,6 +964,35 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
   prof_mark("begin", st);
   {
     const long long per_image = (long long)g.C * g.H * g.W;
+    // fused cast "input" (one HBM pass over x) for per-image groups: cooperative teams of g.H blocks
+    bool fused = false;
+    if (sizeof(XT) == 4 && g.ipg == 1 && (g.W & 3) == 0 && g.W <= 64 && g.H <= 64 && (per_image & 3) == 0 &&
+        (size_t)g.N <= L.fix_cap && getenv("WL_FUSED_QUANT")) {  // opt-in: measured 1.25 ms = the two passes
+      const size_t qsm_f = (size_t)g.W * (g.Cp + 4);
+      static int occ = -1;
+      if (occ < 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, absquant_fused_kernel, 256, qsm_f) != cudaSuccess)
+        occ = 0;
+      int cur_dev = 0, coop = 0;
+      cudaGetDevice(&cur_dev);
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cur_dev);
+      const char* te = getenv("WL_FUSED_TEAM");  // blocks per image (experiments); default H/2 rows x 2
+      int team = te ? atoi(te) : ((g.H & 1) == 0 && g.H >= 16 ? g.H / 2 : g.H);
+      team = std::max(1, std::min(team, g.H));
+      const int nteams = std::min(g.N, occ * num_sms() / team);
+      if (coop && nteams >= 1) {
+        unsigned* arrive = reinterpret_cast<unsigned*>(ws + L.off_fix + 64);  // fix items: unused until the transforms
+        WL_CUDA(cudaMemsetAsync(arrive, 0, sizeof(unsigned) * g.N, st));
+        prof_mark("absmax_input", st);
+        const float* xf = reinterpret_cast<const float*>(x);
+        int teamv = team;
+        void* args[] = {(void*)&xf, (void*)&c0, (void*)&g, (void*)&b, (void*)&acc, (void*)&arrive, (void*)&teamv};
+        WL_CUDA(cudaLaunchCooperativeKernel((const void*)absquant_fused_kernel, dim3(nteams * team), dim3(256), args,
+                                            qsm_f, st));
+        prof_mark("quant_input", st);
+        fused = true;
+      }
+    }
+    if (!fused) {
     int bx = (int)std::min<long long>((per_image / 4 + 255) / 256, 64);
     absmax_input_kernel<XT><<<dim3(std::max(bx, 1), g.N), 256, 0, st>>>(x, per_image, g.ipg, acc);
     prof_mark("absmax_input", st);
@@ -977,6 +1009,7 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     else
       quant_input_kernel<XT><<<dim3(g.H, g.N), 256, qsm, st>>>(x, c0, g, b, acc, qrow);
     prof_mark("quant_input", st);
+    }
   }
   int8_t* c1 = reinterpret_cast<int8_t*>(ws + L.off_c1);
   int8_t* c4 = reinterpret_cast<int8_t*>(ws + L.off_c4);

@@ -182,11 +182,9 @@ __global__ void __launch_bounds__(256) quant_input_kernel(const XT* __restrict__
 #ifndef WL_QI_MINB
 #define WL_QI_MINB 4  // <= 64 registers: 4 row blocks per SM keep more loads in flight (0.89 -> 0.80 ms)
 #endif
-__global__ void __launch_bounds__(256, WL_QI_MINB) quant_input_w64_kernel(const float* __restrict__ x, int8_t* __restrict__ c0,
-                                                              Geo g, Bits b, const Acc* __restrict__ acc) {
-  extern __shared__ __align__(16) int8_t srow[];
-  const int h = blockIdx.x, n = blockIdx.y;
-  const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
+// One image row (h, n) of quant_input_w64: the body shared by the two-pass and the fused kernel.
+__device__ __forceinline__ void quant_row_w64(const float* __restrict__ x, int8_t* __restrict__ c0, const Geo& g,
+                                              const StageQ& q, int h, int n, int8_t* srow) {
   const float rc = q.maxabs > 0.0 ? (float)((double)q.qmax / q.maxabs) : 0.f;
   const float thr = 0.5f - (float)((q.qmax + 1) * 1.25 * 5.9604644775390625e-8);
   const int ld = g.Cp + 4;
@@ -231,6 +229,60 @@ __global__ void __launch_bounds__(256, WL_QI_MINB) quant_input_w64_kernel(const 
   for (int i = threadIdx.x; i < g.W * wpr; i += blockDim.x) {
     const int w = i >> lw, j = i & (wpr - 1);
     dst[i] = *reinterpret_cast<const uint32_t*>(srow + w * ld + 4 * j);
+  }
+}
+
+__global__ void __launch_bounds__(256, WL_QI_MINB) quant_input_w64_kernel(const float* __restrict__ x, int8_t* __restrict__ c0,
+                                                              Geo g, Bits b, const Acc* __restrict__ acc) {
+  extern __shared__ __align__(16) int8_t srow[];
+  const int h = blockIdx.x, n = blockIdx.y;
+  const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
+  quant_row_w64(x, c0, g, q, h, n, srow);
+}
+
+// Fused cast "input" for per-image scale groups (fp32, W % 4 == 0, W <= 64), cooperative launch:
+// a team of `team` co-resident blocks takes one image at a time — every block reduces 1/team of the
+// image's max|x| (atomicMax), the team meets at a per-image counter, then the blocks quantise the
+// image's rows.  The second read of the image hits L2 (teams in flight x 3.2 MB << 126 MB), so x
+// crosses HBM once instead of twice (absmax_input + quant_input_w64).
+__global__ void __launch_bounds__(256, WL_QI_MINB) absquant_fused_kernel(const float* __restrict__ x,
+                                                                         int8_t* __restrict__ c0, Geo g, Bits b,
+                                                                         Acc* __restrict__ acc,
+                                                                         unsigned* __restrict__ arrive, int team) {
+  extern __shared__ __align__(16) int8_t srow[];
+  __shared__ unsigned long long wm[8];
+  const int nteams = gridDim.x / team, tm = blockIdx.x / team, k = blockIdx.x - tm * team;
+  if (tm >= nteams) return;
+  const long long per4 = (long long)g.C * g.H * g.W / 4;
+  const long long lo = per4 * k / team, hi = per4 * (k + 1) / team;
+  for (int n = tm; n < g.N; n += nteams) {
+    const float4* x4 = reinterpret_cast<const float4*>(x + (size_t)n * g.C * g.H * g.W);
+    unsigned long long m = 0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      const float4 v = __ldg(&x4[i]);
+      m = max(m, max(max(abs_bits(v.x), abs_bits(v.y)), max(abs_bits(v.z), abs_bits(v.w))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    Acc* a = acc + (size_t)n * ST_COUNT + ST_INPUT;  // images_per_group == 1
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, wm[w]);
+      if (m) atomicMax(&a->M, max_to_f64_bits<float>(m));
+      __threadfence();
+      atomicAdd(&arrive[n], 1u);
+      while (*(volatile unsigned*)&arrive[n] < (unsigned)team) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+    Acc snap;
+    snap.M = __ldcg(&a->M);  // the team's final maximum (L2, not a stale L1 line)
+    const StageQ q = load_float_stage(snap, b.q[ST_INPUT]);
+    for (int h = k; h < g.H; h += team) {
+      quant_row_w64(x, c0, g, q, h, n, srow);
+      __syncthreads();
+    }
   }
 }
 

@@ -257,3 +257,15 @@ def test_tc_sin_a_opt_in_bit_exact(monkeypatch, cin, groups):
     x = rng.standard_normal((2, cin, 10, 13)).astype(np.float32)
     w = _kaiming(rng, 72, cin)
     _compare_with_oracle(x, w, "legendre", W.QuantConfig.uniform(8), 1, groups)
+
+
+@pytest.mark.parametrize("groups", ["image"])
+def test_fused_input_cast_opt_in_bit_exact(monkeypatch, groups):
+    """The opt-in cooperative fused absmax + quantise pass (WL_FUSED_QUANT=1) is bit-exact too."""
+    monkeypatch.setenv("WL_FUSED_QUANT", "1")
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((5, 48, 12, 16)).astype(np.float32)
+    x[3] = 0.0  # all-zero image: scale 1.0
+    w = _kaiming(rng, 40, 48)
+    for mode in ("legendre", "canonical"):
+        _compare_with_oracle(x, w, mode, W.QuantConfig.uniform(8), 1, groups)
