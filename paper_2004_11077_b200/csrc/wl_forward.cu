@@ -21,6 +21,7 @@
 #include "wl_float.h"
 #include "wl_kernels2.cuh"
 #include "wl_staged.cuh"
+#include "wl_pair.cuh"
 #include "wl_tc.cuh"
 #include "wl_tmap.h"
 
@@ -1040,6 +1041,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
   // the input code pass is staged (bulk-copied c0 windows / c1 blocks); the output code pass stays on
   // the plain grid (staged it measured 2.8x slower: y stores from few resident CTAs)
   const bool staged_c = !getenv("WL_PLAIN_IN_C");
+  // two channels per thread on packed f32x2 (wl_pair.cuh; bit-identical, fewer issued instructions)
+  const bool pair = !getenv("WL_NO_PAIR");
   CUtensorMap c0map;
   if (g.Cp <= 256 && !make_tmap_i8_4d(&c0map, c0, g.Cp, g.W, g.H, g.N, g.Cp, 6, 6))
     return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled (input window) failed");
@@ -1076,6 +1079,11 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
             attr = true;
           }
           tc::sin_a_tc_kernel<<<num_sms(), tc::THREADS, tc::SMEM, st>>>(amap, g, acc, tabs);
+        } else if (pair) {
+          using S2 = Staged2<LDs, 1>;
+          auto ka = sin_a2_kernel<1, LDs>;
+          const long long it2 = (g.T + S2::TPB - 1) / S2::TPB;
+          sin_a2_kernel<1, LDs><<<staged_grid(ka, S2::THREADS, S2::SMEM, it2), S2::THREADS, S2::SMEM, st>>>(c0map, g, acc, tabs);
         } else {
           auto ka = sin_a_kernel<1, LDs>;
           sin_a_kernel<1, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
@@ -1083,13 +1091,25 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC], stage_depth(plan->mode, ST_IBC));
         prof_mark("input_base_change_max", st);
-        auto kb = sin_b_kernel<LDs>;
-        sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM_OUT, iters), S::THREADS, S::SMEM_OUT, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs, fl);
+        if (pair) {
+          using S2 = Staged2<LDs, 1>;
+          auto kb = sin_b2_kernel<LDs>;
+          const long long it2 = (g.T + S2::TPB - 1) / S2::TPB;
+          sin_b2_kernel<LDs><<<staged_grid(kb, S2::THREADS, S2::SMEM_OUT, it2), S2::THREADS, S2::SMEM_OUT, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs, fl);
+        } else {
+          auto kb = sin_b_kernel<LDs>;
+          sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM_OUT, iters), S::THREADS, S::SMEM_OUT, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs, fl);
+        }
         fixup_ibc_kernel<<<fix_blocks, 128, 0, st>>>(fl, c0, c1, g, b, acc, plan->d_pf, tabs);
         finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
-        if (staged_c) {
+        if (staged_c && pair) {
+          using S2 = Staged2<LDs, 1>;
+          auto kc = sin_c2_kernel<LDs>;
+          const long long it2 = (g.T + S2::TPB - 1) / S2::TPB;
+          sin_c2_kernel<LDs><<<staged_grid(kc, S2::THREADS, S2::SMEM_OUT, it2), S2::THREADS, S2::SMEM_OUT, st>>>(c0map, c0, c1, V, g, b, acc, plan->d_pf, fl);
+        } else if (staged_c) {
           auto kc = sin_c_kernel<1, LDs>;
           sin_c_kernel<1, LDs><<<staged_grid(kc, S::THREADS, S::SMEM_OUT, iters), S::THREADS, S::SMEM_OUT, st>>>(c0map, c0, c1, V, g, b, acc, plan->d_pf, fl);
         } else
@@ -1246,17 +1266,32 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         fixup_out_kernel<0, HT, YT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, y, bias, g, b, acc, plan->d_pf);
         prof_mark("output_write", st);
       } else {
-        auto ka = sout_a_kernel<1, HT, LDs>;
-        sout_a_kernel<1, HT, LDs><<<staged_grid(ka, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, g, acc, tabs);
+        if (pair) {
+          using S2 = Staged2<LDs, sizeof(HT)>;
+          auto ka = sout_a2_kernel<1, HT, LDs>;
+          const long long it2 = (g.T + S2::TPB - 1) / S2::TPB;
+          sout_a2_kernel<1, HT, LDs><<<staged_grid(ka, S2::THREADS, S2::SMEM, it2), S2::THREADS, S2::SMEM, st>>>(hh, g, acc, tabs);
+        } else {
+          auto ka = sout_a_kernel<1, HT, LDs>;
+          sout_a_kernel<1, HT, LDs><<<staged_grid(ka, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, g, acc, tabs);
+        }
         finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC], stage_depth(plan->mode, ST_OBC));
         prof_mark("output_base_change_max", st);
         if (t4path) {
           // T4 path: the output stage's fp32 values + error factors are stored instead of c4
-          using ST4 = StagedT4<LDs, sizeof(HT)>;
-          auto kbt = sout_bt_kernel<HT, LDs>;
-          sout_bt_kernel<HT, LDs><<<staged_grid(kbt, ST4::THREADS, ST4::SMEM, iters), ST4::THREADS, ST4::SMEM, st>>>(
-              hh, t4, e4, g, b, acc, plan->d_pf, tabs, fl);
+          if (pair) {
+            using ST42 = StagedT42<LDs, sizeof(HT)>;
+            auto kbt = sout_bt2_kernel<HT, LDs>;
+            const long long it2 = (g.T + ST42::TPB - 1) / ST42::TPB;
+            sout_bt2_kernel<HT, LDs><<<staged_grid(kbt, ST42::THREADS, ST42::SMEM, it2), ST42::THREADS, ST42::SMEM, st>>>(
+                hh, t4, e4, g, b, acc, plan->d_pf, tabs, fl);
+          } else {
+            using ST4 = StagedT4<LDs, sizeof(HT)>;
+            auto kbt = sout_bt_kernel<HT, LDs>;
+            sout_bt_kernel<HT, LDs><<<staged_grid(kbt, ST4::THREADS, ST4::SMEM, iters), ST4::THREADS, ST4::SMEM, st>>>(
+                hh, t4, e4, g, b, acc, plan->d_pf, tabs, fl);
+          }
           fixup_obct_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, t4, e4, g, b, acc, plan->d_pf, tabs);
           finalize_output_kernel<1, ST_OUT, HT, true><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
           stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
