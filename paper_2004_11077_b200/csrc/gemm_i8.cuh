@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;
     const int row = m0 + 32 * q + lane;
     const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16);
+    if constexpr (Epi::kPrefetch) epi.prefetch(row, row < T);
     epi.begin(xi, row, row < T);
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
@@ -250,6 +251,16 @@ __global__ void __launch_bounds__(EpiShape<Epi::kGroups>::kThreads, 1)
     constexpr int HC = BN / kEpiGroups;
     if constexpr (Epi::kStageBytes > 0) epi.set_stage(sEpi + ew * Epi::kStageBytes, HC);
     int local = 0;
+    // Epis with prefetch(): the next tile's per-row parameters are loaded one tile ahead, so their
+    // global-load latency hides behind this tile's drain instead of stalling the epilogue warp
+    constexpr bool kPre = Epi::kPrefetch;
+    if constexpr (kPre) {
+      if ((int)blockIdx.x < ntiles) {
+        int xi, mb, nb;
+        decode(blockIdx.x, xi, mb, nb);
+        epi.prefetch(mb * 128 + 32 * q + lane, mb * 128 + 32 * q + lane < T);
+      }
+    }
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
       int xi, mb, nb;
       decode(tile, xi, mb, nb);
@@ -258,6 +269,13 @@ __global__ void __launch_bounds__(EpiShape<Epi::kGroups>::kThreads, 1)
       const int row = mb * 128 + 32 * q + lane;
       // per-row parameters (global loads) before the wait: their latency overlaps the MMA
       epi.begin(xi, row, row < T);
+      if constexpr (kPre) {
+        if (tile + (int)gridDim.x < ntiles) {
+          int xn, mn, nn;
+          decode(tile + gridDim.x, xn, mn, nn);
+          epi.prefetch(mn * 128 + 32 * q + lane, mn * 128 + 32 * q + lane < T);
+        }
+      }
       mbar_wait(&accfull[a], aph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + (uint32_t)(a * BN + half * HC);

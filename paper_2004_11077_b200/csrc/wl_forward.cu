@@ -322,6 +322,8 @@ struct EpiHadMax {
   long long m;
   int vmax, vmin;
   int grp;
+  static constexpr bool kPrefetch = false;
+  __device__ __forceinline__ void prefetch(int, bool) {}
   __device__ __forceinline__ void begin(int, int row, bool valid) {
     vmax = 0;
     vmin = 0;
@@ -430,9 +432,18 @@ struct EpiHadRq {
   float r_lo, r_hi;
   int grp;
   bool small;  // |I| < 2^22: int -> float by the magic-number add instead of I2F
+  int pgrp;             // prefetched (next tile) group and its stage parameters
+  float pr, pthr;
+  static constexpr bool kPrefetch = true;
+  __device__ __forceinline__ void prefetch(int row, bool valid) {
+    pgrp = valid ? (int)g.fipg.div(g.fTP.div((unsigned)row)) : 0;
+    const Acc& a = acc[(size_t)pgrp * ST_COUNT + ST_HAD];
+    pr = a.r;
+    pthr = a.thr;
+  }
   __device__ __forceinline__ void begin(int, int row, bool valid) {
-    grp = valid ? (int)g.fipg.div(g.fTP.div((unsigned)row)) : 0;
-    const Acc& a = acc[(size_t)grp * ST_COUNT + ST_HAD];
+    grp = pgrp;
+    const struct { float r, thr; } a = {pr, pthr};
     s.r = a.r;
     s.band = 0.5f - a.thr;
     s.qmax = qmax_h;
@@ -448,12 +459,16 @@ struct EpiHadRq {
     uint32_t y[16];
     uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;  // independent chains (ILP)
     if (small) {
+      // column pairs on packed f32x2 (FADD2 / FFMA2: lane-wise identical to the scalar ops)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float fi = __int_as_float((int)v[j] + 0x4B400000) - kMagic;
-        y[j] = __float_as_uint(fmaf(fi, r_lo, kMagic));
-        const uint32_t d = y[j] ^ __float_as_uint(fmaf(fi, r_hi, kMagic));
-        if ((j & 3) == 0) d0 |= d; else if ((j & 3) == 1) d1 |= d; else if ((j & 3) == 2) d2 |= d; else d3 |= d;
+      for (int j = 0; j < 16; j += 2) {
+        const f2 fi = sub2(mk2(__int_as_float((int)v[j] + 0x4B400000), __int_as_float((int)v[j + 1] + 0x4B400000)),
+                           bc2(kMagic));
+        const f2 ya = fma2(fi, bc2(r_lo), bc2(kMagic)), yb = fma2(fi, bc2(r_hi), bc2(kMagic));
+        y[j] = __float_as_uint(lo2(ya));
+        y[j + 1] = __float_as_uint(hi2(ya));
+        const uint32_t da = y[j] ^ __float_as_uint(lo2(yb)), db = y[j + 1] ^ __float_as_uint(hi2(yb));
+        if ((j & 2) == 0) d0 |= da, d1 |= db; else d2 |= da, d3 |= db;
       }
     } else {
 #pragma unroll
@@ -1304,14 +1319,24 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
               oc_rc = fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled (T4) failed");
               return;
             }
-            constexpr int smem = 2 * (StagedOut::TPB * 17 * StagedOut::KB * 4) + StagedOut::OUT_BYTES + 16;
+            // 2-deep input ring at 4 CTAs/SM; WL_CT_NS3=1 selects a 3-deep ring at 3 CTAs/SM (measured
+            // slower on config 4: 2.23 vs 1.78 ms — fewer resident warps to drain the y stores)
+            const bool ns2 = getenv("WL_CT_NS3") == nullptr;
+            const int smem = (ns2 ? 2 : 3) * (StagedOut::TPB * 17 * StagedOut::KB * 4) + StagedOut::OUT_BYTES + 32;
             const long long oiters = (long long)((g.T + StagedOut::TPB - 1) / StagedOut::TPB) * ((g.K + StagedOut::KB - 1) / StagedOut::KB);
             auto launch = [&](auto tabc) {
               constexpr bool TAB = decltype(tabc)::value;
-              auto kern = sout_ct_kernel<HT, TAB>;
-              sout_ct_kernel<HT, TAB><<<staged_grid(kern, StagedOut::THREADS, smem, oiters), StagedOut::THREADS, smem, st>>>(
-                  tm4, em4, hh, reinterpret_cast<float*>(y), reinterpret_cast<const float*>(bias), g, b, acc, plan->d_pf,
-                  otab, fl);
+              if (ns2) {
+                auto kern = sout_ct_kernel<HT, TAB, 2>;
+                kern<<<staged_grid(kern, StagedOut::THREADS, smem, oiters), StagedOut::THREADS, smem, st>>>(
+                    tm4, em4, hh, reinterpret_cast<float*>(y), reinterpret_cast<const float*>(bias), g, b, acc, plan->d_pf,
+                    otab, fl);
+              } else {
+                auto kern = sout_ct_kernel<HT, TAB, 3>;
+                kern<<<staged_grid(kern, StagedOut::THREADS, smem, oiters), StagedOut::THREADS, smem, st>>>(
+                    tm4, em4, hh, reinterpret_cast<float*>(y), reinterpret_cast<const float*>(bias), g, b, acc, plan->d_pf,
+                    otab, fl);
+              }
             };
             if (otab)
               launch(std::true_type{});

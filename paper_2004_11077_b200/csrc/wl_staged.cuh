@@ -621,8 +621,8 @@ __global__ void __launch_bounds__(128) fixup_obct_kernel(FixList fl, const HT* _
 // Final output pass from T4 / e4 (Legendre, fp32 output).  Work item = 8 tiles x 32 channels: TMA
 // boxes {32, 16, 8} of T4 and {32, 1, 8} of e4; warp = tile, lane = channel; outputs staged and
 // stored as in sout_c_kernel.
-template <typename HT, bool TAB>
-__global__ void __launch_bounds__(StagedOut::THREADS, 4)
+template <typename HT, bool TAB, int NS>
+__global__ void __launch_bounds__(StagedOut::THREADS, NS == 2 ? 4 : 3)
     sout_ct_kernel(const __grid_constant__ CUtensorMap t4map, const __grid_constant__ CUtensorMap e4map,
                    const HT* __restrict__ h, float* __restrict__ y, const float* __restrict__ bias,
                    const __grid_constant__ Geo g, const __grid_constant__ Bits b, const Acc* __restrict__ acc,
@@ -631,8 +631,8 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 4)
   constexpr int T4B = S::TPB * 16 * S::KB * 4, EB = S::TPB * S::KB * 4, IN_BYTES = T4B + EB;
   extern __shared__ __align__(128) uint8_t wl_stage_smem[];
   uint8_t* sm = wl_stage_smem;
-  float* so = reinterpret_cast<float*>(sm + 2 * IN_BYTES);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 2 * IN_BYTES + S::OUT_BYTES);
+  float* so = reinterpret_cast<float*>(sm + NS * IN_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + NS * IN_BYTES + S::OUT_BYTES);
   __shared__ long long ybase[S::TPB];
   __shared__ int yrows[S::TPB];
   const int nkb = (g.K + S::KB - 1) / S::KB;
@@ -641,8 +641,8 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 4)
   const int qo = b.q[ST_OUT];
   const long long plane = (long long)g.Ho * g.Wo;
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
     fence_mbar_init();
     tma_prefetch_desc(&t4map);
     tma_prefetch_desc(&e4map);
@@ -654,11 +654,16 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 4)
     tma_load_3d(sm + s * IN_BYTES, &t4map, &bar[s], kb * S::KB, 0, tg * S::TPB);
     tma_load_3d(sm + s * IN_BYTES + T4B, &e4map, &bar[s], kb * S::KB, 0, tg * S::TPB);
   };
-  if (threadIdx.x == 0 && (int)blockIdx.x < niter) issue(blockIdx.x, 0);
+  // NS-deep ring: NS-1 work items in flight while one is computed (buffer (kk-1) % NS is refilled
+  // only after every thread passed iteration kk-1's trailing barrier)
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < NS - 1; ++q)
+      if ((int)blockIdx.x + q * (int)gridDim.x < niter) issue(blockIdx.x + q * gridDim.x, q);
   int kk = 0;
   for (int it = blockIdx.x; it < niter; it += gridDim.x, ++kk) {
-    const int s = kk & 1;
-    if (threadIdx.x == 0 && it + (int)gridDim.x < niter) issue(it + gridDim.x, s ^ 1);
+    const int s = kk % NS;
+    if (threadIdx.x == 0 && it + (NS - 1) * (int)gridDim.x < niter) issue(it + (NS - 1) * gridDim.x, (kk + NS - 1) % NS);
     const int tg = it / nkb, kb = it - tg * nkb;
     const int t0 = tg * S::TPB, k0 = kb * S::KB;
     if (threadIdx.x < S::TPB) {
@@ -674,7 +679,7 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 4)
       ybase[threadIdx.x] = base;
       yrows[threadIdx.x] = rows;
     }
-    mbar_wait(&bar[s], (uint32_t)((kk >> 1) & 1));
+    mbar_wait(&bar[s], (uint32_t)((kk / NS) & 1));
     {
       const int t = t0 + w, k = k0 + lane;
       const bool active = t < g.T && k < g.K;
