@@ -148,10 +148,38 @@ static __device__ __noinline__ double replay_sandwich(const double* __restrict__
 }
 
 // Hadamard element: sum_c deq(u_c) * deq(v_c), c ascending from 0.0 (_kernels.py:99-104).
-static __device__ __noinline__ double replay_hadamard(const int8_t* __restrict__ u, const int8_t* __restrict__ v, int C,
+template <bool kCold = true>
+__device__ __noinline__ double replay_hadamard(const int8_t* __restrict__ u, const int8_t* __restrict__ v, int C,
                                                StageQ qu, StageQ qv) {
+  // kCold (one tie per thread, rows not yet cached: fixup_had_kernel): the two code rows are pulled
+  // into L1 up front — one prefetch per 128-byte line — and read 16 bytes at a time, so the
+  // c-ascending fp64 chain reads L1 instead of paying an HBM/L2 round trip per sector (114 -> 19 us).
+  // Warm callers (finalize_hadamard: rows shared by neighbouring candidates) keep the byte loop,
+  // measured faster there.
+  if (!kCold) {
+    double acc = 0.0;
+    for (int c = 0; c < C; ++c)
+      acc = __dadd_rn(acc, __dmul_rn(deq(u[c], qu.qmax, qu.maxabs, qu.scale), deq(v[c], qv.qmax, qv.maxabs, qv.scale)));
+    return acc;
+  }
+  for (int c = 0; c < C; c += 128) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(u + c));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(v + c));
+  }
   double acc = 0.0;
-  for (int c = 0; c < C; ++c)
+  int c = 0;
+  if ((((uintptr_t)u | (uintptr_t)v) & 15) == 0) {
+    for (; c + 16 <= C; c += 16) {
+      const int4 a = __ldg(reinterpret_cast<const int4*>(u + c)), b = __ldg(reinterpret_cast<const int4*>(v + c));
+      const int aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int cu = (int)(int8_t)(aw[j >> 2] >> (8 * (j & 3))), cv = (int)(int8_t)(bw[j >> 2] >> (8 * (j & 3)));
+        acc = __dadd_rn(acc, __dmul_rn(deq(cu, qu.qmax, qu.maxabs, qu.scale), deq(cv, qv.qmax, qv.maxabs, qv.scale)));
+      }
+    }
+  }
+  for (; c < C; ++c)
     acc = __dadd_rn(acc, __dmul_rn(deq(u[c], qu.qmax, qu.maxabs, qu.scale), deq(v[c], qv.qmax, qv.maxabs, qv.scale)));
   return acc;
 }

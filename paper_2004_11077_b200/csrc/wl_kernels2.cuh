@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
           }
           const long long sdot = (long long)s0 + s1;
           if ((sdot < 0 ? -sdot : sdot) == Ml)
-            f = fmax(f, fabs(replay_hadamard(urow, vrow, g.C, load_int_stage(wacc[wstage], qmax_u),
+            f = fmax(f, fabs(replay_hadamard<false>(urow, vrow, g.C, load_int_stage(wacc[wstage], qmax_u),
                                              load_int_stage(ga[ST_IT], qmax_v))));
         }
         if (f > 0.0) atomicMax(&ga[ST_HAD].F, dbits(f));
