@@ -54,13 +54,13 @@ def layer_units(n, c, k, hw, pad):
 SLOT_KERNELS = {
     "absmax_input": ("absmax_input_kernel",),
     "quant_input": ("quant_input",),
-    "input_base_change_max": ("sin_a_kernel", "finalize_input_kernel<1, 4>"),
-    "input_transform_max": ("sin_b_kernel", "fixup_ibc_kernel", "finalize_input_kernel<1, 5>"),
-    "input_transform_codes": ("sin_c_kernel", "fixup_it_kernel"),
+    "input_base_change_max": ("sin_a_kernel", "sin_a2_kernel", "finalize_input_kernel<1, 4>"),
+    "input_transform_max": ("sin_b_kernel", "sin_b2_kernel", "fixup_ibc_kernel", "finalize_input_kernel<1, 5>"),
+    "input_transform_codes": ("sin_c_kernel", "sin_c2_kernel", "fixup_it_kernel"),
     "gemm_hadamard_max": ("gemm_i8_persistent<256, 128, 4, EpiHadMax>", "finalize_hadamard_kernel"),
     "gemm_hadamard_codes": ("gemm_i8_persistent<256, 128, 3, EpiHadRq", "fixup_had_kernel"),
-    "output_base_change_max": ("sout_a_kernel", "finalize_output_kernel<1, 7"),
-    "output_max": ("sout_bt_kernel", "fixup_obct_kernel", "finalize_output_kernel<1, 8"),
+    "output_base_change_max": ("sout_a_kernel", "sout_a2_kernel", "finalize_output_kernel<1, 7"),
+    "output_max": ("sout_bt_kernel", "sout_bt2_kernel", "fixup_obct_kernel", "finalize_output_kernel<1, 8"),
     "output_write": ("out_table_kernel", "sout_ct_kernel", "fixup_outt_kernel"),
 }
 NCU_FULL = os.path.join(ROOT, "profiles", "r01_ncu_full_cfg4.csv")
