@@ -1070,7 +1070,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
       if (!leg) {
         auto ka = sin_a_kernel<0, LDs>;
         sin_a_kernel<0, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
-        finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+        finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT], fl);
+        finalize_input_exec<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
         if (staged_c) {
@@ -1103,7 +1104,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
           auto ka = sin_a_kernel<1, LDs>;
           sin_a_kernel<1, LDs><<<staged_grid(ka, S::THREADS, S::SMEM, iters), S::THREADS, S::SMEM, st>>>(c0map, g, acc, tabs);
         }
-        finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
+        finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC], fl);
+        finalize_input_exec<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC], stage_depth(plan->mode, ST_IBC));
         prof_mark("input_base_change_max", st);
         if (pair) {
@@ -1116,7 +1118,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
           sin_b_kernel<LDs><<<staged_grid(kb, S::THREADS, S::SMEM_OUT, iters), S::THREADS, S::SMEM_OUT, st>>>(c0map, c0, c1, g, b, acc, plan->d_pf, tabs, fl);
         }
         fixup_ibc_kernel<<<fix_blocks, 128, 0, st>>>(fl, c0, c1, g, b, acc, plan->d_pf, tabs);
-        finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+        finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT], fl);
+        finalize_input_exec<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
         if (staged_c && pair) {
@@ -1135,7 +1138,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     } else {
       if (!leg) {
         in_a_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
-        finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+        finalize_input_kernel<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT], fl);
+        finalize_input_exec<0, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
         in_c_kernel<0, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
@@ -1143,12 +1147,14 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         prof_mark("input_transform_codes", st);
       } else {
         in_a_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, g, acc, tabs);
-        finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC]);
+        finalize_input_kernel<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IBC], E.e[ST_IBC], fl);
+        finalize_input_exec<1, ST_IBC><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IBC, b.q[ST_IBC], E.e[ST_IBC], stage_depth(plan->mode, ST_IBC));
         prof_mark("input_base_change_max", st);
         in_b_kernel<LD><<<tgrid, tb, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs, fl);
         fixup_ibc_kernel<<<fix_blocks, 128, 0, st>>>(fl, c0, c1, g, b, acc, plan->d_pf, tabs);
-        finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT]);
+        finalize_input_kernel<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, tabs.t[ST_IT], E.e[ST_IT], fl);
+        finalize_input_exec<1, ST_IT><<<fin_blocks, 256, 0, st>>>(c0, c1, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_IT, b.q[ST_IT], E.e[ST_IT], stage_depth(plan->mode, ST_IT));
         prof_mark("input_transform_max", st);
         in_c_kernel<1, LD><<<tgrid, tb, 0, st>>>(c0, c1, V, g, b, acc, plan->d_pf, fl);
@@ -1273,7 +1279,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
       if (!leg) {
         auto ka = sout_a_kernel<0, HT, LDs>;
         sout_a_kernel<0, HT, LDs><<<staged_grid(ka, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, g, acc, tabs);
-        finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+        finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT], fl);
+        finalize_output_exec<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
@@ -1290,7 +1297,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
           auto ka = sout_a_kernel<1, HT, LDs>;
           sout_a_kernel<1, HT, LDs><<<staged_grid(ka, SH::THREADS, SH::SMEM, iters), SH::THREADS, SH::SMEM, st>>>(hh, g, acc, tabs);
         }
-        finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
+        finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC], fl);
+        finalize_output_exec<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC], stage_depth(plan->mode, ST_OBC));
         prof_mark("output_base_change_max", st);
         if (t4path) {
@@ -1308,7 +1316,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
                 hh, t4, e4, g, b, acc, plan->d_pf, tabs, fl);
           }
           fixup_obct_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, t4, e4, g, b, acc, plan->d_pf, tabs);
-          finalize_output_kernel<1, ST_OUT, HT, true><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+          finalize_output_kernel<1, ST_OUT, HT, true><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT], fl);
+        finalize_output_exec<1, ST_OUT, HT, true><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, fl);
           stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
           prof_mark("output_max", st);
           make_otab();
@@ -1351,7 +1360,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         auto kb = sout_b_kernel<HT, LDs>;
         sout_b_kernel<HT, LDs><<<staged_grid(kb, SH::THREADS, SH::SMEM_OUT, iters), SH::THREADS, SH::SMEM_OUT, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
         fixup_obc_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, g, b, acc, plan->d_pf, tabs);
-        finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+        finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT], fl);
+        finalize_output_exec<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
@@ -1362,7 +1372,8 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
     } else {
       if (!leg) {
         out_a_kernel<0, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
-        finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+        finalize_output_kernel<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT], fl);
+        finalize_output_exec<0, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();
@@ -1371,12 +1382,14 @@ static int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s
         prof_mark("output_write", st);
       } else {
         out_a_kernel<1, HT, LD><<<ogrid, tb, 0, st>>>(hh, g, acc, tabs);
-        finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC]);
+        finalize_output_kernel<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OBC], E.e[ST_OBC], fl);
+        finalize_output_exec<1, ST_OBC, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OBC, b.q[ST_OBC], E.e[ST_OBC], stage_depth(plan->mode, ST_OBC));
         prof_mark("output_base_change_max", st);
         out_b_kernel<HT, LD><<<ogrid, tb, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs, fl);
         fixup_obc_kernel<HT><<<fix_blocks, 128, 0, st>>>(fl, hh, c4, g, b, acc, plan->d_pf, tabs);
-        finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT]);
+        finalize_output_kernel<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, tabs.t[ST_OUT], E.e[ST_OUT], fl);
+        finalize_output_exec<1, ST_OUT, HT><<<fin_blocks, 256, 0, st>>>(hh, c4, g, b, acc, plan->d_pf, fl);
         stage_params_kernel<<<pgrid, 128, 0, st>>>(acc, L.groups, ST_OUT, b.q[ST_OUT], E.e[ST_OUT], stage_depth(plan->mode, ST_OUT));
         prof_mark("output_max", st);
         make_otab();

@@ -501,11 +501,28 @@ __device__ void exact_input_unit(const int8_t* __restrict__ c0, const int8_t* __
   atomicMax(&ga[STAGE].F, dbits(f));
 }
 
+// Finalize candidate lists: count slot kCandSlot0 + stage of the FixList counters (the fix lists use
+// slots 0..4), items in the shared FixList buffer (free between a stage's fixup and the next
+// producer).  Appends this warp's candidate lanes (entry ids) and returns the lanes that did not fit.
+constexpr int kCandSlot0 = 4;
+__device__ __forceinline__ unsigned defer_cands(const FixList& f, int slot, unsigned mask, unsigned entry) {
+  if (!mask) return 0u;
+  const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+  unsigned base = 0;
+  if (lane == leader) base = atomicAdd(f.count + slot, (unsigned)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  const bool mine = (mask >> lane) & 1u;
+  const unsigned idx = base + (unsigned)__popc(mask & ((1u << lane) - 1u));
+  const bool stored = mine && idx < f.cap;
+  if (stored) f.items[idx] = entry;
+  return mask & ~__ballot_sync(0xffffffffu, stored);
+}
+
 // Scan a stage's max table; warps recompute exactly the entries within 2E of the group's fp32 max.
 template <int MODE, int STAGE>
 __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1, Geo g, Bits b,
                                       Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                      const unsigned* __restrict__ table, float rowsum) {
+                                      const unsigned* __restrict__ table, float rowsum, FixList fl) {
   // thread per tile row t (group data loaded once), walking the row's CB entries; a warp's 32
   // consecutive rows read contiguous table segments.  Entries within 2E of the group's fp32 max are
   // recomputed exactly by the whole warp (lane per channel).
@@ -525,6 +542,10 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
     for (int cb = 0; cb < NB; ++cb) {
       const float v = valid ? __uint_as_float(table[(size_t)t * NB + cb]) : 0.f;
       unsigned mask = __ballot_sync(0xffffffffu, v > 0.f && v >= lim);
+      // candidate entries go to a list processed one warp each by finalize_*_exec (the scan's warps
+      // stay short; a group whose maximum many entries reach no longer serialises on one warp);
+      // a full list falls back to recomputing here
+      mask = defer_cands(fl, kCandSlot0 + STAGE, mask, t * (unsigned)NB + (unsigned)cb);
       while (mask) {
         const int l = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -532,6 +553,22 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
         if (ch < g.C) exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, tl, ch);
       }
     }
+  }
+}
+
+// Finalize candidates, one warp per listed (tile row, 32-channel block) entry, lane per channel.
+template <int MODE, int STAGE>
+__global__ void __launch_bounds__(256) finalize_input_exec(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
+                                                           Geo g, Bits b, Acc* __restrict__ acc,
+                                                           const PlanF64* __restrict__ pf, FixList fl) {
+  const unsigned NB = (unsigned)((g.C + 31) >> 5);
+  const unsigned cnt = fix_count(fl, kCandSlot0 + STAGE);
+  const int lane = threadIdx.x & 31;
+  const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += nw) {
+    const unsigned e = fl.items[i], t = e / NB, cb = e - t * NB;
+    const int ch = (int)cb * 32 + lane;
+    if (ch < g.C) exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, (int)t, ch);
   }
 }
 
@@ -769,7 +806,7 @@ __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __rest
 template <int MODE, int STAGE, typename HT, bool FROM_H = false>
 __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* __restrict__ c4, Geo g, Bits b,
                                        Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
-                                       const unsigned* __restrict__ table, float rowsum) {
+                                       const unsigned* __restrict__ table, float rowsum, FixList fl) {
   // thread per tile row t (group data loaded once), walking the row's KB entries; a warp's 32
   // consecutive rows read contiguous table segments.  Entries within 2E of the group's fp32 max are
   // recomputed exactly by the whole warp (lane per channel).
@@ -789,6 +826,10 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
     for (int cb = 0; cb < NB; ++cb) {
       const float v = valid ? __uint_as_float(table[(size_t)t * NB + cb]) : 0.f;
       unsigned mask = __ballot_sync(0xffffffffu, v > 0.f && v >= lim);
+      // candidate entries go to a list processed one warp each by finalize_*_exec (the scan's warps
+      // stay short; a group whose maximum many entries reach no longer serialises on one warp);
+      // a full list falls back to recomputing here
+      mask = defer_cands(fl, kCandSlot0 + STAGE, mask, t * (unsigned)NB + (unsigned)cb);
       while (mask) {
         const int l = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -796,6 +837,21 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
         if (ch < g.K) exact_output_unit<MODE, STAGE, HT, FROM_H>(h, c4, g, b, acc, pf, tl, ch);
       }
     }
+  }
+}
+
+template <int MODE, int STAGE, typename HT, bool FROM_H = false>
+__global__ void __launch_bounds__(256) finalize_output_exec(const HT* __restrict__ h, const int8_t* __restrict__ c4,
+                                                            Geo g, Bits b, Acc* __restrict__ acc,
+                                                            const PlanF64* __restrict__ pf, FixList fl) {
+  const unsigned NB = (unsigned)((g.K + 31) >> 5);
+  const unsigned cnt = fix_count(fl, kCandSlot0 + STAGE);
+  const int lane = threadIdx.x & 31;
+  const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += nw) {
+    const unsigned e = fl.items[i], t = e / NB, cb = e - t * NB;
+    const int ch = (int)cb * 32 + lane;
+    if (ch < g.K) exact_output_unit<MODE, STAGE, HT, FROM_H>(h, c4, g, b, acc, pf, (int)t, ch);
   }
 }
 
