@@ -948,7 +948,8 @@ int wl_forward_launches(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q
   // absmax, quant, [in_a|in_b(+fixup), finalize, params] x2|1, in_c, fixup, gemm max, finalize, params,
   // gemm codes, tie fixup, [out_a|out_b(+fixup), finalize, params] x2|1, output table, out_c, fixup
   const int otab = (q && q->output_transform_bits <= 12) ? 1 : 0;
-  return (plan->mode == WL_LEGENDRE ? 25 : 17) + otab - fused;
+  // + one finalize_*_exec per transform finalize (4 Legendre, 2 canonical)
+  return (plan->mode == WL_LEGENDRE ? 29 : 19) + otab - fused;
 }
 
 }  // extern "C"

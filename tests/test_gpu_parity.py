@@ -269,3 +269,21 @@ def test_fused_input_cast_opt_in_bit_exact(monkeypatch, groups):
     w = _kaiming(rng, 40, 48)
     for mode in ("legendre", "canonical"):
         _compare_with_oracle(x, w, mode, W.QuantConfig.uniform(8), 1, groups)
+
+
+@pytest.mark.parametrize("cin,cout,hw,bits", [(17, 24, (9, 11), 8), (64, 70, (14, 14), 8), (256, 256, (12, 12), 8),
+                                               (33, 40, (10, 13), 9)])
+def test_one_channel_kernels_equal_two_channel_kernels(monkeypatch, cin, cout, hw, bits):
+    """WL_NO_PAIR=1 (one channel per thread, scalar fp32) and the default two-channel f32x2 kernels
+    (wl_pair.cuh) give identical outputs and stage statistics; both also equal the oracle."""
+    rng = np.random.default_rng(cin * 7 + cout)
+    x = rng.standard_normal((3, cin) + hw).astype(np.float32)
+    w = _kaiming(rng, cout, cin)
+    qc = W.QuantConfig.uniform(8, hadamard_bits=bits)
+    r2, y2 = run_gpu(x, w, "legendre", qc, 1)
+    monkeypatch.setenv("WL_NO_PAIR", "1")
+    r1, y1 = run_gpu(x, w, "legendre", qc, 1)
+    assert torch.equal(y1, y2)
+    for s1, s2 in zip(r1.stats(), r2.stats()):
+        assert stats_tuples(s1) == stats_tuples(s2)
+    _compare_with_oracle(x, w, "legendre", qc, 1, "image")
