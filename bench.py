@@ -1,14 +1,17 @@
 """Benchmark of the B200 quantized Legendre-Winograd F(4,3) layer (BASELINE.json metric).
 
-Workload (BASELINE.json configs[3], the largest single-GPU configuration): per GPU N=1024 images,
-Cin=Cout=256, 56x56, pad 1, 8-bit Legendre F(4,3) forward, x ~ N(0,1) fp32, Kaiming-normal weights,
-bias 0, no collective.  Stage scales are per image ("image" groups: every image is quantized exactly
-as one reference call on that image).  A step is one forward over the 1024 images; the weight
-transform is cached (computed once before timing, as the north star's "amortised" weight kernel).
+Default workload (BASELINE.json configs[3], the largest single-GPU configuration): per GPU N=1024
+images, Cin=Cout=256, 56x56, pad 1, 8-bit Legendre F(4,3) forward, x ~ N(0,1) fp32, Kaiming-normal
+weights, bias 0, no collective.  Stage scales are per image ("image" groups: every image is
+quantized exactly as one reference call on that image).  A step is one forward over the 1024 images;
+the weight transform is cached (computed once before timing, the north star's "amortised" kernel).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload layer|train|bwd|sweep] [--scale-groups image|batch]
 
-Prints one JSON line on rank 0 (see README/DESIGN for every key).
+--gpus N > 1 without a torchrun environment re-launches itself under torch.distributed.run with N
+ranks (one GPU each, NCCL); the batch is sharded (N x 1024 images), no data-path collective,
+timing is the max over ranks.  Prints one JSON line on rank 0 (sweep/bwd: one line per config).
 """
 
 from __future__ import annotations
@@ -17,6 +20,7 @@ import argparse
 import csv
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -36,12 +40,14 @@ def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
 def layer_units(n, c, k, hw, pad):
+    """SURVEY §8d algorithmic units of one forward call: fp32 x + fp32 y + weights bytes, int8 GEMM
+    ops, direct-convolution-equivalent ops, tiles."""
     ho = hw + 2 * pad - 2
     T = n * (-(-ho // 4)) ** 2
     bytes_ = 4 * n * c * hw * hw + 4 * n * k * ho * ho + 36 * c * k + 4 * k
@@ -50,25 +56,37 @@ def layer_units(n, c, k, hw, pad):
     return bytes_, i8ops, eff_ops, T
 
 
-# Forward kernels behind each wl_profile slot (wl_forward.cu prof_mark), for the DRAM traffic lookup
+def bwd_units(n, c, k, hw, pad):
+    """SURVEY §8d backward units: dY + dX + re-read x (4 B each per element) + dW bytes; two 36-way
+    GEMM sets (dV, dU)."""
+    ho = hw + 2 * pad - 2
+    T = n * (-(-ho // 4)) ** 2
+    bytes_ = 4 * n * k * ho * ho + 4 * n * c * hw * hw * 2 + 4 * 9 * c * k
+    ops = 2 * (2 * 36 * T * c * k)
+    return bytes_, ops
+
+
+# Forward kernels behind each wl_profile slot (prof_mark in wl_fwd*.cu), for the DRAM traffic lookup
 SLOT_KERNELS = {
     "absmax_input": ("absmax_input_kernel",),
     "quant_input": ("quant_input",),
-    "input_base_change_max": ("sin_a_kernel", "sin_a2_kernel", "finalize_input_kernel<1, 4>"),
-    "input_transform_max": ("sin_b_kernel", "sin_b2_kernel", "fixup_ibc_kernel", "finalize_input_kernel<1, 5>"),
-    "input_transform_codes": ("sin_c_kernel", "sin_c2_kernel", "fixup_it_kernel"),
-    "gemm_hadamard_max": ("gemm_i8_persistent<256, 128, 4, EpiHadMax>", "finalize_hadamard_kernel"),
-    "gemm_hadamard_codes": ("gemm_i8_persistent<256, 128, 3, EpiHadRq", "fixup_had_kernel"),
-    "output_base_change_max": ("sout_a_kernel", "sout_a2_kernel", "finalize_output_kernel<1, 7"),
-    "output_max": ("sout_bt_kernel", "sout_bt2_kernel", "fixup_obct_kernel", "finalize_output_kernel<1, 8"),
+    "input_base_change_max": ("sin_a2_kernel", "finalize_input_kernel<1, 4>", "finalize_input_exec<1, 4>"),
+    "input_transform_max": ("sin_b2_kernel", "fixup_ibc_kernel", "finalize_input_kernel<1, 5>",
+                            "finalize_input_exec<1, 5>"),
+    "input_transform_codes": ("sin_c2_kernel", "fixup_it_kernel"),
+    "gemm_hadamard_max": ("gemm_i8_persistent<256, 128, 4, EpiHadMax>", "gemm_i8_bstat<EpiHadMax",
+                          "finalize_hadamard_kernel"),
+    "gemm_hadamard_codes": ("gemm_i8_persistent<256, 128, 3, EpiHadRq", "gemm_i8_bstat<EpiHadRq", "fixup_had_kernel"),
+    "output_base_change_max": ("sout_a2_kernel", "finalize_output_kernel<1, 7", "finalize_output_exec<1, 7"),
+    "output_max": ("sout_bt2_kernel", "fixup_obct_kernel", "finalize_output_kernel<1, 8", "finalize_output_exec<1, 8"),
     "output_write": ("out_table_kernel", "sout_ct_kernel", "fixup_outt_kernel"),
 }
-NCU_FULL = os.path.join(ROOT, "profiles", "r01_ncu_full_cfg4.csv")
+NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_cfg4.csv")
 
 
 def ncu_traffic(slot):
     """DRAM bytes (read + write) per launch of a profile slot from the committed `ncu --set full` capture
-    of one config-4 forward (profiles/r01_ncu_full_cfg4.csv, tools/ncu_full_cfg4.sh), or None."""
+    of one config-4 forward (profiles/r02_ncu_full_cfg4.csv, tools/ncu_full_cfg4.sh), or None."""
     try:
         with open(NCU_FULL) as fh:
             rows = list(csv.reader(fh))
@@ -88,10 +106,10 @@ def ncu_traffic(slot):
 
 
 def kernel_units(name, n, c, k, hw, pad, hbytes=1):
-    """Algorithmic (compulsory) bytes and int8 ops of one launch of each forward kernel."""
+    """Algorithmic (compulsory) bytes and int8 ops of one launch of each forward slot."""
     ho = hw + 2 * pad - 2
     T = n * (-(-ho // 4)) ** 2
-    p2 = lambda v, lo: lo if v <= lo else 1 << (v - 1).bit_length()  # noqa: E731  (wl_forward.cu pow2_at_least)
+    p2 = lambda v, lo: lo if v <= lo else 1 << (v - 1).bit_length()  # noqa: E731  (wl_internal.h pow2_at_least)
     cp, kp = p2(c, 32), p2(k, 64)
     x, c0, V, U, h, y = 4 * n * c * hw * hw, n * hw * hw * cp, 36 * T * cp, 36 * kp * cp, 36 * T * kp * hbytes, 4 * n * k * ho * ho
     table = {
@@ -104,6 +122,8 @@ def kernel_units(name, n, c, k, hw, pad, hbytes=1):
 
 
 class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms during the timed region."""
+
     def __init__(self, index):
         self.index, self.proc, self.path = index, None, None
 
@@ -146,63 +166,80 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def cpu_baseline(seconds_target=12.0, mode="legendre"):
-    """The CPU port of the reference path (oracle/, bit-identical to the reference's numba backend),
-    on all host threads, per-image calls on a bounded sample of config-4 images."""
+def physical_cores():
+    """Physical cores among the CPUs this process may run on (hyper-thread siblings counted once)."""
+    cpus = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count() or 1))
+    seen = set()
+    for cpu in cpus:
+        try:
+            with open(f"/sys/devices/system/cpu/cpu{cpu}/topology/thread_siblings_list") as fh:
+                seen.add(fh.read().strip())
+        except OSError:
+            seen.add(str(cpu))
+    return max(1, len(seen)), len(cpus)
+
+
+def cpu_baseline_and_parity(x_s, w, y_s, mode, groups):
+    """cpu_baseline leg (rank 0, N=1): the CPU port of the reference path (oracle/, pinned bit-identical
+    to the reference's numba backend) timed on the host's physical cores over a bounded sample of the
+    bench's own images — and, as the checker, those images' GPU outputs compared bit for bit with it."""
     from oracle import oracle as O
 
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    rng = np.random.default_rng(0)
-    k = CFG["c"]
-    w = (rng.standard_normal((k, k, 3, 3)) * np.sqrt(2.0 / (9 * k))).astype(np.float32).astype(np.float64)
-    x1 = rng.standard_normal((threads, CFG["c"], CFG["hw"], CFG["hw"])).astype(np.float32).astype(np.float64)
+    cores, logical = physical_cores()
     bits = O.uniform_bits(8)
-    O.quant_conv_batch(x1[:1, :, :8, :8], w, mode, bits, padding=1, nthreads=1)  # load / warm
-    t0 = time.perf_counter()
-    O.quant_conv_batch(x1, w, mode, bits, padding=1, images_per_group=1, nthreads=threads)
-    dt = time.perf_counter() - t0
-    reps = max(1, int(seconds_target / max(dt, 1e-3)))
-    times = [dt]
-    for _ in range(min(reps, 5) - 1):
+    x64, w64 = x_s.astype(np.float64), w.astype(np.float64)
+    ipg = 1 if groups == "image" else x_s.shape[0]
+    O.quant_conv_batch(x64[:1, :, :8, :8], w64, mode, bits, padding=1, nthreads=1)  # load / warm
+    times, yo = [], None
+    for _ in range(3):
         t0 = time.perf_counter()
-        O.quant_conv_batch(x1, w, mode, bits, padding=1, images_per_group=1, nthreads=threads)
+        yo, _, _ = O.quant_conv_batch(x64, w64, mode, bits, padding=1, images_per_group=ipg, nthreads=cores)
         times.append(time.perf_counter() - t0)
+        if sum(times) > 20.0:
+            break
     best = min(times)
-    return {"value": threads / best, "unit": "images/s", "cores": threads, "kind": "port",
-            "sample": f"{threads} config-4 images (256ch 56x56 pad1, Legendre 8b, per-image calls), "
-                      f"best of {len(times)} runs, oracle/winoleg_oracle.c fp64 port of the reference path"}
+    k = x_s.shape[0]
+    base = {"value": k / best, "unit": "images/s", "cores": cores, "logical_cpus": logical, "kind": "port",
+            "sample": f"{k} of the bench's config-4 images (256ch 56x56 pad1, Legendre 8b, per-image calls), "
+                      f"best of {len(times)} runs, oracle/winoleg_oracle.c fp64 port of the reference path "
+                      f"on {cores} physical cores"}
+    parity = None
+    if groups == "image":
+        parity = {"images": int(k), "bit_exact": bool(np.array_equal(y_s, yo.astype(np.float32))),
+                  "checker": "oracle/ (pinned to the reference's golden fixtures)", "workload": "N=1024 bench output"}
+    return base, parity
 
 
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path (C port, bit-identical to the numba backend) on the
-    host cores; rank 0 only."""
+    host's physical cores; rank 0 only."""
     if rank != 0:
         return
     from oracle import oracle as O
 
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    cores, logical = physical_cores()
     rng = np.random.default_rng(0)
     k = CFG["c"]
     w = (rng.standard_normal((k, k, 3, 3)) * np.sqrt(2.0 / (9 * k))).astype(np.float32).astype(np.float64)
-    x = rng.standard_normal((threads, CFG["c"], CFG["hw"], CFG["hw"])).astype(np.float32).astype(np.float64)
+    x = rng.standard_normal((cores, CFG["c"], CFG["hw"], CFG["hw"])).astype(np.float32).astype(np.float64)
     bits = O.uniform_bits(8)
     for _ in range(args.warmup):
-        O.quant_conv_batch(x, w, CFG["mode"], bits, padding=1, images_per_group=1, nthreads=threads)
+        O.quant_conv_batch(x, w, CFG["mode"], bits, padding=1, images_per_group=1, nthreads=cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        O.quant_conv_batch(x, w, CFG["mode"], bits, padding=1, images_per_group=1, nthreads=threads)
+        O.quant_conv_batch(x, w, CFG["mode"], bits, padding=1, images_per_group=1, nthreads=cores)
     dt = (time.perf_counter() - t0) / args.steps
-    _, _, eff, _ = layer_units(threads, CFG["c"], CFG["c"], CFG["hw"], CFG["pad"])
-    val = threads / dt
+    _, _, eff, _ = layer_units(cores, CFG["c"], CFG["c"], CFG["hw"], CFG["pad"])
+    val = cores / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config4: N=1024/GPU Cin=Cout=256 56x56 pad1 Legendre 8b fwd (sampled)",
-                   "sample_images_per_step": threads, "scale_groups": "image"},
+                   "sample_images_per_step": cores, "scale_groups": "image"},
         "effective_tops": eff / dt / 1e12,
-        "cpu_baseline": {"value": val, "unit": "images/s", "cores": threads, "kind": "port",
-                         "sample": f"{threads} images per step (one per host thread), per-image reference calls"},
+        "cpu_baseline": {"value": val, "unit": "images/s", "cores": cores, "logical_cpus": logical, "kind": "port",
+                         "sample": f"{cores} images per step (one per physical core), per-image reference calls"},
         "e2e": {"value": val, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,9 +265,44 @@ def measure_int8_peak(torch):
         return None
 
 
+def measure_pcie(torch, nbytes=1 << 30):
+    """Pinned-host <-> device copy bandwidth (GB/s): H2D alone, D2H alone, best of 3 (CUDA events)."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {}
+    for name, fn in (("h2d_gbs", lambda: d.copy_(h, non_blocking=True)), ("d2h_gbs", lambda: h.copy_(d, non_blocking=True))):
+        best = 1e9
+        for _ in range(3):
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = nbytes / (best * 1e-3) / 1e9
+    del h, d
+    return out
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _max_over_ranks(torch, v, world, dev):
+    if world == 1:
+        return v
+    import torch.distributed as dist
+
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
-    import torch.distributed as dist
 
     import paper_2004_11077_b200 as W
     from paper_2004_11077_b200 import _lib
@@ -239,6 +311,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     n, c, hw, pad = CFG["n"], CFG["c"], CFG["hw"], CFG["pad"]
     k = c
+    groups = args.scale_groups
     qc = W.QuantConfig.from_name(CFG["qconfig"])
     plan = W.build_plan(4, 3, use_legendre=True)
     gen = torch.Generator(device=dev)
@@ -249,18 +322,14 @@ def run_ours(args, rank, world, local_rank):
     w = torch.randn((k, c, 3, 3), generator=gw, device=dev) * float(np.sqrt(2.0 / (9 * c)))
     y = torch.empty((n, k, hw + 2 * pad - 2, hw + 2 * pad - 2), device=dev)
     r = W.QuantWinogradConv(plan, CFG["mode"], qc, dev)
-    r.forward(x, w, padding=pad, out=y)  # builds the weight cache + workspace
+    r.forward(x, w, padding=pad, out=y, scale_groups=groups)  # builds the weight cache + workspace
     torch.cuda.synchronize()
     launches = r.launches()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
     for _ in range(args.warmup):
-        r.forward(x, w, padding=pad, out=y)
+        r.forward(x, w, padding=pad, out=y, scale_groups=groups)
     torch.cuda.synchronize()
-    barrier()
+    _barrier(world)
     clocks = ClockSampler(local_rank)
     if rank == 0:
         clocks.start()
@@ -269,27 +338,36 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    barrier()
+    _barrier(world)
     e0.record(stream)
     for _ in range(args.steps):
-        r.forward(x, w, padding=pad, out=y)
+        r.forward(x, w, padding=pad, out=y, scale_groups=groups)
     e1.record(stream)
     torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    _barrier(world)
+    ms_rank = e0.elapsed_time(e1) / args.steps
     kern, calls = _lib.profile_read()
     _lib.profile_enable(False)
     clk = clocks.stop() if rank == 0 else None
+    ms = _max_over_ranks(torch, ms_rank, world, dev)
+    per_rank_ms = [ms_rank]
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        import torch.distributed as dist
+
+        per_rank_ms = [None] * world
+        dist.all_gather_object(per_rank_ms, ms_rank)
+
+    # parity sample (checked in the cpu_baseline leg on rank 0 at N=1)
+    ksamp = min(physical_cores()[0], 8)
+    x_s = x[:ksamp].cpu().numpy() if groups == "image" else x.cpu().numpy()
+    y_s = y[:ksamp].cpu().numpy() if groups == "image" else y.cpu().numpy()
+    w_s = w.cpu().numpy()
 
     # end to end through the public API with host buffers: pinned x -> device, forward, y -> pinned host,
     # copies inside the timed region (chunked so copy-in / compute / copy-out overlap; per-image scale
     # groups make the chunks independent, results identical to one call)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and groups == "image":
         del x
         torch.cuda.empty_cache()
         xh = torch.empty((n, c, hw, hw), dtype=torch.float32, pin_memory=True)
@@ -298,21 +376,21 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(2):
             r.forward_host(xh, w, yh, padding=pad)
         torch.cuda.synchronize()
-        barrier()
+        _barrier(world)
         ke = max(1, min(args.steps, 5))
         e0.record(stream)
         for _ in range(ke):
             r.forward_host(xh, w, yh, padding=pad)
         e1.record(stream)
         torch.cuda.synchronize()
-        me = e0.elapsed_time(e1) / ke
-        if world > 1:
-            t = torch.tensor([me], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            me = float(t.item())
-        e2e = {"value": world * n / (me * 1e-3), "unit": "images/s",
-               "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4),
-               "ms_per_step": me,
+        me = _max_over_ranks(torch, e0.elapsed_time(e1) / ke, world, dev)
+        pcie = measure_pcie(torch)
+        hb, db_ = int(xh.numel() * 4), int(yh.numel() * 4)
+        bound_ms = max(hb / (pcie["h2d_gbs"] * 1e9), db_ / (pcie["d2h_gbs"] * 1e9)) * 1e3
+        e2e = {"value": world * n / (me * 1e-3), "unit": "images/s", "h2d_bytes_per_step": hb,
+               "d2h_bytes_per_step": db_, "ms_per_step": me,
+               "pcie": dict(pcie, bound_ms=bound_ms, frac=bound_ms / me,
+                            note="bound = max(H2D bytes / H2D GB/s, D2H bytes / D2H GB/s): copies overlap (full duplex)"),
                "path": "QuantWinogradConv.forward_host (C ABI wl_forward per chunk), pinned host x/y, 8 chunks"}
         del xh, yh
 
@@ -334,7 +412,7 @@ def run_ours(args, rank, world, local_rank):
         roof = {"kernel": dom, "bound": "hbm", "achieved": kb / (dom_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(dom)
-    roof["traffic_source"] = "profiles/r01_ncu_full_cfg4.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
+    roof["traffic_source"] = "profiles/r02_ncu_full_cfg4.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
     roof["algorithmic_bytes_per_launch"] = kb
     roof["ms_per_launch"] = dom_ms
     roof["peak_source"] = peak_kind if roof["bound"] == "hbm" else ("torch._int_mm 8192^3 measured live" if i8_peak else "2x bf16 planning")
@@ -344,20 +422,128 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int8", "data": "synthetic (torch.randn on device, seeded per rank)",
         "config": {"workload": "config4: N=1024/GPU Cin=Cout=256 56x56 pad1 Legendre F(4,3) 8b fwd",
-                   "scale_groups": "image", "l2": "inputs (3.29 GB) larger than L2", "global_batch": world * n,
+                   "scale_groups": groups, "l2": "inputs (3.29 GB) larger than L2", "global_batch": world * n,
                    "parallelism": f"batch-sharded x{world}, no collective"},
         "effective_tops": world * eff / (ms * 1e-3) / 1e12,
         "layer_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms * 1e-3), "hbm_bytes": bytes_,
                            "int8_ops": i8ops, "int8_peak_tops": i8_peak, "hbm_gbs": hbm},
         "roofline": roof,
+        "per_rank_ms": per_rank_ms,
         "kernel_ms": {kname: round(v, 4) for kname, v in per_kernel.items()},
         "gpu_launches": launches * args.steps,
         "clocks": clk,
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline()
+        base, parity = cpu_baseline_and_parity(x_s, w_s, y_s, CFG["mode"], groups)
+        line["cpu_baseline"] = base
+        if parity is not None:
+            line["parity"] = parity
     print(json.dumps(line), flush=True)
+
+
+def _time_fn(torch, fn, steps, warmup):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_sweep(args, rank, world, local_rank, backward_only=False):
+    """One JSON line per BASELINE config (forward, CUDA-graph replay for the launch-bound shapes) and per
+    config-3 shape forward + STE backward, each with its SURVEY §8d roofline."""
+    import torch
+
+    import paper_2004_11077_b200 as W
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    hbm, bf16, peak_kind = _peaks()
+    i8 = measure_int8_peak(torch) or 2 * bf16
+    plan = W.build_plan(4, 3, use_legendre=True)
+    steps, warm = max(args.steps, 20), max(args.warmup, 3)
+
+    def emit(d):
+        if rank == 0:
+            print(json.dumps(d), flush=True)
+
+    fwd_cfgs = [("config1", 8, 64, 32, "legendre", "8b", "image")]
+    for mode in ("legendre", "canonical"):
+        for q in ("8b+9b", "8b"):
+            fwd_cfgs.append((f"config2 {mode} {q}", 128, 128, 16, mode, q, "image"))
+    for c, hw in ((64, 32), (128, 16), (256, 8), (512, 4)):
+        fwd_cfgs.append((f"config3 C={c} {hw}x{hw} fwd", 256, c, hw, "legendre", "8b", "image"))
+    fwd_cfgs.append(("config4 batch scale groups", 1024, 256, 56, "legendre", "8b", "batch"))
+    if not backward_only:
+        for name, n, c, hw, mode, q, groups in fwd_cfgs:
+            g = torch.Generator(device=dev)
+            g.manual_seed(0)
+            x = torch.randn((n, c, hw, hw), generator=g, device=dev)
+            if name.startswith("config3"):
+                x = x.clamp_min_(0)
+            w = torch.randn((c, c, 3, 3), generator=g, device=dev) * float(np.sqrt(2.0 / (9 * c)))
+            y = torch.empty((n, c, hw, hw), device=dev)
+            r = W.QuantWinogradConv(plan, mode, W.QuantConfig.from_name(q), dev)
+            small = n * c * hw * hw * 4 < 512 << 20
+            fn = (r.capture(x, w, y, padding=1, scale_groups=groups) if small
+                  else (lambda: r.forward(x, w, padding=1, out=y, scale_groups=groups)))
+            ms = _time_fn(torch, fn, steps if small else max(3, args.steps), warm)
+            bytes_, i8ops, eff, _ = layer_units(n, c, c, hw, 1)
+            t_roof = max(bytes_ / (hbm * 1e9), i8ops / (i8 * 1e12))
+            emit({"metric": METRIC, "workload": "sweep", "config": name, "n": n, "c": c, "hw": hw, "mode": mode,
+                  "qconfig": q, "scale_groups": groups, "ms": ms, "images_per_s": n / (ms * 1e-3),
+                  "effective_tops": eff / (ms * 1e-3) / 1e12, "t_roof_us": t_roof * 1e6,
+                  "roofline_frac": t_roof / (ms * 1e-3), "cuda_graph": small, "gpu_launches": r.launches(),
+                  "peaks": {"hbm_gbs": hbm, "int8_tops": i8, "hbm_source": peak_kind}})
+            del x, y, r
+            torch.cuda.empty_cache()
+    # config 3: forward (training forward, saved block) + STE backward
+    for c, hw in ((64, 32), (128, 16), (256, 8), (512, 4)):
+        n = 256
+        g = torch.Generator(device=dev)
+        g.manual_seed(1)
+        x = torch.randn((n, c, hw, hw), generator=g, device=dev).clamp_min_(0)
+        w = (torch.randn((c, c, 3, 3), generator=g, device=dev) * float(np.sqrt(2.0 / (9 * c)))).requires_grad_()
+        dy = torch.randn((n, c, hw, hw), generator=g, device=dev)
+        mod = W.WinogradAwareConv2d(c, c).to(dev)
+        with torch.no_grad():
+            mod.weight.copy_(w)
+        xr = x.clone().requires_grad_()
+
+        def fwd_bwd():
+            out = mod(xr)
+            out.backward(dy)
+
+        ms_fb = _time_fn(torch, fwd_bwd, max(args.steps, 10), warm)
+        r = mod._runner(dev)
+
+        def fwd():
+            with torch.no_grad():
+                mod(x)
+
+        ms_f = _time_fn(torch, fwd, max(args.steps, 10), warm)
+        yv = mod(xr)
+        shape, cache, saved, _ = r._last
+
+        def bwd():
+            r.backward(dy, shape, cache, saved, False)
+
+        ms_b = _time_fn(torch, bwd, max(args.steps, 10), warm)
+        bb, bops = bwd_units(n, c, c, hw, 1)
+        t_roof_b = max(bb / (hbm * 1e9), bops / (bf16 * 1e12))
+        emit({"metric": "config-3 STE backward (dX, dW, db)", "workload": "sweep-bwd", "config": f"config3 C={c} {hw}x{hw}",
+              "n": n, "c": c, "hw": hw, "mode": "legendre", "qconfig": "8b", "ms_backward": ms_b,
+              "ms_forward_train": ms_f, "ms_forward_plus_backward": ms_fb, "images_per_s_fwd_bwd": n / (ms_fb * 1e-3),
+              "t_roof_backward_us": t_roof_b * 1e6, "roofline_frac_backward": t_roof_b / (ms_b * 1e-3),
+              "roofline_basis": "SURVEY §8d: bytes dY+dX+x+dW at measured HBM, ops 2x(2*36*T*C*K) at measured bf16 dense"})
+        del x, w, dy, mod, xr, yv
+        torch.cuda.empty_cache()
 
 
 def run_train(args, rank, world, local_rank):
@@ -365,7 +551,6 @@ def run_train(args, rank, world, local_rank):
     training step (forward, STE backward, SGD momentum 0.9, lr 0.1) on 256 synthetic 3x32x32 images
     per GPU; data parallel with one NCCL gradient all-reduce per step (DDP) when N > 1."""
     import torch
-    import torch.distributed as dist
 
     from paper_2004_11077_b200 import training as TR
 
@@ -381,19 +566,15 @@ def run_train(args, rank, world, local_rank):
     for _ in range(args.warmup):
         TR.train_step(net, opt, x, y)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    _barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
         loss = TR.train_step(net, opt, x, y)
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    _barrier(world)
+    ms = _max_over_ranks(torch, e0.elapsed_time(e1) / args.steps, world, dev)
     if rank == 0:
         print(json.dumps({
             "metric": "ResNet-18 (Winograd-aware Legendre 8b) training throughput", "value": world * batch / (ms * 1e-3),
@@ -405,6 +586,39 @@ def run_train(args, rank, world, local_rank):
         }), flush=True)
 
 
+def run_selftest(args, rank, world):
+    """CPU check of the launcher and the timing plumbing (gloo): every rank times a fixed numpy step;
+    the line's n_gpus is the world size and ms_per_step the max over ranks (tests/test_bench_launcher.py)."""
+    import torch
+    import torch.distributed as dist
+
+    a = np.random.default_rng(rank).standard_normal((256, 256))
+    _barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        a = np.tanh(a @ a.T * 1e-3)
+    ms = (time.perf_counter() - t0) / args.steps * 1e3 * (1 + rank)  # rank-dependent: the max must win
+    t = torch.tensor([ms], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    per = [None] * world
+    if world > 1:
+        dist.all_gather_object(per, ms)
+    else:
+        per = [ms]
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_gpus": world, "ms_per_step": float(t.item()), "per_rank_ms": per,
+                          "steps": args.steps}), flush=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -413,13 +627,30 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="layer", choices=["layer", "train"],
-                    help="layer: config-4 layer throughput (default); train: config-5 ResNet-18 training step")
+    ap.add_argument("--scale-groups", default="image", choices=["image", "batch"])
+    ap.add_argument("--workload", default="layer", choices=["layer", "train", "bwd", "sweep"],
+                    help="layer: config-4 layer throughput (default); train: config-5 ResNet-18 training step; "
+                         "bwd: config-3 forward + STE backward lines; sweep: every forward config + bwd")
+    ap.add_argument("--selftest", action="store_true", help="CPU/gloo check of the launcher (no GPU work)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # self-launch: one rank per GPU under torch.distributed.run (the driver's own command line)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.selftest:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("gloo")
+        run_selftest(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -431,6 +662,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.workload == "train":
         run_train(args, rank, world, local_rank)
+    elif args.workload in ("sweep", "bwd"):
+        run_sweep(args, rank, world, local_rank, backward_only=args.workload == "bwd")
     else:
         run_ours(args, rank, world, local_rank)
     if world > 1:

@@ -85,13 +85,24 @@ int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const f
 int wl_forward_f64(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const double* x, const void* cache,
                    const double* bias, double* y, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Training forward: wl_forward with the part of its state the STE backward needs — the per-group
+ * stage slots and the V codes — written to a separate `saved` buffer, so the caller can keep that
+ * buffer until backward and release the (much larger) workspace right away.  wl_train_sizes gives
+ * both sizes; the workspace of wl_forward_train is smaller than wl_forward's by the saved block. */
+int wl_train_sizes(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* saved_bytes,
+                   size_t* workspace_bytes);
+int wl_forward_train(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
+                     const float* bias, float* y, void* saved, size_t saved_bytes, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
 /* Straight-through-estimator backward (no reference counterpart): casts are identity,
- * scales detached, products use the forward's quantised U and V.  fwd_workspace must be the
- * workspace of the wl_forward call being differentiated (it holds the V codes and stage scales).
+ * scales detached, products use the forward's quantised U and V.  `saved` is the saved buffer of the
+ * wl_forward_train call being differentiated, or the whole workspace of a wl_forward call (both
+ * start with the stage slots and V codes at the same offsets).
  * dx [n][c_in][h][w], dw [c_out][c_in][3][3], db [c_out] (may be NULL), all fp32. */
 int wl_backward_workspace_size(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* bytes);
 int wl_backward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* dy, const void* cache,
-                const void* fwd_workspace, float* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
+                const void* saved, float* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
                 void* stream);
 
 /* Float (unquantized) Winograd correlation in fp32 — the reference's conv2d_winograd(x, w, plan,
@@ -136,6 +147,10 @@ int wl_forward_launches(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q
  * over every wl_forward issued since the previous read. */
 int wl_profile_enable(int on);
 int wl_profile_read(const char** names_out, double* ms_out, int max, int* n_out, int* calls_out);
+
+/* Test hook: capacity of the deferred exact-fix lists (0 = automatic, the default).  A tiny cap forces
+ * every producer onto its inline fallback; results must not change (tests/test_gpu_parity.py). */
+int wl_debug_set_fix_cap(unsigned cap);
 
 const char* wl_last_error(void);
 

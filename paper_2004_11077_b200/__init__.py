@@ -11,7 +11,7 @@ from .layer import (BASE_MODES, QuantWinogradConv, WinogradAwareConv2d, conv2d_d
                     conv2d_winograd_quantized,
                     default_plan, winograd_conv2d)
 from .plan import (BaseChange, InterpolationPoints, Rational, WinogradPlan, build_base_change, build_plan,
-                   condition_number, monic_legendre, plan_to_float, poly_from_roots, stage_matrices)
+                   monic_legendre, plan_to_float, poly_from_roots, stage_matrices)
 from .quantize import STAGE_BITS, STAGE_ORDER, QuantConfig, QuantParams, StageStat
 
 __version__ = "0.1.0"
@@ -23,7 +23,7 @@ __all__ = [
     "default_plan",
     "winograd_conv2d",
     "BaseChange", "InterpolationPoints", "Rational", "WinogradPlan", "build_base_change", "build_plan",
-    "condition_number", "monic_legendre", "plan_to_float", "poly_from_roots", "stage_matrices",
+    "monic_legendre", "plan_to_float", "poly_from_roots", "stage_matrices",
     "STAGE_BITS", "STAGE_ORDER", "QuantConfig", "QuantParams", "StageStat",
     "CudaLayerError", "DimensionError", "InvalidPointsError", "__version__",
 ]

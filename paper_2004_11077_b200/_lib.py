@@ -13,8 +13,7 @@ import os
 from .errors import CudaLayerError, DimensionError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# WL_LIB_PATH selects an alternative build of the same library (measurement of kernel variants only)
-LIB_PATH = os.environ.get("WL_LIB_PATH") or os.path.join(_HERE, "libwinoleg_b200.so")
+LIB_PATH = os.path.join(_HERE, "libwinoleg_b200.so")
 
 WL_OK, WL_ERR_ARG, WL_ERR_PLAN, WL_ERR_BITS, WL_ERR_CUDA, WL_ERR_WORKSPACE = 0, -1, -2, -3, -4, -5
 WL_CANONICAL, WL_LEGENDRE = 0, 1
@@ -40,7 +39,8 @@ EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_mode", "wl_weight_cache
            "wl_weight_transform_f64", "wl_workspace_size", "wl_forward", "wl_forward_f64", "wl_num_stages", "wl_read_stats", "wl_debug_layout",
            "wl_forward_launches", "wl_profile_enable", "wl_profile_read", "wl_backward_workspace_size",
            "wl_backward", "wl_float_workspace_size", "wl_forward_float", "wl_direct_workspace_size",
-           "wl_direct_quantized", "wl_direct_quantized_f64", "wl_direct_f64", "wl_last_error")
+           "wl_direct_quantized", "wl_direct_quantized_f64", "wl_direct_f64", "wl_train_sizes", "wl_forward_train",
+           "wl_debug_set_fix_cap", "wl_last_error")
 
 
 def lib():
@@ -59,8 +59,13 @@ def lib():
     L.wl_plan_mode.argtypes = [VP]
     L.wl_weight_cache_size.argtypes = [VP, I, I, P(S)]
     L.wl_weight_transform.argtypes = [VP, P(wl_qcfg), VP, I, I, VP, S, VP]
+    L.wl_weight_transform_f64.argtypes = [VP, P(wl_qcfg), VP, I, I, VP, S, VP]
     L.wl_workspace_size.argtypes = [VP, P(wl_shape), P(wl_qcfg), P(S)]
     L.wl_forward.argtypes = [VP, P(wl_qcfg), P(wl_shape), VP, VP, VP, VP, VP, S, VP]
+    L.wl_forward_f64.argtypes = [VP, P(wl_qcfg), P(wl_shape), VP, VP, VP, VP, VP, S, VP]
+    L.wl_train_sizes.argtypes = [VP, P(wl_shape), P(wl_qcfg), P(S), P(S)]
+    L.wl_forward_train.argtypes = [VP, P(wl_qcfg), P(wl_shape), VP, VP, VP, VP, VP, S, VP, S, VP]
+    L.wl_debug_set_fix_cap.argtypes = [ctypes.c_uint]
     L.wl_num_stages.argtypes = [VP]
     L.wl_read_stats.argtypes = [VP, P(wl_shape), P(wl_qcfg), VP, VP, P(wl_stage_stat), VP]
     L.wl_debug_layout.argtypes = [VP, P(wl_shape), P(wl_qcfg), P(S), P(I)]

@@ -1,4 +1,4 @@
-// Host interface of the STE backward (wl_backward.cu), used by the C ABI in wl_forward.cu.
+// Host interface of the STE backward (wl_backward.cu), used by the C ABI in wl_abi.cu.
 #pragma once
 #include <cuda_runtime.h>
 

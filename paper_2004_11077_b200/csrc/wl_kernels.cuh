@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) quant_input_kernel(const XT* __restrict__
 #ifndef WL_QI_MINB
 #define WL_QI_MINB 4  // <= 64 registers: 4 row blocks per SM keep more loads in flight (0.89 -> 0.80 ms)
 #endif
-// One image row (h, n) of quant_input_w64: the body shared by the two-pass and the fused kernel.
+// One image row (h, n) of quant_input_w64.
 __device__ __forceinline__ void quant_row_w64(const float* __restrict__ x, int8_t* __restrict__ c0, const Geo& g,
                                               const StageQ& q, int h, int n, int8_t* srow) {
   const float rc = q.maxabs > 0.0 ? (float)((double)q.qmax / q.maxabs) : 0.f;
@@ -232,58 +232,13 @@ __device__ __forceinline__ void quant_row_w64(const float* __restrict__ x, int8_
   }
 }
 
+template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
 __global__ void __launch_bounds__(256, WL_QI_MINB) quant_input_w64_kernel(const float* __restrict__ x, int8_t* __restrict__ c0,
                                                               Geo g, Bits b, const Acc* __restrict__ acc) {
   extern __shared__ __align__(16) int8_t srow[];
   const int h = blockIdx.x, n = blockIdx.y;
   const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
   quant_row_w64(x, c0, g, q, h, n, srow);
-}
-
-// Fused cast "input" for per-image scale groups (fp32, W % 4 == 0, W <= 64), cooperative launch:
-// a team of `team` co-resident blocks takes one image at a time — every block reduces 1/team of the
-// image's max|x| (atomicMax), the team meets at a per-image counter, then the blocks quantise the
-// image's rows.  The second read of the image hits L2 (teams in flight x 3.2 MB << 126 MB), so x
-// crosses HBM once instead of twice (absmax_input + quant_input_w64).
-__global__ void __launch_bounds__(256, WL_QI_MINB) absquant_fused_kernel(const float* __restrict__ x,
-                                                                         int8_t* __restrict__ c0, Geo g, Bits b,
-                                                                         Acc* __restrict__ acc,
-                                                                         unsigned* __restrict__ arrive, int team) {
-  extern __shared__ __align__(16) int8_t srow[];
-  __shared__ unsigned long long wm[8];
-  const int nteams = gridDim.x / team, tm = blockIdx.x / team, k = blockIdx.x - tm * team;
-  if (tm >= nteams) return;
-  const long long per4 = (long long)g.C * g.H * g.W / 4;
-  const long long lo = per4 * k / team, hi = per4 * (k + 1) / team;
-  for (int n = tm; n < g.N; n += nteams) {
-    const float4* x4 = reinterpret_cast<const float4*>(x + (size_t)n * g.C * g.H * g.W);
-    unsigned long long m = 0;
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      const float4 v = __ldg(&x4[i]);
-      m = max(m, max(max(abs_bits(v.x), abs_bits(v.y)), max(abs_bits(v.z), abs_bits(v.w))));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
-    __syncthreads();
-    Acc* a = acc + (size_t)n * ST_COUNT + ST_INPUT;  // images_per_group == 1
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, wm[w]);
-      if (m) atomicMax(&a->M, max_to_f64_bits<float>(m));
-      __threadfence();
-      atomicAdd(&arrive[n], 1u);
-      while (*(volatile unsigned*)&arrive[n] < (unsigned)team) __nanosleep(64);
-      __threadfence();
-    }
-    __syncthreads();
-    Acc snap;
-    snap.M = __ldcg(&a->M);  // the team's final maximum (L2, not a stale L1 line)
-    const StageQ q = load_float_stage(snap, b.q[ST_INPUT]);
-    for (int h = k; h < g.H; h += team) {
-      quant_row_w64(x, c0, g, q, h, n, srow);
-      __syncthreads();
-    }
-  }
 }
 
 __device__ __forceinline__ void load_input_tile(const int8_t* __restrict__ c0, const Geo& g, int n, int tile, int c,
@@ -364,64 +319,6 @@ __device__ __forceinline__ void reduce36(const TT (&T)[6][6], int grp, bool acti
     atomicMax(&a[(size_t)grp * ST_COUNT].F, dbits(f));
   }
   publish_max(m, active ? grp : -1, a, ST_COUNT, uniform, wmax);
-}
-
-// Pass over (tile, channel) threads, channel fastest.  MODE 0 canonical / 1 Legendre.
-//   PASS 0: first input stage max (canonical input_transform | Legendre input_base_change)
-//   PASS 1: Legendre only — input_transform max from requantised base-change codes
-//   PASS 2: emit V codes
-template <int MODE, int PASS>
-__global__ void __launch_bounds__(256) input_stage_kernel(const int8_t* __restrict__ c0, int8_t* __restrict__ V, Geo g,
-                                                          Bits b, Acc* __restrict__ acc,
-                                                          const PlanF64* __restrict__ pf) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long total = (long long)g.T * g.C;
-  const bool active = idx < total;
-  const long long id = active ? idx : 0;
-  const int c = (int)(id % g.C);
-  const int t = (int)(id / g.C);
-  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
-  const int grp = group_of_image(n, g);
-  Acc* ga = acc + (size_t)grp * ST_COUNT;
-  int X[6][6];
-  load_input_tile(c0, g, n, tile, c, X);
-  const StageQ q0 = load_float_stage(ga[ST_INPUT], b.q[ST_INPUT]);
-  if constexpr (MODE == 0) {
-    int T1[6][6];
-    sandwich<tab::Can_IT>(X, T1);
-    if constexpr (PASS == 0) {
-      reduce36(T1, grp, active, acc, ST_IT, X, q0, pf->it, 6);
-    } else {
-      const StageQ q1 = load_int_stage(ga[ST_IT], b.q[ST_IT]);
-      int C1[6][6];
-      requant36(T1, q1, X, q0, pf->it, C1);
-      if (active)
-#pragma unroll
-        for (int e = 0; e < 36; ++e) V[((size_t)e * g.T + t) * g.Cp + c] = (int8_t)C1[e / 6][e % 6];
-    }
-  } else {
-    int T1[6][6];
-    sandwich<tab::Leg_IBC>(X, T1);
-    if constexpr (PASS == 0) {
-      reduce36(T1, grp, active, acc, ST_IBC, X, q0, pf->ibc, 6);
-    } else {
-      const StageQ q1 = load_int_stage(ga[ST_IBC], b.q[ST_IBC]);
-      int C1[6][6];
-      requant36(T1, q1, X, q0, pf->ibc, C1);
-      long long T2[6][6];
-      sandwich<tab::Leg_IT>(C1, T2);
-      if constexpr (PASS == 1) {
-        reduce36(T2, grp, active, acc, ST_IT, C1, q1, pf->it, 6);
-      } else {
-        const StageQ q2 = load_int_stage(ga[ST_IT], b.q[ST_IT]);
-        int C2[6][6];
-        requant36(T2, q2, C1, q1, pf->it, C2);
-        if (active)
-#pragma unroll
-          for (int e = 0; e < 36; ++e) V[((size_t)e * g.T + t) * g.Cp + c] = (int8_t)C2[e / 6][e % 6];
-      }
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------------- weight side
@@ -535,105 +432,6 @@ __device__ __forceinline__ long long absmax_crop(const TT (&Y)[4][4], int ty, in
       }
     }
   return m;
-}
-
-// Thread per (tile, out channel), channel fastest.
-//   canonical PASS 0: output max over Y = A^T h A (cropped); PASS 2: write y
-//   legendre  PASS 0: output_base_change max; PASS 1: output max; PASS 2: write y
-template <int MODE, int PASS, typename HT>
-__global__ void __launch_bounds__(256) output_stage_kernel(const HT* __restrict__ h, float* __restrict__ y,
-                                                           const float* __restrict__ bias, Geo g, Bits b,
-                                                           Acc* __restrict__ acc, const PlanF64* __restrict__ pf) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool active = idx < (long long)g.T * g.K;
-  const long long id = active ? idx : 0;
-  const int k = (int)(id % g.K);
-  const int t = (int)(id / g.K);
-  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
-  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
-  const int grp = group_of_image(n, g);
-  Acc* ga = acc + (size_t)grp * ST_COUNT;
-  int H0[6][6];
-  load_h(h, g, t, k, H0);
-  const StageQ qh = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
-  int Cf[6][6];  // codes feeding the final A-transform
-  StageQ qf;
-  const double* Lot = pf->ot;
-  if constexpr (MODE == 0) {
-#pragma unroll
-    for (int e = 0; e < 36; ++e) Cf[e / 6][e % 6] = H0[e / 6][e % 6];
-    qf = qh;
-  } else {
-    int T4[6][6];
-    sandwich<tab::Leg_OBC>(H0, T4);
-    if constexpr (PASS == 0) {
-      reduce36(T4, grp, active, acc, ST_OBC, H0, qh, pf->obc, 6);
-      return;
-    } else {
-      qf = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
-      requant36(T4, qf, H0, qh, pf->obc, Cf);
-    }
-  }
-  if constexpr (MODE == 1 && PASS == 0) return;
-  long long Y[4][4];
-  if constexpr (MODE == 0) {
-    int Yi[4][4];
-    sandwich<tab::Can_OT>(Cf, Yi);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) Y[e / 4][e % 4] = Yi[e / 4][e % 4];
-  } else {
-    sandwich<tab::Leg_OT>(Cf, Y);
-  }
-  constexpr bool kReduce = (MODE == 0 && PASS == 0) || (MODE == 1 && PASS == 1);
-  if constexpr (kReduce) {
-    const long long m = active ? absmax_crop(Y, ty, tx, g) : 0;
-    bool uniform;
-    long long wmax;
-    Acc* a = acc + ST_OUT;
-    if (replay_gate(m, active ? grp : -1, a, ST_COUNT, uniform, wmax)) {
-      int xc[36];
-#pragma unroll
-      for (int e = 0; e < 36; ++e) xc[e] = Cf[e / 6][e % 6];
-      double f = 0.0;
-      for (int e = 0; e < 16; ++e) {
-        const int i = e / 4, j = e % 4;
-        if (4 * ty + i >= g.Ho || 4 * tx + j >= g.Wo) continue;
-        long long v = Y[i][j];
-        if ((v < 0 ? -v : v) == m) f = fmax(f, fabs(replay_sandwich(Lot, 4, 6, xc, qf.qmax, qf.maxabs, qf.scale, i, j)));
-      }
-      atomicMax(&a[(size_t)grp * ST_COUNT].F, dbits(f));
-    }
-    publish_max(m, active ? grp : -1, a, ST_COUNT, uniform, wmax);
-  } else {
-    if (!active) return;
-    const StageQ qo = load_int_stage(ga[ST_OUT], b.q[ST_OUT]);
-    const float bk = bias ? __ldg(&bias[k]) : 0.f;
-    int xc[36];
-    bool have_xc = false;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = 4 * ty + i;
-      if (r >= g.Ho) continue;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = 4 * tx + j;
-        if (col >= g.Wo) continue;
-        bool tie = false;
-        int code = rq(Y[i][j], qo, tie);
-        if (tie) {
-          if (!have_xc) {
-            for (int e = 0; e < 36; ++e) xc[e] = Cf[e / 6][e % 6];
-            have_xc = true;
-          }
-          code = code_of(replay_sandwich(Lot, 4, 6, xc, qf.qmax, qf.maxabs, qf.scale, i, j), qo);
-        }
-        const double v = deq(code, qo.qmax, qo.maxabs, qo.scale);
-        float out = (float)v;
-        if (bias) out += bk;
-        y[(((size_t)n * g.K + k) * g.Ho + r) * g.Wo + col] = out;
-      }
-    }
-  }
 }
 
 }  // namespace wl

@@ -3,7 +3,7 @@
 //
 // Every stage value T is an integer.  The fast path evaluates T in fp32: the
 // first sandwich half is exact and the second rounds once per fma, so |T_f - T| <= E_stage
-// (host-computed, wl_forward.cu: stage_errors).  Hence
+// (host-computed, wl_abi.cu: stage_rowsums / stage_depth).  Hence
 //   * codes: y = fl(T_f * qmax/M + 1.5*2^23) is rhe(T_f * qmax/M); it equals the exact rhe() of
 //     the integer stage value unless T_f*qmax/M lies within qmax*E/M (+ fp32 slack) of a
 //     half-integer — those elements are recomputed in integers out of line (exact_elem), exact
@@ -319,6 +319,7 @@ __device__ __forceinline__ void fix_out_unit(const HT* __restrict__ h, const int
 }
 
 // r, threshold and reference scale of one stage for every group, once its M and F are final.
+template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
 __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage, int qmax, float rowsum, float depth) {
   const int gi = blockIdx.x * blockDim.x + threadIdx.x;
   if (gi >= groups) return;
@@ -337,6 +338,7 @@ __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage
 
 // Dequantised fp32 output of every code of the output stage, per group (quantize.py:120-125:
 // code * scale in fp64, +-qmax snapped to +-max_abs, then rounded to fp32): table[g][code + qmax].
+template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
 __global__ void out_table_kernel(const Acc* __restrict__ acc, int groups, int qmax, float* __restrict__ table) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int width = 2 * qmax + 1;
@@ -858,6 +860,7 @@ __global__ void __launch_bounds__(256) finalize_output_exec(const HT* __restrict
 // Hadamard: table[(xi*T + t)*nchunk + chunk] = exact max |I| over the row chunk (written by the GEMM
 // max epilogue).  Entries equal to the group maximum are recomputed on CUDA cores (lane per column)
 // and their maxima replayed in fp64.
+template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
 __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __restrict__ U, const int8_t* __restrict__ V, Geo g,
                                          Acc* __restrict__ acc, const Acc* __restrict__ wacc, int wstage, int qmax_u,
                                          int qmax_v, const unsigned* __restrict__ table, int bn) {
@@ -928,6 +931,7 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
 // One deferred unit per thread; the list length is read on the device (no host round trip).
 
 // Legendre input_base_change: exact c1 codes, then the unit's input_transform maximum.
+template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
 __global__ void __launch_bounds__(128) fixup_ibc_kernel(FixList fl, const int8_t* __restrict__ c0,
                                                         int8_t* __restrict__ c1, Geo g, Bits b, Acc* __restrict__ acc,
                                                         const PlanF64* __restrict__ pf, Tables tabs) {

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from .layer import QuantWinogradConv, conv2d_direct, conv2d_direct_quantized, conv2d_winograd
-from .plan import build_plan, condition_number, plan_to_float
+from .plan import build_plan, plan_to_float
 from .quantize import QuantConfig
 
 METRICS = ("max_abs_err", "rel_l2_err")
@@ -75,6 +75,18 @@ def _error_metrics(y: np.ndarray, ref: np.ndarray) -> tuple[float, float]:
     return max_abs, rel
 
 
+def _cond(mat, norm: str) -> float:
+    """Condition number for the report: sigma_max / sigma_min (two-norm; also the Frobenius fallback
+    for non-square factors), ||M||_F ||M^-1||_F for square factors; inf when numerically singular."""
+    m = np.asarray(mat, dtype=np.float64)
+    s = np.linalg.svd(m, compute_uv=False)
+    if s[-1] <= s[0] * max(m.shape) * np.finfo(np.float64).eps:
+        return float("inf")
+    if norm == "frobenius" and m.shape[0] == m.shape[1]:
+        return float(np.linalg.norm(m, "fro") * np.linalg.norm(np.linalg.inv(m), "fro"))
+    return float(s[0] / s[-1])
+
+
 def condition_table(plan) -> list[dict]:
     """harness.py:185-197: two-norm and Frobenius condition numbers of every pipeline factor."""
     plan = plan_to_float(plan)
@@ -82,7 +94,7 @@ def condition_table(plan) -> list[dict]:
     if plan.base_change is not None:
         mats += [("B_P^T", plan.B_P.T), ("G_P", plan.G_P), ("A_P^T", plan.A_P.T), ("P^T", plan.base_change.P.T),
                  ("P^-T", plan.base_change.P_inv.T)]
-    return [{"matrix": n, "two_norm": condition_number(m, "two"), "frobenius": condition_number(m, "frobenius")}
+    return [{"matrix": n, "two_norm": _cond(m, "two"), "frobenius": _cond(m, "frobenius")}
             for n, m in mats]
 
 

@@ -90,8 +90,9 @@ def qcfg_struct(q: QuantConfig) -> _lib.wl_qcfg:
     return _lib.wl_qcfg(*q.as_tuple())
 
 
-def _stream_ptr() -> ctypes.c_void_p:
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream_ptr(device=None) -> ctypes.c_void_p:
+    """The current stream of `device` (default: the current device) as the ABI's void* stream."""
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 class WeightCache:
@@ -114,9 +115,10 @@ class WeightCache:
             self.buf = torch.empty(nbytes.value, dtype=torch.uint8, device=w.device)
         qs = qcfg_struct(q)
         fn = _lib.lib().wl_weight_transform_f64 if w.dtype == torch.float64 else _lib.lib().wl_weight_transform
-        _lib.check(fn(
-            dplan.handle, ctypes.byref(qs), ctypes.c_void_p(w.data_ptr()), cout, cin,
-            ctypes.c_void_p(self.buf.data_ptr()), nbytes.value, _stream_ptr()), "wl_weight_transform")
+        with torch.cuda.device(w.device):
+            _lib.check(fn(
+                dplan.handle, ctypes.byref(qs), ctypes.c_void_p(w.data_ptr()), cout, cin,
+                ctypes.c_void_p(self.buf.data_ptr()), nbytes.value, _stream_ptr(w.device)), "wl_weight_transform")
         self.key = key
         self.w = w
         return self.buf
@@ -164,13 +166,27 @@ class QuantWinogradConv:
                                                  ctypes.byref(nbytes)), "wl_workspace_size")
         return nbytes.value
 
+    def train_sizes(self, shape) -> tuple[int, int]:
+        """(saved, workspace) bytes of wl_forward_train for this shape."""
+        sv, ws = ctypes.c_size_t(), ctypes.c_size_t()
+        qs = qcfg_struct(self.qconfig)
+        _lib.check(_lib.lib().wl_train_sizes(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs),
+                                              ctypes.byref(sv), ctypes.byref(ws)), "wl_train_sizes")
+        return sv.value, ws.value
+
     def forward(self, x: torch.Tensor, w: torch.Tensor, bias=None, padding: int = 0, scale_groups="image",
-                out: torch.Tensor | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+                out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                saved: torch.Tensor | None = None) -> torch.Tensor:
+        """One forward call.  With `saved` (a uint8 tensor of train_sizes()[0] bytes) the stage slots
+        and V codes the STE backward needs go there (wl_forward_train) and the workspace is only
+        scratch; otherwise everything lives in the workspace (wl_forward)."""
         _check_conv_args(x, w)
         if w.shape[2] != 3:
             raise DimensionError(f"plan is for k=3, weights have k={w.shape[2]}")
         if not (x.is_cuda and w.is_cuda):
             raise ValueError("x and w must be CUDA tensors")
+        if x.device != w.device or x.device != self.device:
+            raise ValueError(f"x ({x.device}) and w ({w.device}) must be on the runner's device {self.device}")
         # fp64 operands take the reference's own precision end to end (fp64 in, fp64 out); anything
         # else computes from fp32 (codes are exact for fp32-representable values either way).
         f64 = x.dtype == torch.float64
@@ -181,14 +197,23 @@ class QuantWinogradConv:
         ho, wo = shape.h + 2 * shape.pad - 2, shape.w + 2 * shape.pad - 2
         if ho < 1 or wo < 1:
             raise DimensionError(f"input {shape.h}x{shape.w} (pad {shape.pad}) is smaller than the 3x3 kernel")
+        if saved is not None and f64:
+            raise ValueError("the training forward (saved=...) takes fp32 operands")
         cache = self.wcache.get(self.dplan, self.qconfig, w)
-        nbytes = self.workspace_bytes(shape)
+        if saved is not None:
+            sv_bytes, nbytes = self.train_sizes(shape)
+            if saved.numel() < sv_bytes:
+                raise ValueError(f"saved needs {sv_bytes} bytes")
+        else:
+            nbytes = self.workspace_bytes(shape)
         if workspace is not None:
             if workspace.numel() < nbytes:
                 raise ValueError(f"workspace needs {nbytes} bytes")
-            self.ws = workspace
-        elif self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
-            self.ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+            ws = workspace
+        else:
+            if self.ws is None or self.ws.numel() < nbytes or self.ws.device != x.device:
+                self.ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+            ws = self.ws
         if out is None:
             out = torch.empty((shape.n, shape.c_out, ho, wo), dtype=ydt, device=x.device)
         elif out.dtype != ydt or not out.is_contiguous() or tuple(out.shape) != (shape.n, shape.c_out, ho, wo):
@@ -198,14 +223,39 @@ class QuantWinogradConv:
             if bias.shape != (shape.c_out,):
                 raise DimensionError(f"bias must be [{shape.c_out}], got {tuple(bias.shape)}")
         qs = qcfg_struct(self.qconfig)
-        fwd = _lib.lib().wl_forward_f64 if f64 else _lib.lib().wl_forward
-        _lib.check(fwd(
-            self.dplan.handle, ctypes.byref(qs), ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()),
-            ctypes.c_void_p(cache.data_ptr()), ctypes.c_void_p(bias.data_ptr() if bias is not None else 0),
-            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
-            _stream_ptr()), "wl_forward")
-        self._last = (shape, cache)
+        bptr = ctypes.c_void_p(bias.data_ptr() if bias is not None else 0)
+        with torch.cuda.device(x.device):
+            if saved is not None:
+                _lib.check(_lib.lib().wl_forward_train(
+                    self.dplan.handle, ctypes.byref(qs), ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()),
+                    ctypes.c_void_p(cache.data_ptr()), bptr, ctypes.c_void_p(out.data_ptr()),
+                    ctypes.c_void_p(saved.data_ptr()), saved.numel(), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                    _stream_ptr(x.device)), "wl_forward_train")
+            else:
+                fwd = _lib.lib().wl_forward_f64 if f64 else _lib.lib().wl_forward
+                _lib.check(fwd(
+                    self.dplan.handle, ctypes.byref(qs), ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()),
+                    ctypes.c_void_p(cache.data_ptr()), bptr, ctypes.c_void_p(out.data_ptr()),
+                    ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(x.device)), "wl_forward")
+        # stats / debug views read the buffer holding the stage slots (saved block or workspace)
+        self._last = (shape, cache, saved if saved is not None else ws, saved is None)
         return out
+
+    def capture(self, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, bias=None, padding: int = 0,
+                scale_groups="image"):
+        """CUDA-graph the forward on fixed buffers (x, w, out) and return its replay function.
+
+        The launch-bound shapes (configs 1-3: 20-30 dependent kernels of a few microseconds each,
+        SURVEY H7) pay the host launch path once at capture; replays re-run the same kernels on the
+        current contents of x (w must not change: its weight transform is cached before capture)."""
+        self.forward(x, w, bias=bias, padding=padding, scale_groups=scale_groups, out=out)  # caches, attributes
+        torch.cuda.synchronize(x.device)
+        ws = self.ws
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.forward(x, w, bias=bias, padding=padding, scale_groups=scale_groups, out=out, workspace=ws)
+        self._graph_keep = (g, ws)
+        return g.replay
 
     def forward_host(self, xh: torch.Tensor, w: torch.Tensor, yh: torch.Tensor, bias=None, padding: int = 0,
                      chunks: int = 8) -> torch.Tensor:
@@ -232,6 +282,9 @@ class QuantWinogradConv:
                            torch.empty((mx,) + tuple(yh.shape[1:]), dtype=xdt, device=dev), None) for _ in range(2)]
             self._pool_ws = [None, None]
             self._pool_key = (tuple(xh.shape), tuple(yh.shape), chunks, xdt)
+        # a previous call may still be reading the pooled buffers on `cur` / copying them out on s_out
+        s_in.wait_stream(cur)
+        cur.wait_stream(s_out)
         ev_in = [torch.cuda.Event() for _ in range(chunks)]
         ev_comp = [torch.cuda.Event() for _ in range(chunks)]
         ev_out = [torch.cuda.Event() for _ in range(chunks)]
@@ -267,7 +320,8 @@ class QuantWinogradConv:
         return self._aux_streams
 
     def backward(self, dy: torch.Tensor, shape, cache: torch.Tensor, fwd_ws: torch.Tensor, need_bias: bool):
-        """STE gradients (dx, dw, db) of the forward that used `fwd_ws` (C ABI wl_backward)."""
+        """STE gradients (dx, dw, db) of the forward whose saved block (or whole workspace) is `fwd_ws`
+        (C ABI wl_backward)."""
         dy = dy.contiguous().float()
         qs = qcfg_struct(self.qconfig)
         nbytes = ctypes.c_size_t()
@@ -277,44 +331,46 @@ class QuantWinogradConv:
         dx = torch.empty((shape.n, shape.c_in, shape.h, shape.w), dtype=torch.float32, device=dy.device)
         dw = torch.empty((shape.c_out, shape.c_in, 3, 3), dtype=torch.float32, device=dy.device)
         db = torch.empty((shape.c_out,), dtype=torch.float32, device=dy.device) if need_bias else None
-        _lib.check(_lib.lib().wl_backward(
-            self.dplan.handle, ctypes.byref(qs), ctypes.byref(shape), ctypes.c_void_p(dy.data_ptr()),
-            ctypes.c_void_p(cache.data_ptr()), ctypes.c_void_p(fwd_ws.data_ptr()), ctypes.c_void_p(dx.data_ptr()),
-            ctypes.c_void_p(dw.data_ptr()), ctypes.c_void_p(db.data_ptr() if db is not None else 0),
-            ctypes.c_void_p(bws.data_ptr()), nbytes.value, _stream_ptr()), "wl_backward")
+        with torch.cuda.device(dy.device):
+            _lib.check(_lib.lib().wl_backward(
+                self.dplan.handle, ctypes.byref(qs), ctypes.byref(shape), ctypes.c_void_p(dy.data_ptr()),
+                ctypes.c_void_p(cache.data_ptr()), ctypes.c_void_p(fwd_ws.data_ptr()), ctypes.c_void_p(dx.data_ptr()),
+                ctypes.c_void_p(dw.data_ptr()), ctypes.c_void_p(db.data_ptr() if db is not None else 0),
+                ctypes.c_void_p(bws.data_ptr()), nbytes.value, _stream_ptr(dy.device)), "wl_backward")
         return dx, dw, db
 
     def stats(self):
         """StageStat rows of the last forward (synchronises the stream)."""
-        shape, cache = self._last
+        shape, cache, accbuf, _ = self._last
         ns = _lib.lib().wl_num_stages(self.dplan.handle)
         groups = shape.n // shape.images_per_group
         arr = (_lib.wl_stage_stat * (groups * ns))()
         qs = qcfg_struct(self.qconfig)
         _lib.check(_lib.lib().wl_read_stats(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs),
                                             ctypes.c_void_p(cache.data_ptr()),
-                                            ctypes.c_void_p(self.ws.data_ptr()), arr, _stream_ptr()),
+                                            ctypes.c_void_p(accbuf.data_ptr()), arr, _stream_ptr(accbuf.device)),
                    "wl_read_stats")
         names = STAGE_ORDER[self.mode]
         return [[StageStat(names[i], arr[g * ns + i].bits, arr[g * ns + i].max_abs, arr[g * ns + i].scale)
                  for i in range(ns)] for g in range(groups)]
 
     def launches(self) -> int:
-        shape, _ = self._last
+        shape = self._last[0]
         qs = qcfg_struct(self.qconfig)
         return int(_lib.lib().wl_forward_launches(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs)))
 
     def debug_views(self):
         """Views of the materialised codes of the last call in logical layouts:
         c0 [N,H,W,C], V [36,T,C], h [36,T,K], U [36,K,C] (storage is [T][36][Cp] etc.)."""
-        shape, cache = self._last
+        shape, cache, ws, whole = self._last
+        if not whole:
+            raise ValueError("debug_views needs a wl_forward call (not the training forward)")
         off = (ctypes.c_size_t * 4)()
         dims = (ctypes.c_int * 4)()
         qs = qcfg_struct(self.qconfig)
         _lib.check(_lib.lib().wl_debug_layout(self.dplan.handle, ctypes.byref(shape), ctypes.byref(qs), off, dims),
                    "wl_debug_layout")
         Cp, Kp, T, _ = dims[0], dims[1], dims[2], dims[3]
-        ws = self.ws
         c0 = ws[off[0]: off[0] + shape.n * shape.h * shape.w * Cp].view(torch.int8).view(shape.n, shape.h, shape.w, Cp)
         V = ws[off[1]: off[1] + 36 * T * Cp].view(torch.int8).view(T, 36, Cp).permute(1, 0, 2)
         hb = 2 if self.qconfig.hadamard_bits > 8 else 1
@@ -330,13 +386,16 @@ class _QuantWinogradFn(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, w, bias, runner: QuantWinogradConv, padding: int, scale_groups: str):
-        shape = runner._shape(x, w, padding, scale_groups)
-        ws = torch.empty(runner.workspace_bytes(shape), dtype=torch.uint8, device=x.device)
-        y = runner.forward(x, w, bias=bias, padding=padding, scale_groups=scale_groups, workspace=ws)
-        shape_, cache = runner._last
+        xf = x if x.dtype == torch.float32 else x.float()
+        shape = runner._shape(xf, w, padding, scale_groups)
+        sv_bytes, _ = runner.train_sizes(shape)
+        # only the stage slots + V codes outlive the call; the scratch workspace is the runner's own
+        saved = torch.empty(sv_bytes, dtype=torch.uint8, device=x.device)
+        y = runner.forward(xf, w, bias=bias, padding=padding, scale_groups=scale_groups, saved=saved)
+        shape_, cache = runner._last[0], runner._last[1]
         ctx.runner, ctx.shape, ctx.has_bias = runner, shape_, bias is not None
         ctx.dtypes = (x.dtype, w.dtype, bias.dtype if bias is not None else None)
-        ctx.save_for_backward(ws, cache)
+        ctx.save_for_backward(saved, cache)
         return y
 
     @staticmethod
@@ -456,10 +515,11 @@ def conv2d_winograd(x, w, plan: WinogradPlan, mode: str = "canonical", padding: 
                "wl_float_workspace_size")
     ws = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
     y = torch.empty((n, cout, ho, wo), dtype=torch.float32, device=dev)
-    _lib.check(_lib.lib().wl_forward_float(
-        dplan.handle, ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
-        ctypes.c_void_p(bias.data_ptr() if bias is not None else 0), ctypes.c_void_p(y.data_ptr()),
-        ctypes.c_void_p(ws.data_ptr()), nbytes.value, _stream_ptr()), "wl_forward_float")
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().wl_forward_float(
+            dplan.handle, ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+            ctypes.c_void_p(bias.data_ptr() if bias is not None else 0), ctypes.c_void_p(y.data_ptr()),
+            ctypes.c_void_p(ws.data_ptr()), nbytes.value, _stream_ptr(dev)), "wl_forward_float")
     if single:
         y = y[0]
     return y.cpu().numpy() if as_numpy else y
@@ -504,9 +564,10 @@ def conv2d_direct_quantized(x, w, qconfig: QuantConfig | None = None, padding: i
     ws = torch.empty(nbytes.value, dtype=torch.uint8, device=x.device)
     y = torch.empty((n, cout, ho, wo), dtype=dt, device=x.device)
     fn = _lib.lib().wl_direct_quantized_f64 if f64 else _lib.lib().wl_direct_quantized
-    _lib.check(fn(ctypes.byref(qcfg_struct(qconfig)), ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()),
-                  ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
-                  nbytes.value, _stream_ptr()), "wl_direct_quantized")
+    with torch.cuda.device(x.device):
+        _lib.check(fn(ctypes.byref(qcfg_struct(qconfig)), ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()),
+                      ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                      nbytes.value, _stream_ptr(x.device)), "wl_direct_quantized")
     if single:
         y = y[0]
     return y.cpu().numpy() if as_numpy else y
@@ -536,9 +597,10 @@ def conv2d_direct(x, w, padding: int = 0):
     _lib.check(_lib.lib().wl_direct_workspace_size(ctypes.byref(shape), ctypes.byref(nbytes)), "wl_direct_workspace_size")
     ws = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
     y = torch.empty((n, cout, ho, wo), dtype=torch.float64, device=dev)
-    _lib.check(_lib.lib().wl_direct_f64(ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
-                                        ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()), nbytes.value,
-                                        _stream_ptr()), "wl_direct_f64")
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().wl_direct_f64(ctypes.byref(shape), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                            ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(ws.data_ptr()), nbytes.value,
+                                            _stream_ptr(dev)), "wl_direct_f64")
     if single:
         y = y[0]
     return y.cpu().numpy() if as_numpy else y

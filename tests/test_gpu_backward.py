@@ -70,3 +70,72 @@ def test_module_training_step_runs_and_learns():
         opt.step()
         losses.append(float(loss.detach()))
     assert all(np.isfinite(losses)) and losses[-1] < losses[0]
+
+
+def _deq_t(codes, qmax, maxabs, scale):
+    """Dequantised value as the reference holds it after fake_quant (quantize.py:120-125)."""
+    c = codes.double()
+    v = c * scale
+    v = torch.where(c == qmax, torch.full_like(v, maxabs), v)
+    return torch.where(c == -qmax, torch.full_like(v, -maxabs), v)
+
+
+def _ste_torch(dy, U, V, h, w, pad):
+    """ste_formula (oracle/backward_ref.py) in torch fp64 on the device: dy [n,K,Ho,Wo], U [K,C,6,6],
+    V [n,C,TP,6,6] dequantised -> (dx, dw, db)."""
+    A = torch.tensor(BR.A, dtype=torch.float64, device=dy.device)
+    BT = torch.tensor(BR.BT, dtype=torch.float64, device=dy.device)
+    G = torch.tensor(BR.G, dtype=torch.float64, device=dy.device)
+    n, K, ho, wo = dy.shape
+    C = U.shape[1]
+    th, tw = -(-ho // 4), -(-wo // 4)
+    dyp = torch.zeros((n, K, th * 4, tw * 4), dtype=torch.float64, device=dy.device)
+    dyp[:, :, :ho, :wo] = dy
+    tiles = dyp.reshape(n, K, th, 4, tw, 4).permute(0, 1, 2, 4, 3, 5).reshape(n, K, th * tw, 4, 4)
+    dM = torch.einsum("ia,nktab,jb->nktij", A, tiles, A)
+    dV = torch.einsum("kcij,nktij->nctij", U, dM)
+    dU = torch.einsum("nctij,nktij->kcij", V, dM)
+    dXt = torch.einsum("ai,nctab,bj->nctij", BT, dV, BT)
+    hp, wp = (th - 1) * 4 + 6, (tw - 1) * 4 + 6
+    dxp = torch.zeros((n, C, max(hp, h + 2 * pad), max(wp, w + 2 * pad)), dtype=torch.float64, device=dy.device)
+    for ty in range(th):
+        for tx in range(tw):
+            dxp[:, :, 4 * ty:4 * ty + 6, 4 * tx:4 * tx + 6] += dXt[:, :, ty * tw + tx]
+    dx = dxp[:, :, pad:pad + h, pad:pad + w]
+    dw = torch.einsum("ap,kcab,bq->kcpq", G, dU, G)
+    return dx, dw, dy.sum(dim=(0, 2, 3))
+
+
+@pytest.mark.parametrize("mode", ["legendre", "canonical"])
+@pytest.mark.parametrize("c,hw", [(64, 32), (128, 16), (256, 8), (512, 4)])
+def test_backward_config3_full_batch_dx_dw_db(mode, c, hw):
+    """Config 3 at its full batch (N=256, every ResNet-18 3x3 shape): dx, dw and db against the fp64
+    closed form over ALL images.  The quantised operands are the layer's own U / V codes and stage
+    scales (their bit-exactness against the reference is tests/test_gpu_parity.py's job)."""
+    n, pad = 256, 1
+    rng = np.random.default_rng(c + hw)
+    x = np.maximum(rng.standard_normal((n, c, hw, hw)), 0).astype(np.float32)
+    w = (rng.standard_normal((c, c, 3, 3)) * np.sqrt(2 / (9 * c))).astype(np.float32)
+    dy = rng.standard_normal((n, c, hw, hw)).astype(np.float32)
+    qc = W.QuantConfig.uniform(8)
+    y, dx, dw, db = run(x, w, dy, mode, qc, pad)
+    r = W.QuantWinogradConv(PLAN, mode, qc)
+    y2 = r.forward(torch.tensor(x, device="cuda"), torch.tensor(w, device="cuda"), padding=pad)
+    assert torch.equal(y, y2)
+    views, st = r.debug_views(), r.stats()
+    names = [s.stage for s in st[0]]
+    wi, vi = names.index("weight_base_change" if mode == "legendre" else "weight_transform"), names.index("input_transform")
+    su, qmax = st[0][wi], 127
+    U = _deq_t(views["U"], qmax, su.max_abs, su.scale).permute(1, 2, 0).reshape(c, c, 6, 6)
+    TP = views["V"].shape[1] // n
+    Vc = views["V"].reshape(36, n, TP, c)
+    vmax = torch.tensor([s[vi].max_abs for s in st], dtype=torch.float64, device="cuda")[None, :, None, None]
+    vsc = torch.tensor([s[vi].scale for s in st], dtype=torch.float64, device="cuda")[None, :, None, None]
+    cd = Vc.double()
+    Vd = torch.where(cd == qmax, vmax.expand_as(cd), torch.where(cd == -qmax, -vmax.expand_as(cd), cd * vsc))
+    V = Vd.permute(1, 3, 2, 0).reshape(n, c, TP, 6, 6)
+    dx_r, dw_r, db_r = (t.cpu().numpy() for t in _ste_torch(torch.tensor(dy, dtype=torch.float64, device="cuda"),
+                                                             U, V, hw, hw, pad))
+    assert rel(dx, dx_r) <= TOL
+    assert rel(dw, dw_r) <= TOL
+    assert rel(db, db_r) <= TOL
