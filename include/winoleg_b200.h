@@ -148,6 +148,13 @@ int wl_forward_launches(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q
 int wl_profile_enable(int on);
 int wl_profile_read(const char** names_out, double* ms_out, int max, int* n_out, int* calls_out);
 
+/* Test hook: the split-bf16 tcgen05 GEMM behind the STE backward and the float path, on device
+ * buffers: D[s][b][m][n] (row stride ldd) = alpha * sum_{k in split s} A[b][m][k] B[b][n][k] with
+ * A bf16 [PA][batch][M][Kd], B bf16 [PB][batch][N][Kd] (planes summed: x = hi + mid + lo), Kd and ks
+ * multiples of 64, splits = ceil(Kd / ks); plane products (i, j) with i + j < max(PA, PB). */
+int wl_debug_gemm_bf16(const void* A, int PA, const void* B, int PB, int batch, int M, int N, int Kd, int ks,
+                       float* D, int ldd, float alpha, void* stream);
+
 /* Test hook: capacity of the deferred exact-fix lists (0 = automatic, the default).  A tiny cap forces
  * every producer onto its inline fallback; results must not change (tests/test_gpu_parity.py). */
 int wl_debug_set_fix_cap(unsigned cap);

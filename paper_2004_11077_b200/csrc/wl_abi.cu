@@ -15,6 +15,7 @@
 #include "wl_backward.h"
 #include "wl_direct.h"
 #include "wl_float.h"
+#include "wl_gemm_bf16.h"
 #include "wl_internal.h"
 
 namespace wl {
@@ -422,6 +423,14 @@ int wl_profile_read(const char** names_out, double* ms_out, int max, int* n_out,
   if (calls_out) *calls_out = (int)g_prof.calls.size();
   g_prof.calls.clear();
   g_prof.cur = nullptr;
+  return WL_OK;
+}
+
+int wl_debug_gemm_bf16(const void* A, int PA, const void* B, int PB, int batch, int M, int N, int Kd, int ks,
+                       float* D, int ldd, float alpha, void* stream) {
+  if (!A || !B || !D) return fail(WL_ERR_ARG, "NULL argument");
+  cudaError_t e = gemm_bf16_split(A, PA, B, PB, batch, M, N, Kd, ks, D, ldd, alpha, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(WL_ERR_CUDA, "gemm_bf16_split: %s", cudaGetErrorString(e));
   return WL_OK;
 }
 

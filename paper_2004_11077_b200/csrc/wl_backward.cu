@@ -4,20 +4,26 @@
 // times their stage scale), and — since every Legendre composite equals the canonical transform in
 // exact arithmetic (pipeline.py:9-11: P^-1 A_P = A, P^-1 B_P = B, P^-1 G_P = G) — both bases use
 //   dM  = A . dY . A^T                       (6x6 per (tile, out channel))
-//   dV  = sum_k U_k (.) dM_k,  dU = sum_t V_t (.) dM_t   (36 batched fp32 GEMMs, cuBLAS)
+//   dV  = sum_k U_k (.) dM_k,  dU = sum_t V_t (.) dM_t   (two 36-way batched GEMMs on tcgen05)
 //   dX  = col2im( B . dV . B^T )             (gather over the <= 2x2 tiles covering a pixel)
 //   dW  = G^T . dU . G,   db = sum dY
-// Transform / gather kernels are hand written; the batched GEMMs are plain library GEMMs.
-#include <cublas_v2.h>
+// GEMMs (gemm_bf16.cuh): the codes are exact in bf16, dM is carried as three bf16 planes
+// (hi + mid + lo == fp32), fp32 accumulation in TMEM.  dV = dM . U^T over K (one pass);
+// dU^T = V^T . (s_v dM) over the tiles, split into <= 4096-tile chunks whose partial sums are
+// added in fp64 by the dW kernel.  The per-image V scale s_v is folded into dM's planes, the
+// weight scale s_u into the dX transform.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
-#include <mutex>
 #include <string>
 
 #include "../../include/winoleg_b200.h"
+#include "gemm_bf16.cuh"
 #include "wl_backward.h"
+#include "wl_gemm_bf16.h"
 
 namespace wl {
 namespace bw {
@@ -26,18 +32,21 @@ namespace bw {
 __constant__ float kAT[4][6] = {{1, 1, 1, 1, 1, 0}, {0, 1, -1, 2, -2, 0}, {0, 1, 1, 4, 4, 0}, {0, 1, -1, 8, -8, 1}};
 __constant__ float kBT[6][6] = {{4, 0, -5, 0, 1, 0},  {0, -4, -4, 1, 1, 0}, {0, 4, -4, -1, 1, 0},
                                 {0, -2, -1, 2, 1, 0}, {0, 2, -1, -2, 1, 0}, {0, 4, 0, -5, 0, 1}};
-__constant__ float kG[6][3] = {{0.25f, 0, 0},
-                               {-1.f / 6, -1.f / 6, -1.f / 6},
-                               {-1.f / 6, 1.f / 6, -1.f / 6},
-                               {1.f / 24, 1.f / 12, 1.f / 6},
-                               {1.f / 24, -1.f / 12, 1.f / 6},
-                               {0, 0, 1}};
+__constant__ double kG[6][3] = {{0.25, 0, 0},
+                                {-1.0 / 6, -1.0 / 6, -1.0 / 6},
+                                {-1.0 / 6, 1.0 / 6, -1.0 / 6},
+                                {1.0 / 24, 1.0 / 12, 1.0 / 6},
+                                {1.0 / 24, -1.0 / 12, 1.0 / 6},
+                                {0, 0, 1}};
 
-// dM[e][t][k] = (A . dY_tile . A^T)[e], dY cropped to the valid output (pad-to-tile spill is zero).
-__global__ void dm_kernel(const float* __restrict__ dy, float* __restrict__ dm, BwGeo g) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)g.T * g.K) return;
-  const int k = (int)(idx % g.K), t = (int)(idx / g.K);
+struct Work {  // workspace carve-up (wl_bw_workspace_bytes)
+  __nv_bfloat16 *dmA, *dmB, *ut, *vt;
+  float *dv, *dup, *dxt;
+  int Kpad, Tpad, S, ks;
+};
+
+// dM of tile t, output channel k: A . dY_tile . A^T, dY cropped to the valid output.
+__device__ __forceinline__ void dm_tile(const float* __restrict__ dy, const BwGeo& g, int t, int k, float (&out)[36]) {
   const int n = t / g.TP, tile = t % g.TP, ty = tile / g.tw, tx = tile % g.tw;
   float Y[4][4];
 #pragma unroll
@@ -64,37 +73,97 @@ __global__ void dm_kernel(const float* __restrict__ dy, float* __restrict__ dm, 
       float s = 0.f;
 #pragma unroll
       for (int a = 0; a < 4; ++a) s = fmaf(kAT[a][i], tmp[a][j], s);
-      dm[((size_t)(6 * i + j) * g.T + t) * g.K + k] = s;
+      out[6 * i + j] = s;
     }
 }
 
-// Dequantised GEMM operands: U [36][K][C] and V [36][T][C] fp32 from the int8 codes.
-__global__ void deq_u_kernel(const int8_t* __restrict__ ucodes, float* __restrict__ ud, BwGeo g,
-                             const Acc* __restrict__ wacc, int wstage, int qmax_u) {
+// GEMM operand of dV: dM planes [3][36][T][Kpad] (k fastest: coalesced plane stores), zero padded.
+__global__ void dm_rows_kernel(const float* __restrict__ dy, __nv_bfloat16* __restrict__ dmA, BwGeo g, int Kpad) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= 36LL * g.K * g.C) return;
-  const double su = load_int_stage(wacc[wstage], qmax_u).scale;
-  const int c = (int)(idx % g.C);
-  const long long r = idx / g.C;
-  const int k = (int)(r % g.K), e = (int)(r / g.K);
-  ud[idx] = (float)((double)ucodes[((size_t)k * 36 + e) * g.Cp + c] * su);
-}
-__global__ void deq_v_kernel(const int8_t* __restrict__ vcodes, float* __restrict__ vd, BwGeo g,
-                             const Acc* __restrict__ acc) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= 36LL * g.T * g.C) return;
-  const int c = (int)(idx % g.C);
-  const long long r = idx / g.C;
-  const int t = (int)(r % g.T), e = (int)(r / g.T);
-  const int grp = (t / g.TP) / g.ipg;
-  vd[idx] = (float)((double)vcodes[((size_t)t * 36 + e) * g.Cp + c] * acc[(size_t)grp * ST_COUNT + ST_IT].scale);
+  if (idx >= (long long)g.T * Kpad) return;
+  const int k = (int)(idx % Kpad), t = (int)(idx / Kpad);
+  float m[36];
+  if (k < g.K) {
+    dm_tile(dy, g, t, k, m);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 36; ++e) m[e] = 0.f;
+  }
+  const size_t plane = (size_t)36 * g.T * Kpad;
+#pragma unroll
+  for (int e = 0; e < 36; ++e) {
+    __nv_bfloat16 h, md, l;
+    wl_split3(m[e], h, md, l);
+    const size_t o = ((size_t)e * g.T + t) * Kpad + k;
+    dmA[o] = h;
+    dmA[plane + o] = md;
+    dmA[2 * plane + o] = l;
+  }
 }
 
-// dXt[t][c][36] = B . dV_tile . B^T (dV gathered from [36][T][C]).
-__global__ void dxt_kernel(const float* __restrict__ dv, float* __restrict__ dxt, BwGeo g) {
+// GEMM operand of dU^T: s_v(t) * dM as planes [3][36][K][Tpad] (t fastest), zero padded.
+__global__ void dm_cols_kernel(const float* __restrict__ dy, __nv_bfloat16* __restrict__ dmB, BwGeo g, int Tpad,
+                               const Acc* __restrict__ acc) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)Tpad * g.K) return;
+  const int t = (int)(idx % Tpad), k = (int)(idx / Tpad);
+  float m[36];
+  if (t < g.T) {
+    dm_tile(dy, g, t, k, m);
+    const float sv = (float)acc[(size_t)((t / g.TP) / g.ipg) * ST_COUNT + ST_IT].scale;
+#pragma unroll
+    for (int e = 0; e < 36; ++e) m[e] *= sv;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 36; ++e) m[e] = 0.f;
+  }
+  const size_t plane = (size_t)36 * g.K * Tpad;
+#pragma unroll
+  for (int e = 0; e < 36; ++e) {
+    __nv_bfloat16 h, md, l;
+    wl_split3(m[e], h, md, l);
+    const size_t o = ((size_t)e * g.K + k) * Tpad + t;
+    dmB[o] = h;
+    dmB[plane + o] = md;
+    dmB[2 * plane + o] = l;
+  }
+}
+
+// U codes [Kp][36][Cp] -> bf16 [36][C][Kpad] (exact), zero padded.
+__global__ void ut_kernel(const int8_t* __restrict__ ucodes, __nv_bfloat16* __restrict__ ut, BwGeo g, int Kpad) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= 36LL * g.C * Kpad) return;
+  const int k = (int)(idx % Kpad);
+  const long long r = idx / Kpad;
+  const int c = (int)(r % g.C), e = (int)(r / g.C);
+  ut[idx] = __float2bfloat16_rn(k < g.K ? (float)ucodes[((size_t)k * 36 + e) * g.Cp + c] : 0.f);
+}
+
+// V codes [T][36][Cp] -> bf16 [36][C][Tpad] (exact), a 64 x 64 shared-memory transpose per block.
+__global__ void __launch_bounds__(256) vt_kernel(const int8_t* __restrict__ vcodes, __nv_bfloat16* __restrict__ vt,
+                                                 BwGeo g, int Tpad) {
+  __shared__ int8_t sm[64][65];
+  const int t0 = blockIdx.x * 64, c0 = blockIdx.y * 64, e = blockIdx.z;
+  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
+    const int tt = i >> 6, cc = i & 63;
+    const int t = t0 + tt, c = c0 + cc;
+    sm[cc][tt] = (t < g.T && c < g.C) ? vcodes[((size_t)t * 36 + e) * g.Cp + c] : (int8_t)0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
+    const int cc = i >> 6, tt = i & 63;
+    const int c = c0 + cc;
+    if (c < g.C) vt[((size_t)e * g.C + c) * Tpad + t0 + tt] = __float2bfloat16_rn((float)sm[cc][tt]);
+  }
+}
+
+// dXt = s_u * B . dV_tile . B^T, dV [36][T][C] -> dxt [T][36][C] (c fastest: coalesced both ways).
+__global__ void dxt_kernel(const float* __restrict__ dv, float* __restrict__ dxt, BwGeo g, const Acc* __restrict__ wacc,
+                           int wstage, int qmax_u) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= (long long)g.T * g.C) return;
   const int c = (int)(idx % g.C), t = (int)(idx / g.C);
+  const float su = (float)load_int_stage(wacc[wstage], qmax_u).scale;
   float D[6][6];
 #pragma unroll
   for (int e = 0; e < 36; ++e) D[e / 6][e % 6] = __ldg(&dv[((size_t)e * g.T + t) * g.C + c]);
@@ -108,7 +177,6 @@ __global__ void dxt_kernel(const float* __restrict__ dv, float* __restrict__ dxt
       for (int b = 0; b < 6; ++b) s = fmaf(D[a][b], kBT[b][j], s);
       tmp[a][j] = s;
     }
-  float* out = dxt + idx * 36;
 #pragma unroll
   for (int i = 0; i < 6; ++i)
 #pragma unroll
@@ -116,146 +184,171 @@ __global__ void dxt_kernel(const float* __restrict__ dv, float* __restrict__ dxt
       float s = 0.f;
 #pragma unroll
       for (int a = 0; a < 6; ++a) s = fmaf(kBT[a][i], tmp[a][j], s);
-      out[6 * i + j] = s;
+      dxt[((size_t)t * 36 + 6 * i + j) * g.C + c] = su * s;
     }
 }
 
 // Gather col2im: each input pixel sums the <= 2x2 tile contributions covering it (no atomics).
-__global__ void dx_gather_kernel(const float* __restrict__ dxt, float* __restrict__ dx, BwGeo g) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)g.N * g.C * g.H * g.W) return;
-  const int col = (int)(idx % g.W);
-  long long r_ = idx / g.W;
-  const int row = (int)(r_ % g.H);
-  r_ /= g.H;
-  const int c = (int)(r_ % g.C), n = (int)(r_ / g.C);
-  const int rp = row + g.pad, cp = col + g.pad;
-  float s = 0.f;
-  for (int ty = max(0, (rp - 2) / 4); ty <= min(g.th - 1, rp / 4); ++ty) {
-    const int i = rp - 4 * ty;
-    if (i < 0 || i > 5) continue;
-    for (int tx = max(0, (cp - 2) / 4); tx <= min(g.tw - 1, cp / 4); ++tx) {
-      const int j = cp - 4 * tx;
-      if (j < 0 || j > 5) continue;
-      const int t = n * g.TP + ty * g.tw + tx;
-      s += __ldg(&dxt[((size_t)t * g.C + c) * 36 + 6 * i + j]);
+// Block = (image n, input row, 32 columns, 32 channels): the sums are formed with channels across
+// lanes (coalesced dxt reads) and leave through shared memory with columns across lanes
+// (coalesced dx rows).
+__global__ void __launch_bounds__(256) dx_gather_kernel(const float* __restrict__ dxt, float* __restrict__ dx, BwGeo g) {
+  __shared__ float sm[32][33];
+  const int n = blockIdx.x / g.H, row = blockIdx.x % g.H;
+  const int col0 = blockIdx.y * 32, c0 = blockIdx.z * 32;
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int rp = row + g.pad;
+  {
+    const int c = c0 + lane;
+    for (int cl = grp; cl < 32; cl += 8) {
+      const int col = col0 + cl;
+      float s = 0.f;
+      if (c < g.C && col < g.W) {
+        const int cp = col + g.pad;
+        for (int ty = max(0, (rp - 2) / 4); ty <= min(g.th - 1, rp / 4); ++ty) {
+          const int i = rp - 4 * ty;
+          if (i < 0 || i > 5) continue;
+          for (int tx = max(0, (cp - 2) / 4); tx <= min(g.tw - 1, cp / 4); ++tx) {
+            const int j = cp - 4 * tx;
+            if (j < 0 || j > 5) continue;
+            const int t = n * g.TP + ty * g.tw + tx;
+            s += __ldg(&dxt[((size_t)t * 36 + 6 * i + j) * g.C + c]);
+          }
+        }
+      }
+      sm[cl][lane] = s;
     }
   }
-  dx[idx] = s;
+  __syncthreads();
+  for (int cl = grp; cl < 32; cl += 8) {
+    const int c = c0 + cl, col = col0 + lane;
+    if (c < g.C && col < g.W) dx[(((size_t)n * g.C + c) * g.H + row) * g.W + col] = sm[lane][cl];
+  }
 }
 
-// dW[k][c] = G^T . dU . G with dU[e][c][k] from the batched GEMM.
-__global__ void dw_kernel(const float* __restrict__ du, float* __restrict__ dw, BwGeo g) {
+// dW[k][c] = G^T . dU . G with dU^T[e][c][k] summed over the S split partials in fp64.
+__global__ void dw_kernel(const float* __restrict__ dup, float* __restrict__ dw, BwGeo g, int S) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= g.K * g.C) return;
-  const int c = idx % g.C, k = idx / g.C;
-  float D[6][6];
+  const int k = idx % g.K, c = idx / g.K;  // k fastest: coalesced partial reads
+  double D[6][6];
 #pragma unroll
-  for (int e = 0; e < 36; ++e) D[e / 6][e % 6] = du[((size_t)e * g.C + c) * g.K + k];
-  float tmp[6][3];  // dU . G
+  for (int e = 0; e < 36; ++e) {
+    double s = 0.0;
+    for (int sp = 0; sp < S; ++sp) s += (double)__ldg(&dup[(((size_t)sp * 36 + e) * g.C + c) * g.K + k]);
+    D[e / 6][e % 6] = s;
+  }
+  double tmp[6][3];  // dU . G
 #pragma unroll
   for (int a = 0; a < 6; ++a)
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      float s = 0.f;
+      double s = 0.0;
 #pragma unroll
-      for (int b = 0; b < 6; ++b) s = fmaf(D[a][b], kG[b][q], s);
+      for (int b = 0; b < 6; ++b) s += D[a][b] * kG[b][q];
       tmp[a][q] = s;
     }
+  float* out = dw + ((size_t)k * g.C + c) * 9;
 #pragma unroll
   for (int p = 0; p < 3; ++p)
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      float s = 0.f;
+      double s = 0.0;
 #pragma unroll
-      for (int a = 0; a < 6; ++a) s = fmaf(kG[a][p], tmp[a][q], s);
-      dw[(size_t)idx * 9 + 3 * p + q] = s;
+      for (int a = 0; a < 6; ++a) s += kG[a][p] * tmp[a][q];
+      out[3 * p + q] = (float)s;
     }
 }
 
 __global__ void db_kernel(const float* __restrict__ dy, float* __restrict__ db, BwGeo g) {
   const int k = blockIdx.x;
-  float s = 0.f;
+  double s = 0.0;
   const long long per = (long long)g.Ho * g.Wo;
   for (long long i = threadIdx.x; i < (long long)g.N * per; i += blockDim.x) {
     const long long n = i / per, p = i % per;
     s += dy[((size_t)n * g.K + k) * per + p];
   }
-  __shared__ float red[32];
+  __shared__ double red[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
   if (threadIdx.x < 32) {
-    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) db[k] = s;
+    if (threadIdx.x == 0) db[k] = (float)s;
   }
+}
+
+size_t a256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// dU^T reduction split over the tiles: chunks of <= 4096 tiles (fp32 accumulation length), and
+// enough (batch x tile x split) CTAs for two waves.
+void splits(const BwGeo& g, int Tpad, int* S, int* ks) {
+  const int tiles = 36 * ((g.C + 127) / 128) * ((g.K + 255) / 256);
+  int s = std::max((Tpad + 4095) / 4096, (296 + tiles - 1) / tiles);
+  s = std::min(s, Tpad / 64);
+  s = std::max(s, 1);
+  *ks = round_up((Tpad + s - 1) / s, 64);
+  *S = (Tpad + *ks - 1) / *ks;
+}
+
+size_t carve(const BwGeo& g, void* ws, Work* w) {
+  const size_t T = g.T, C = g.C, K = g.K;
+  const int Kpad = round_up(g.K, 64), Tpad = round_up(g.T, 64);
+  int S, ks;
+  splits(g, Tpad, &S, &ks);
+  uint8_t* p = reinterpret_cast<uint8_t*>(ws);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* q = p ? p + o : nullptr;
+    o += a256(bytes);
+    return q;
+  };
+  Work W;
+  W.dmA = reinterpret_cast<__nv_bfloat16*>(take(3 * 36 * T * Kpad * 2));
+  W.dmB = reinterpret_cast<__nv_bfloat16*>(take(3 * 36 * K * (size_t)Tpad * 2));
+  W.ut = reinterpret_cast<__nv_bfloat16*>(take(36 * C * (size_t)Kpad * 2));
+  W.vt = reinterpret_cast<__nv_bfloat16*>(take(36 * C * (size_t)Tpad * 2));
+  W.dv = reinterpret_cast<float*>(take(36 * T * C * 4));
+  W.dup = reinterpret_cast<float*>(take((size_t)S * 36 * C * K * 4));
+  W.dxt = reinterpret_cast<float*>(take(36 * T * C * 4));
+  W.Kpad = Kpad, W.Tpad = Tpad, W.S = S, W.ks = ks;
+  if (w) *w = W;
+  return o;
 }
 
 }  // namespace bw
 }  // namespace wl
 
+using namespace wl;
 using namespace wl::bw;
 
-namespace {
-std::mutex g_cublas_mu;
-cublasHandle_t cublas_for_device() {
-  static cublasHandle_t handles[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_cublas_mu);
-  if (!handles[dev]) cublasCreate(&handles[dev]);
-  return handles[dev];
-}
-size_t a256(size_t v) { return (v + 255) & ~size_t(255); }
-}  // namespace
-
-size_t wl_bw_workspace_bytes(const BwGeo& g) {
-  const size_t T = g.T, C = g.C, K = g.K;
-  return a256(36 * T * K * 4) + a256(36 * K * C * 4) + a256(36 * T * C * 4) + a256(36 * T * C * 4) +
-         a256(36 * C * K * 4);
-}
+size_t wl_bw_workspace_bytes(const BwGeo& g) { return carve(g, nullptr, nullptr); }
 
 int wl_bw_run(const BwGeo& g, const float* dy, const int8_t* ucodes, const wl::Acc* wacc, int wstage, int qmax_u,
               const int8_t* vcodes, const wl::Acc* acc, float* dx, float* dw, float* db, void* ws, cudaStream_t st,
               std::string* err) {
-  const size_t T = g.T, C = g.C, K = g.K;
-  uint8_t* p = reinterpret_cast<uint8_t*>(ws);
-  float* dm = reinterpret_cast<float*>(p);
-  p += a256(36 * T * K * 4);
-  float* ud = reinterpret_cast<float*>(p);
-  p += a256(36 * K * C * 4);
-  float* vd = reinterpret_cast<float*>(p);
-  p += a256(36 * T * C * 4);
-  float* dv = reinterpret_cast<float*>(p);
-  p += a256(36 * T * C * 4);
-  float* du = reinterpret_cast<float*>(p);
+  Work W;
+  carve(g, ws, &W);
   const int tb = 256;
-  dm_kernel<<<(unsigned)((T * K + tb - 1) / tb), tb, 0, st>>>(dy, dm, g);
-  deq_u_kernel<<<(unsigned)((36 * K * C + tb - 1) / tb), tb, 0, st>>>(ucodes, ud, g, wacc, wstage, qmax_u);
-  deq_v_kernel<<<(unsigned)((36 * T * C + tb - 1) / tb), tb, 0, st>>>(vcodes, vd, g, acc);
-  cublasHandle_t h = cublas_for_device();
-  cublasSetStream(h, st);
-  const float one = 1.f, zero = 0.f;
-  // dV_e [T x C] = dM_e [T x K] . U_e [K x C]   (row-major; column-major view: dV^T = U^T . dM^T)
-  cublasStatus_t s1 = cublasSgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)C, (int)T, (int)K, &one, ud,
-                                                (int)C, (long long)K * C, dm, (int)K, (long long)T * K, &zero, dv,
-                                                (int)C, (long long)T * C, 36);
-  // dU_e [C x K] = V_e^T [C x T] . dM_e [T x K]  (column-major result dU^T [K x C] = dM^T . V)
-  cublasStatus_t s2 = cublasSgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)K, (int)C, (int)T, &one, dm,
-                                                (int)K, (long long)T * K, vd, (int)C, (long long)T * C, &zero, du,
-                                                (int)K, (long long)C * K, 36);
-  if (s1 != CUBLAS_STATUS_SUCCESS || s2 != CUBLAS_STATUS_SUCCESS) {
-    *err = "cublasSgemmStridedBatched failed";
+  const long long T = g.T, C = g.C, K = g.K;
+  dm_rows_kernel<<<(unsigned)((T * W.Kpad + tb - 1) / tb), tb, 0, st>>>(dy, W.dmA, g, W.Kpad);
+  dm_cols_kernel<<<(unsigned)(((long long)W.Tpad * K + tb - 1) / tb), tb, 0, st>>>(dy, W.dmB, g, W.Tpad, acc);
+  ut_kernel<<<(unsigned)((36 * C * W.Kpad + tb - 1) / tb), tb, 0, st>>>(ucodes, W.ut, g, W.Kpad);
+  vt_kernel<<<dim3(W.Tpad / 64, (unsigned)((C + 63) / 64), 36), 256, 0, st>>>(vcodes, W.vt, g, W.Tpad);
+  // dV[e] (T x C) = dM[e] (T x K) . U[e]^T      (s_u applied in dxt_kernel)
+  cudaError_t e1 = gemm_bf16_split(W.dmA, 3, W.ut, 1, 36, g.T, g.C, W.Kpad, W.Kpad, W.dv, g.C, 1.f, st);
+  // dU^T[e] (C x K) = V[e]^T (C x T) . (s_v dM)[e] (T x K), split over the tiles
+  cudaError_t e2 = gemm_bf16_split(W.vt, 1, W.dmB, 3, 36, g.C, g.K, W.Tpad, W.ks, W.dup, g.K, 1.f, st);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    *err = std::string("tcgen05 backward GEMM launch: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2);
     return WL_ERR_CUDA;
   }
-  // dX: tile transforms into vd (no longer needed), then the gather
-  float* dxt = vd;
-  dxt_kernel<<<(unsigned)((T * C + tb - 1) / tb), tb, 0, st>>>(dv, dxt, g);
-  dx_gather_kernel<<<(unsigned)(((size_t)g.N * C * g.H * g.W + tb - 1) / tb), tb, 0, st>>>(dxt, dx, g);
-  dw_kernel<<<(unsigned)((K * C + tb - 1) / tb), tb, 0, st>>>(du, dw, g);
+  dxt_kernel<<<(unsigned)((T * C + tb - 1) / tb), tb, 0, st>>>(W.dv, W.dxt, g, wacc, wstage, qmax_u);
+  dx_gather_kernel<<<dim3((unsigned)(g.N * g.H), (g.W + 31) / 32, (unsigned)((C + 31) / 32)), 256, 0, st>>>(W.dxt, dx, g);
+  dw_kernel<<<(unsigned)((K * C + tb - 1) / tb), tb, 0, st>>>(W.dup, dw, g, W.S);
   if (db) db_kernel<<<(unsigned)K, 256, 0, st>>>(dy, db, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -4,18 +4,21 @@
 // L . X . L^T with the plan's nearest-double matrices (construct.py:191-208) rounded to fp32:
 //   canonical: U = G w G^T,                      V = B^T d B,                   Y = A^T M A
 //   legendre:  U = P^-1 (G_P w G_P^T) P^-T,       V = B_P^T (P^-T d P^-1) B_P,   Y = A_P^T (P^-T M P^-1) A_P
-//   M[xi] = sum_c U[xi] (.) V[xi]  (36 batched fp32 GEMMs, cuBLAS: plain library GEMMs).
+//   M[xi] = sum_c U[xi] (.) V[xi]  (36 batched GEMMs on tcgen05, gemm_bf16.cuh: U and V carried as
+//   three bf16 planes each, the six plane products with i + j <= 2 give fp32-accurate products,
+//   fp32 accumulation in TMEM).
 // Same batch / padding / crop conventions as the quantized layer (wl_forward).  Kernels: one
 // weight transform (thread per (out, in) channel pair), one input transform (thread per (tile,
 // channel), channel fastest: V stores coalesce), one output transform (thread per (tile, out
 // channel)), all in fp32 with the reference's sandwich order (tmp = X . R first, then L . tmp).
-#include <cublas_v2.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
-#include <mutex>
 #include <string>
 
+#include "gemm_bf16.cuh"
 #include "wl_float.h"
+#include "wl_gemm_bf16.h"
 
 namespace wl {
 namespace fl32 {
@@ -60,15 +63,30 @@ __global__ void mats_kernel(const wl::PlanF64* __restrict__ pf, Mats* __restrict
   if (i < 24) m->ot[i] = (float)pf->ot[i];
 }
 
-// U[xi][k][c] (row-major [K][C] per xi)
-__global__ void weight_kernel(const float* __restrict__ w, float* __restrict__ U, const Mats* __restrict__ mp, FGeo g,
-                              int legendre) {
+// three bf16 planes of v at P[o], P[o + plane], P[o + 2 plane]
+__device__ __forceinline__ void put3(__nv_bfloat16* __restrict__ P, size_t plane, size_t o, float v) {
+  __nv_bfloat16 h, m, l;
+  wl_split3(v, h, m, l);
+  P[o] = h;
+  P[plane + o] = m;
+  P[2 * plane + o] = l;
+}
+
+// U planes [3][36][K][Cpad] (zero padded channels)
+__global__ void weight_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ U, const Mats* __restrict__ mp,
+                              FGeo g, int legendre, int Cpad) {
   __shared__ Mats m;
   if (threadIdx.x < sizeof(Mats) / 4) reinterpret_cast<float*>(&m)[threadIdx.x] = reinterpret_cast<const float*>(mp)[threadIdx.x];
   __syncthreads();
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)g.K * g.C) return;
-  const int c = (int)(idx % g.C), k = (int)(idx / g.C);
+  if (idx >= (long long)g.K * Cpad) return;
+  const int c = (int)(idx % Cpad), k = (int)(idx / Cpad);
+  const size_t plane = (size_t)36 * g.K * Cpad;
+  if (c >= g.C) {
+#pragma unroll
+    for (int e = 0; e < 36; ++e) put3(U, plane, ((size_t)e * g.K + k) * Cpad + c, 0.f);
+    return;
+  }
   float X[3][3];
 #pragma unroll
   for (int e = 0; e < 9; ++e) X[e / 3][e % 3] = __ldg(&w[((size_t)k * g.C + c) * 9 + e]);
@@ -81,18 +99,24 @@ __global__ void weight_kernel(const float* __restrict__ w, float* __restrict__ U
     for (int e = 0; e < 36; ++e) u[e / 6][e % 6] = v[e / 6][e % 6];
   }
 #pragma unroll
-  for (int e = 0; e < 36; ++e) U[((size_t)e * g.K + k) * g.C + c] = u[e / 6][e % 6];
+  for (int e = 0; e < 36; ++e) put3(U, plane, ((size_t)e * g.K + k) * Cpad + c, u[e / 6][e % 6]);
 }
 
-// V[xi][t][c] (row-major [T][C] per xi) from the zero-padded NCHW input
-__global__ void input_kernel(const float* __restrict__ x, float* __restrict__ V, const Mats* __restrict__ mp, FGeo g,
-                             int legendre) {
+// V planes [3][36][T][Cpad] from the zero-padded NCHW input
+__global__ void input_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ V, const Mats* __restrict__ mp,
+                             FGeo g, int legendre, int Cpad) {
   __shared__ Mats m;
   if (threadIdx.x < sizeof(Mats) / 4) reinterpret_cast<float*>(&m)[threadIdx.x] = reinterpret_cast<const float*>(mp)[threadIdx.x];
   __syncthreads();
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)g.T * g.C) return;
-  const int c = (int)(idx % g.C), t = (int)(idx / g.C);
+  if (idx >= (long long)g.T * Cpad) return;
+  const int c = (int)(idx % Cpad), t = (int)(idx / Cpad);
+  const size_t plane = (size_t)36 * g.T * Cpad;
+  if (c >= g.C) {
+#pragma unroll
+    for (int e = 0; e < 36; ++e) put3(V, plane, ((size_t)e * g.T + t) * Cpad + c, 0.f);
+    return;
+  }
   const int n = t / g.TP, tile = t % g.TP, ty = tile / g.tw, tx = tile % g.tw;
   float X[6][6];
 #pragma unroll
@@ -111,7 +135,7 @@ __global__ void input_kernel(const float* __restrict__ x, float* __restrict__ V,
     sandwich_f<6, 6>(m.it, X, v);
   }
 #pragma unroll
-  for (int e = 0; e < 36; ++e) V[((size_t)e * g.T + t) * g.C + c] = v[e / 6][e % 6];
+  for (int e = 0; e < 36; ++e) put3(V, plane, ((size_t)e * g.T + t) * Cpad + c, v[e / 6][e % 6]);
 }
 
 // y (cropped NCHW) from M[xi][t][k] (row-major [T][K] per xi)
@@ -150,50 +174,30 @@ __global__ void output_kernel(const float* __restrict__ M, const float* __restri
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 size_t wl_float_workspace_bytes(const FGeo& g) {
-  return align256(sizeof(fl32::Mats)) + align256((size_t)36 * g.K * g.C * 4) + align256((size_t)36 * g.T * g.C * 4) +
-         align256((size_t)36 * g.T * g.K * 4);
-}
-
-// one handle per device, fp32 "pedantic" math (the backward's handle keeps the default mode)
-static cublasHandle_t float_cublas_for_device() {
-  static cublasHandle_t handles[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!handles[dev] && cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
-  return handles[dev];
+  const size_t Cpad = round_up(g.C, 64);
+  return align256(sizeof(fl32::Mats)) + align256(3 * 36 * (size_t)g.K * Cpad * 2) +
+         align256(3 * 36 * (size_t)g.T * Cpad * 2) + align256((size_t)36 * g.T * g.K * 4);
 }
 
 int wl_float_run(int legendre, const PlanF64* d_pf, const FGeo& g, const float* x, const float* w, const float* bias,
                  float* y, void* ws, cudaStream_t st, std::string* err) {
+  const int Cpad = round_up(g.C, 64);
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
   fl32::Mats* mats = reinterpret_cast<fl32::Mats*>(p);
   p += align256(sizeof(fl32::Mats));
-  float* U = reinterpret_cast<float*>(p);
-  p += align256((size_t)36 * g.K * g.C * 4);
-  float* V = reinterpret_cast<float*>(p);
-  p += align256((size_t)36 * g.T * g.C * 4);
+  __nv_bfloat16* U = reinterpret_cast<__nv_bfloat16*>(p);
+  p += align256(3 * 36 * (size_t)g.K * Cpad * 2);
+  __nv_bfloat16* V = reinterpret_cast<__nv_bfloat16*>(p);
+  p += align256(3 * 36 * (size_t)g.T * Cpad * 2);
   float* M = reinterpret_cast<float*>(p);
   fl32::mats_kernel<<<1, 64, 0, st>>>(d_pf, mats);
   const int tb = 256;
-  fl32::weight_kernel<<<(unsigned)(((long long)g.K * g.C + tb - 1) / tb), tb, 0, st>>>(w, U, mats, g, legendre);
-  fl32::input_kernel<<<(unsigned)(((long long)g.T * g.C + tb - 1) / tb), tb, 0, st>>>(x, V, mats, g, legendre);
-  cublasHandle_t h = float_cublas_for_device();
-  if (!h) {
-    *err = "cublasCreate failed";
-    return -1;
-  }
-  cublasSetStream(h, st);
-  cublasSetMathMode(h, CUBLAS_PEDANTIC_MATH);  // true fp32 FMA products (no tf32 / bf16x3 emulation)
-  const float one = 1.f, zero = 0.f;
-  // column-major view: M_xi (K x T) = U_xi^T (K x C) . V_xi (C x T)
-  cublasStatus_t s = cublasSgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, g.K, g.T, g.C, &one, U, g.C,
-                                               (long long)g.K * g.C, V, g.C, (long long)g.T * g.C, &zero, M, g.K,
-                                               (long long)g.T * g.K, 36);
-  if (s != CUBLAS_STATUS_SUCCESS) {
-    *err = "cublasSgemmStridedBatched failed";
+  fl32::weight_kernel<<<(unsigned)(((long long)g.K * Cpad + tb - 1) / tb), tb, 0, st>>>(w, U, mats, g, legendre, Cpad);
+  fl32::input_kernel<<<(unsigned)(((long long)g.T * Cpad + tb - 1) / tb), tb, 0, st>>>(x, V, mats, g, legendre, Cpad);
+  // M[xi] (T x K) = V[xi] (T x C) . U[xi]^T (C x K): fp32-accurate products from 3 x 3 bf16 planes
+  cudaError_t ge = gemm_bf16_split(V, 3, U, 3, 36, g.T, g.K, Cpad, Cpad, M, g.K, 1.f, st);
+  if (ge != cudaSuccess) {
+    *err = std::string("tcgen05 float GEMM launch: ") + cudaGetErrorString(ge);
     return -1;
   }
   fl32::output_kernel<<<(unsigned)(((long long)g.T * g.K + tb - 1) / tb), tb, 0, st>>>(M, bias, y, mats, g, legendre);
