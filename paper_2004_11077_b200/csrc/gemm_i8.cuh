@@ -308,3 +308,166 @@ __global__ void __launch_bounds__(EpiShape<Epi::kGroups>::kThreads, 1)
 }
 
 }  // namespace wl
+
+namespace wl {
+
+// ----------------------------------------------------------------------------------------------
+// B-stationary variant: every CTA owns one B tile (Winograd element xi, output-channel block nb) —
+// U_xi's BN x Cpad codes stay resident in shared memory (one TMA load) — and walks a contiguous range
+// of m-blocks of that xi, so only the A operand (V) streams through the ring: 1/3 of the persistent
+// kernel's shared-memory fill per tile for Cpad = Kout = 256.  The nslots CTAs sharing a B tile split
+// its m-blocks into contiguous ranges (measured: 0.59 ms vs 0.62 ms with round-robin m-blocks on
+// config 4).  grid >= 36 * nblocks always (ntiles = 36 * nblocks * mblocks).  Same epilogue contract
+// and TMEM double buffering as gemm_i8_persistent.  Used for the max pass (0.58 -> 0.49 ms kernel on
+// config 4); the requantisation pass is epilogue-bound and measured slower with it (1.12 -> 1.21 ms).
+template <int BN, int SW, int STAGES, int EPI_STAGE, int EPI_WARPS>
+struct GemmBSmem {
+  static constexpr int kA = 128 * SW;
+  static constexpr int kEpi = EPI_WARPS * EPI_STAGE;
+  static constexpr int bytes(int kblocks) { return 1024 + kblocks * BN * SW + STAGES * kA + kEpi + 512; }
+};
+
+template <int BN, int SW, int STAGES, class Epi>
+__global__ void __launch_bounds__(EpiShape<Epi::kGroups>::kThreads, 1)
+    gemm_i8_bstat(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int T, int Kout,
+                  int Cpad, int Kpad, Epi epi) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kEpiGroups = Epi::kGroups, kEpiWarps = 4 * kEpiGroups;
+  using L = GemmBSmem<BN, SW, STAGES, Epi::kStageBytes, kEpiWarps>;
+  const int kblocks = Cpad / SW;
+  uint8_t* sB = smem;                          // [kblocks][BN rows][SW bytes]
+  uint8_t* sA = sB + kblocks * BN * SW;        // ring [STAGES][128 rows][SW bytes]
+  uint8_t* sEpi = sA + STAGES * L::kA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + L::kEpi);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accfull = empty + STAGES;  // [2]
+  uint64_t* accempty = accfull + 2;    // [2]
+  uint64_t* bfull = accempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mblocks = (T + 127) / 128, nblocks = Kpad / BN, nkeys = 36 * nblocks;
+  const int key = (int)blockIdx.x % nkeys, slot = (int)blockIdx.x / nkeys;
+  const int nslots = ((int)gridDim.x - key + nkeys - 1) / nkeys;
+  const int mb0 = (int)((long long)slot * mblocks / nslots), mb1 = (int)((long long)(slot + 1) * mblocks / nslots);
+  constexpr int mstep = 1;
+  const int xi = key % 36, nb = key / 36;
+  constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&accfull[a], 1);
+      mbar_init(&accempty[a], kEpiWarps);
+    }
+    mbar_init(bfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(bfull, (uint32_t)(kblocks * BN * SW));
+      for (int kb = 0; kb < kblocks; ++kb) tma_load_3d(sB + kb * BN * SW, &tmB, bfull, kb * SW, xi, nb * BN);
+      int it = 0;
+      for (int mb = mb0; mb < mb1; mb += mstep)
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], L::kA);
+          tma_load_3d(sA + s * L::kA, &tmA, &full[s], kb * SW, xi, mb * 128);
+        }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_i8(128, BN);
+      mbar_wait(bfull, 0);
+      tc_fence_after();
+      int it = 0, local = 0;
+      for (int mb = mb0; mb < mb1; mb += mstep, ++local) {
+        const int a = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        mbar_wait(&accempty[a], aph ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem_base + (uint32_t)(a * BN);
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < SW / 32; ++k) {
+            const uint64_t ad = smem_desc_kmajor(sA + s * L::kA + k * 32, SW);
+            const uint64_t bd = smem_desc_kmajor(sB + kb * BN * SW + k * 32, SW);
+            umma_i8(dacc, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&accfull[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    constexpr int HC = BN / kEpiGroups;
+    static_assert(HC % 16 == 0, "epilogue column group must be a multiple of 16");
+    if constexpr (Epi::kStageBytes > 0) epi.set_stage(sEpi + ew * Epi::kStageBytes, HC);
+    constexpr bool kPre = Epi::kPrefetch;
+    if constexpr (kPre) {
+      if (mb0 < mb1) epi.prefetch(mb0 * 128 + 32 * q + lane, mb0 * 128 + 32 * q + lane < T);
+    }
+    int local = 0;
+    const int n0 = nb * BN + half * HC;
+    for (int mb = mb0; mb < mb1; mb += mstep, ++local) {
+      const int a = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      const int row = mb * 128 + 32 * q + lane;
+      epi.begin(xi, row, row < T);
+      if constexpr (kPre) {
+        const int mn = mb + mstep;
+        if (mn < mb1) epi.prefetch(mn * 128 + 32 * q + lane, mn * 128 + 32 * q + lane < T);
+      }
+      mbar_wait(&accfull[a], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + (uint32_t)(a * BN + half * HC);
+#pragma unroll 1
+      for (int c = 0; c < HC; c += 32) {
+        uint32_t r0[16], r1[16];
+        tmem_ld16(taddr + c, r0);
+        if (c + 16 < HC) tmem_ld16(taddr + c + 16, r1);
+        tmem_ld_wait();
+        const int col = n0 + c;
+        const int nv0 = Kout - col, nv1 = Kout - col - 16;
+        if (row < T && nv0 > 0) epi.apply(xi, row, col, r0, nv0 > 16 ? 16 : nv0);
+        if (c + 16 < HC && row < T && nv1 > 0) epi.apply(xi, row, col + 16, r1, nv1 > 16 ? 16 : nv1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty[a]);
+      epi.finish_chunk(xi, row, row < T, nb * kEpiGroups + half);
+      if constexpr (Epi::kStageBytes > 0) epi.flush(xi, mb * 128 + 32 * q, n0, HC, T, lane);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace wl

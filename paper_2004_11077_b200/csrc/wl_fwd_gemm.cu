@@ -258,12 +258,32 @@ __global__ void __launch_bounds__(128) fixup_had_kernel(FixList fl, const int8_t
 
 template <int BN, int SW, class Epi>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Geo& g, const Epi& e, cudaStream_t st) {
+  const int ntiles = 36 * ((g.T + 127) / 128) * (g.Kp / BN);
+  const int grid = std::min(ntiles, num_sms());
+  const int kblocks = g.Cp / SW;
+  constexpr int kMaxSmem = 227 * 1024;
+  // max pass: B-stationary schedule when U's tile (kblocks x BN x SW bytes) fits next to a 2..4-deep A
+  // ring (the requantisation pass is epilogue-bound: it keeps the persistent tile order, gemm_i8.cuh)
+  auto bstat = [&](auto stages) -> int {
+    constexpr int S = decltype(stages)::value;
+    using LB = GemmBSmem<BN, SW, S, Epi::kStageBytes, 4 * Epi::kGroups>;
+    auto kern = gemm_i8_bstat<BN, SW, S, Epi>;
+    const int smem = LB::bytes(kblocks);
+    WL_CUDA(ensure_smem_attr(reinterpret_cast<const void*>(kern), smem));
+    kern<<<grid, EpiShape<Epi::kGroups>::kThreads, smem, st>>>(ta, tb, g.T, g.K, g.Cp, g.Kp, e);
+    WL_CUDA(cudaGetLastError());
+    return WL_OK;
+  };
+  if (Epi::kStageBytes == 0 && grid >= 36 * (g.Kp / BN)) {
+    if (GemmBSmem<BN, SW, 4, Epi::kStageBytes, 4 * Epi::kGroups>::bytes(kblocks) <= kMaxSmem)
+      return bstat(std::integral_constant<int, 4>{});
+    if (GemmBSmem<BN, SW, 2, Epi::kStageBytes, 4 * Epi::kGroups>::bytes(kblocks) <= kMaxSmem)
+      return bstat(std::integral_constant<int, 2>{});
+  }
   constexpr int STAGES = Epi::kStageBytes > 0 ? 3 : 4;
   using L = GemmPSmem<BN, SW, STAGES, Epi::kStageBytes, 4 * Epi::kGroups>;
   auto kern = gemm_i8_persistent<BN, SW, STAGES, Epi>;
   WL_CUDA(ensure_smem_attr(reinterpret_cast<const void*>(kern), L::kBytes));
-  const int ntiles = 36 * ((g.T + 127) / 128) * (g.Kp / BN);
-  const int grid = std::min(ntiles, num_sms());
   kern<<<grid, EpiShape<Epi::kGroups>::kThreads, L::kBytes, st>>>(ta, tb, g.T, g.K, g.Cp, g.Kp, e);
   WL_CUDA(cudaGetLastError());
   return WL_OK;
