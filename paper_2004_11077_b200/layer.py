@@ -258,16 +258,18 @@ class QuantWinogradConv:
         return g.replay
 
     def forward_host(self, xh: torch.Tensor, w: torch.Tensor, yh: torch.Tensor, bias=None, padding: int = 0,
-                     chunks: int = 8) -> torch.Tensor:
+                     chunks: int = 16, depth: int = 3) -> torch.Tensor:
         """End-to-end call on HOST buffers (pinned for overlap): x [N,C,H,W] -> y [N,K,Ho,Wo] in place.
 
-        With per-image scale groups the batch splits exactly into independent chunks, so the copy
-        in of chunk i+1, the forward of chunk i and the copy out of chunk i-1 overlap on three
-        streams (per-chunk workspaces, shared weight cache)."""
+        With per-image scale groups the batch splits exactly into independent chunks, so the copy in
+        of chunk i+1, the forward of chunk i and the copy out of chunk i-1 overlap on three streams
+        (`depth` rotating device buffer slots, one workspace: the forwards are serialised on the
+        current stream).  The run is PCIe bound; more chunks shorten the pipeline fill and drain."""
         if xh.is_cuda or yh.is_cuda:
             raise ValueError("forward_host takes host tensors")
         n = xh.shape[0]
         chunks = max(1, min(chunks, n))
+        depth = max(2, depth)
         dev = w.device
         w = w.contiguous() if w.dtype == torch.float64 else w.contiguous().float()  # the object forward() caches
         xdt = torch.float64 if xh.dtype == torch.float64 else torch.float32
@@ -276,12 +278,15 @@ class QuantWinogradConv:
         s_in, s_out = self._streams(dev)
         if yh.dtype != xdt:
             raise ValueError(f"yh must be {xdt} for {xh.dtype} input")
-        if not hasattr(self, "_pool") or self._pool_key != (tuple(xh.shape), tuple(yh.shape), chunks, xdt):
+        key = (tuple(xh.shape), tuple(yh.shape), chunks, depth, xdt)
+        if getattr(self, "_pool_key", None) != key:
+            self._pool = None
             mx = max(bounds[i + 1] - bounds[i] for i in range(chunks))
             self._pool = [(torch.empty((mx,) + tuple(xh.shape[1:]), dtype=xdt, device=dev),
-                           torch.empty((mx,) + tuple(yh.shape[1:]), dtype=xdt, device=dev), None) for _ in range(2)]
-            self._pool_ws = [None, None]
-            self._pool_key = (tuple(xh.shape), tuple(yh.shape), chunks, xdt)
+                           torch.empty((mx,) + tuple(yh.shape[1:]), dtype=xdt, device=dev)) for _ in range(depth)]
+            shape = self._shape(self._pool[0][0], w, padding, "image")
+            self._pool_ws = torch.empty(self.workspace_bytes(shape), dtype=torch.uint8, device=dev)
+            self._pool_key = key
         # a previous call may still be reading the pooled buffers on `cur` / copying them out on s_out
         s_in.wait_stream(cur)
         cur.wait_stream(s_out)
@@ -291,21 +296,16 @@ class QuantWinogradConv:
         self.wcache.get(self.dplan, self.qconfig, w)
         for i in range(chunks):
             a, b = bounds[i], bounds[i + 1]
-            xd, yd, _ = self._pool[i % 2]
+            xd, yd = self._pool[i % depth]
             with torch.cuda.stream(s_in):
-                if i >= 2:
-                    s_in.wait_event(ev_comp[i - 2])   # buffer reuse: chunk i-2 consumed xd
+                if i >= depth:
+                    s_in.wait_event(ev_comp[i - depth])   # slot reuse: chunk i-depth consumed xd
                 xd[: b - a].copy_(xh[a:b], non_blocking=True)
                 ev_in[i].record(s_in)
             cur.wait_event(ev_in[i])
-            if i >= 2:
-                cur.wait_event(ev_out[i - 2])          # yd of chunk i-2 copied out
-            shape = self._shape(xd[: b - a], w, padding, "image")
-            nbytes = self.workspace_bytes(shape)
-            k = i % 2
-            if self._pool_ws[k] is None or self._pool_ws[k].numel() < nbytes:
-                self._pool_ws[k] = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-            self.forward(xd[: b - a], w, bias=bias, padding=padding, out=yd[: b - a], workspace=self._pool_ws[k])
+            if i >= depth:
+                cur.wait_event(ev_out[i - depth])          # yd of chunk i-depth copied out
+            self.forward(xd[: b - a], w, bias=bias, padding=padding, out=yd[: b - a], workspace=self._pool_ws)
             ev_comp[i].record(cur)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_comp[i])
