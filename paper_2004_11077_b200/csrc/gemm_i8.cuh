@@ -281,16 +281,30 @@ __global__ void __launch_bounds__(EpiShape<Epi::kGroups>::kThreads, 1)
       const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + (uint32_t)(a * BN + half * HC);
       const int n0 = nb * BN + half * HC;
       static_assert(HC % 16 == 0, "epilogue column group must be a multiple of 16");
+      if constexpr (Epi::kNarrow) {
+        // 16 columns per step (16 epilogue warps: fewer live registers per warp, latency hidden by the
+        // four warps per scheduler instead of by two interleaved 16-column groups)
 #pragma unroll 1
-      for (int c = 0; c < HC; c += 32) {
-        uint32_t r0[16], r1[16];
-        tmem_ld16(taddr + c, r0);
-        if (c + 16 < HC) tmem_ld16(taddr + c + 16, r1);
-        tmem_ld_wait();
-        const int col = n0 + c;
-        const int nv0 = Kout - col, nv1 = Kout - col - 16;
-        if (row < T && nv0 > 0) epi.apply(xi, row, col, r0, nv0 > 16 ? 16 : nv0);
-        if (c + 16 < HC && row < T && nv1 > 0) epi.apply(xi, row, col + 16, r1, nv1 > 16 ? 16 : nv1);
+        for (int c = 0; c < HC; c += 16) {
+          uint32_t r0[16];
+          tmem_ld16(taddr + c, r0);
+          tmem_ld_wait();
+          const int col = n0 + c;
+          const int nv0 = Kout - col;
+          if (row < T && nv0 > 0) epi.apply(xi, row, col, r0, nv0 > 16 ? 16 : nv0);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < HC; c += 32) {
+          uint32_t r0[16], r1[16];
+          tmem_ld16(taddr + c, r0);
+          if (c + 16 < HC) tmem_ld16(taddr + c + 16, r1);
+          tmem_ld_wait();
+          const int col = n0 + c;
+          const int nv0 = Kout - col, nv1 = Kout - col - 16;
+          if (row < T && nv0 > 0) epi.apply(xi, row, col, r0, nv0 > 16 ? 16 : nv0);
+          if (c + 16 < HC && row < T && nv1 > 0) epi.apply(xi, row, col + 16, r1, nv1 > 16 ? 16 : nv1);
+        }
       }
       tc_fence_before();
       __syncwarp();

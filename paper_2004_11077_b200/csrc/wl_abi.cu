@@ -307,11 +307,10 @@ int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L, bool split) {
   o = align256(o + (size_t)36 * g.T * g.Cp);
   L->off_c4 = o;
   o = align256(o + (size_t)36 * g.T * g.Kp);
-  // Legendre fp32-output path: output-stage fast-path values T4 [T][16][Kp] and error factors [T][Kp]
-  L->off_t4 = o;
-  o = align256(o + (size_t)16 * g.T * g.Kp * sizeof(float));
+  // Legendre fp32-output path: output-stage fast-path values + error factors, T4E [Kp/4][T][17][4]
+  L->off_t4 = o;  // T4E [Kp/4][T][17][4] floats
+  o = align256(o + (size_t)17 * g.T * g.Kp * sizeof(float));
   L->off_e4 = o;
-  o = align256(o + (size_t)g.T * g.Kp * sizeof(float));
   L->bn = (g.Kp >= 256 ? 256 : g.Kp) / 4;  // table chunk = one max-pass epilogue warp's columns (EpiHadMax::kGroups)
   const size_t CB = (g.C + 31) / 32, KB = (g.K + 31) / 32;
   const size_t ents[kNumTables] = {g.T * CB, g.T * CB, (size_t)36 * g.T * (g.Kp / L->bn), g.T * KB, g.T * KB};
@@ -323,6 +322,8 @@ int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L, bool split) {
   // dequantised output table (output widths <= 12 bits; wider widths dequantise in fp64 inline)
   L->off_otab = o;
   if (q->output_transform_bits <= 12) o = align256(o + sizeof(float) * (size_t)L->groups * ((1 << q->output_transform_bits) - 1));
+  L->off_odq = o;
+  if (q->output_transform_bits <= 12) o = align256(o + sizeof(float4) * (size_t)L->groups);
   // deferred-fix list: counters + unit ids (expected ~0.2% of units; overflow falls back inline)
   L->off_fix = o;
   const size_t units = (size_t)g.T * std::max(g.C, g.K);

@@ -63,8 +63,7 @@ void finalize_output_stage(FwdCtx& c, int stage, bool t4) {
 
 void make_output_table(FwdCtx& c) {
   if (!c.otab) return;
-  const long long n = (long long)c.L->groups * (2 * c.b.q[ST_OUT] + 1);
-  out_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.st>>>(c.acc, c.L->groups, c.b.q[ST_OUT], c.otab);
+  out_table_kernel<<<(unsigned)c.L->groups, 256, 0, c.st>>>(c.acc, c.L->groups, c.b.q[ST_OUT], c.otab, c.odq);
 }
 
 // cast "input": per-group max|x|, then x (NCHW fp32/fp64) -> c0 (NHWC int8)
@@ -130,6 +129,7 @@ int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const
   c.t4 = reinterpret_cast<float*>(ws + L.off_t4);
   c.e4 = reinterpret_cast<float*>(ws + L.off_e4);
   c.otab = sizeof(YT) == 4 && q->output_transform_bits <= 12 ? reinterpret_cast<float*>(ws + L.off_otab) : nullptr;
+  c.odq = c.otab ? reinterpret_cast<float4*>(ws + L.off_odq) : nullptr;
   c.pf = plan->d_pf;
   c.st = st;
   c.bias = bias;

@@ -20,6 +20,7 @@ namespace wl {
 struct EpiHadMax {
   static constexpr int kGroups = 4;
   static constexpr int kStageBytes = 0;
+  static constexpr bool kNarrow = false;
   Acc* acc;
   unsigned* table;
   Geo g;
@@ -116,6 +117,7 @@ struct EpiHadRq {
   // each epilogue warp stages its 32 rows x 128 columns of codes (swizzled 16-byte slots) and
   // writes them back as whole row segments
   static constexpr int kGroups = WL_RQ_GROUPS;
+  static constexpr bool kNarrow = WL_RQ_GROUPS == 4;
   static constexpr int kStageBytes = 32 * (256 / kGroups) * (int)sizeof(HT);
   static constexpr int kRowBytes = (256 / kGroups) * (int)sizeof(HT);
   static constexpr int kSwz = kRowBytes / 16 - 1;  // XOR swizzle of the 16-byte slots within a row

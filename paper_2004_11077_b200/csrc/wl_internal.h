@@ -44,7 +44,7 @@ extern const int kTableStage[kNumTables];
 struct Layout {
   Geo g;
   size_t off_acc, off_v, saved_total;  // offsets inside the saved block
-  size_t off_c0, off_h, off_c1, off_c4, off_t4, off_e4, off_tab[kNumTables], tab_bytes[kNumTables], off_otab, off_fix,
+  size_t off_c0, off_h, off_c1, off_c4, off_t4, off_e4, off_tab[kNumTables], tab_bytes[kNumTables], off_otab, off_odq, off_fix,
       total;  // offsets inside the workspace (split: the workspace excludes the saved block)
   unsigned fix_cap;
   int groups, hbytes, bn;
@@ -107,6 +107,7 @@ struct FwdCtx {
   int8_t *c0, *c1, *V, *c4;
   void* h;
   float *t4, *e4, *otab;
+  float4* odq;  // per group {s_hi, s_lo, ok}: certified arithmetic dequantisation (out_table_kernel)
   Tables tabs;
   FixList fl;
   StageE E;

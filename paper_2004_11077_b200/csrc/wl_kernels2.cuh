@@ -338,15 +338,30 @@ __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage
 
 // Dequantised fp32 output of every code of the output stage, per group (quantize.py:120-125:
 // code * scale in fp64, +-qmax snapped to +-max_abs, then rounded to fp32): table[g][code + qmax].
+// One block per group.  The block also certifies an arithmetic form of the same map for the hot
+// output pass: with scale = s_hi + s_lo (fp32 head and tail of the fp64 scale) the value
+// fma(k, s_hi, k * s_lo) is compared with the table entry of EVERY code of the group, +-qmax included;
+// odq[g] = {s_hi, s_lo, ok}.  A group with ok = 1 dequantises with two fp32 instructions per output
+// (bit-identical to the table by this exhaustive check); any other group keeps the table gather.
 template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
-__global__ void out_table_kernel(const Acc* __restrict__ acc, int groups, int qmax, float* __restrict__ table) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) out_table_kernel(const Acc* __restrict__ acc, int groups, int qmax,
+                                                        float* __restrict__ table, float4* __restrict__ odq) {
+  const int gi = blockIdx.x;
+  if (gi >= groups) return;
   const int width = 2 * qmax + 1;
-  if (idx >= (long long)groups * width) return;
-  const int gi = (int)(idx / width), code = (int)(idx % width) - qmax;
   const Acc& a = acc[(size_t)gi * ST_COUNT + ST_OUT];
-  const double maxabs = __longlong_as_double((long long)a.F);
-  table[idx] = code == qmax ? (float)maxabs : (code == -qmax ? (float)-maxabs : (float)((double)code * a.scale));
+  const double maxabs = __longlong_as_double((long long)a.F), scale = a.scale;
+  const float s_hi = (float)scale, s_lo = (float)(scale - (double)s_hi);
+  bool ok = true;
+  for (int i = threadIdx.x; i < width; i += blockDim.x) {
+    const int code = i - qmax;
+    const float v = code == qmax ? (float)maxabs : (code == -qmax ? (float)-maxabs : (float)((double)code * scale));
+    table[(size_t)gi * width + i] = v;
+    const float kf = (float)code;
+    ok = ok && __float_as_uint(__fmaf_rn(kf, s_hi, __fmul_rn(kf, s_lo))) == __float_as_uint(v);
+  }
+  ok = __syncthreads_and(ok);
+  if (threadIdx.x == 0) odq[gi] = make_float4(s_hi, s_lo, ok ? 1.f : 0.f, 0.f);
 }
 
 // ---------------------------------------------------------------------------------- input side

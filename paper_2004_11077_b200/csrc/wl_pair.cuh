@@ -9,49 +9,10 @@
 // while halving issue slots, measured by tools/probe_ffma2.cu), one 16-bit shared load per two
 // codes and one 16-bit shared store per two output codes.
 #pragma once
+#include "wl_f2.cuh"
 #include "wl_staged.cuh"
 
 namespace wl {
-
-struct f2 {
-  unsigned long long u;
-};
-__device__ __forceinline__ f2 mk2(float a, float b) {
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r.u) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float lo2(f2 x) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.u));
-  return a;
-}
-__device__ __forceinline__ float hi2(f2 x) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.u));
-  return b;
-}
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  f2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.u) : "l"(a.u), "l"(b.u), "l"(c.u));
-  return d;
-}
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-  f2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.u) : "l"(a.u), "l"(b.u));
-  return d;
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b) {
-  f2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.u) : "l"(a.u), "l"(b.u));
-  return d;
-}
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
-  f2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.u) : "l"(a.u), "l"(b.u));
-  return d;
-}
-__device__ __forceinline__ f2 bc2(float a) { return mk2(a, a); }
 
 // Row J (and partner P) of L dotted with the packed vector v: the lane-wise sequence of lrows_dot.
 // The first product of a chain is an fma with a +0 addend in the scalar code; mul gives the same
@@ -479,7 +440,7 @@ struct StagedT42 {
 // sout_bt on two channels: output_base_change codes (registers) -> T4 / e4, output maximum.
 template <typename HT, int LD>
 __global__ void __launch_bounds__(StagedT42<LD, sizeof(HT)>::THREADS, 2)
-    sout_bt2_kernel(const HT* __restrict__ h, float* __restrict__ t4, float* __restrict__ e4, Geo g, Bits b,
+    sout_bt2_kernel(const HT* __restrict__ h, const __grid_constant__ CUtensorMap t4map, Geo g, Bits b,
                     Acc* __restrict__ acc, const PlanF64* __restrict__ pf, Tables tabs, FixList fl) {
   using S = StagedT42<LD, sizeof(HT)>;
   extern __shared__ __align__(128) uint8_t wl_stage_smem[];
@@ -492,6 +453,7 @@ __global__ void __launch_bounds__(StagedT42<LD, sizeof(HT)>::THREADS, 2)
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
+    tma_prefetch_desc(&t4map);
   }
   __syncthreads();
   auto issue = [&](int it, int s) {
@@ -515,8 +477,10 @@ __global__ void __launch_bounds__(StagedT42<LD, sizeof(HT)>::THREADS, 2)
     const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr, ef = ga[ST_OBC].ef;
     const f2 r2 = bc2(r);
     const uint8_t* st = sm + s * S::STAGE_BYTES + tl * S::TILE_BYTES;
-    float* ot = reinterpret_cast<float*>(osm + s * S::OUT_BYTES) + tl * 16 * LD + k;
-    float* oe = reinterpret_cast<float*>(osm + s * S::OUT_BYTES + S::TPB * S::T4_TILE) + tl * LD + k;
+    // staged block in the T4E layout [LD/4 channel groups][TPB tiles][17 rows][4 channels]: rows 0..15
+    // = T4 elements, row 16 = error factors (wl_staged.cuh, sout_cw_kernel)
+    float* ot = reinterpret_cast<float*>(osm + s * S::OUT_BYTES) + ((k >> 2) * S::TPB + tl) * 68 + (k & 3);
+    float* oe = ot + 64;
     f2 K4[6][6];
     bool def0, def1, f0, f1;
     {
@@ -538,14 +502,14 @@ __global__ void __launch_bounds__(StagedT42<LD, sizeof(HT)>::THREADS, 2)
     }
     const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
     float m0, m1, tm0, tm1, ef0, ef1;
-    t4_of_unit2(K4, ty, tx, g, ot, LD, ef0, ef1, m0, m1, tm0, tm1);
+    t4_of_unit2(K4, ty, tx, g, ot, 4, ef0, ef1, m0, m1, tm0, tm1);
     *reinterpret_cast<float2*>(oe) = make_float2(ef0, ef1);
     if (f0) {
-      const float2 mm = exact_t4_unit<HT>(h, g, b, ga, pf, tt, k, ty, tx, ot, LD, oe);
+      const float2 mm = exact_t4_unit<HT>(h, g, b, ga, pf, tt, k, ty, tx, ot, 4, oe);
       m0 = mm.x, tm0 = mm.y;
     }
     if (f1) {
-      const float2 mm = exact_t4_unit<HT>(h, g, b, ga, pf, tt, k + 1, ty, tx, ot + 1, LD, oe + 1);
+      const float2 mm = exact_t4_unit<HT>(h, g, b, ga, pf, tt, k + 1, ty, tx, ot + 1, 4, oe + 1);
       m1 = mm.x, tm1 = mm.y;
     }
     if (def0) m0 = tm0 = 0.f;  // recorded by fixup_obct_kernel from the exact codes
@@ -555,9 +519,8 @@ __global__ void __launch_bounds__(StagedT42<LD, sizeof(HT)>::THREADS, 2)
     if (threadIdx.x == 0) bulk_wait_read<0>();  // the store issued last iteration has read buffer s^1
     __syncthreads();
     if (threadIdx.x == 0) {
-      const int t0 = it * S::TPB, nt = min(S::TPB, g.T - t0);
-      bulk_s2g(t4 + (size_t)t0 * 16 * LD, osm + s * S::OUT_BYTES, (uint32_t)(nt * S::T4_TILE));
-      bulk_s2g(e4 + (size_t)t0 * LD, osm + s * S::OUT_BYTES + S::TPB * S::T4_TILE, (uint32_t)(nt * S::E_TILE));
+      // one tensor store of the box {68 floats, TPB tiles, LD/4 channel groups}; tiles past T are clipped
+      tma_store_3d(&t4map, osm + s * S::OUT_BYTES, 0, it * S::TPB, 0);
       bulk_commit();
     }
   }

@@ -9,6 +9,7 @@
 // each, channel fastest) walks tile groups grid-stride; thread 0 prefetches group k+1 into the other
 // buffer while group k is computed, completion tracked by one mbarrier per buffer.
 #pragma once
+#include "wl_f2.cuh"
 #include "wl_kernels2.cuh"
 #include "wl_ptx.cuh"
 
@@ -297,7 +298,8 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
     sout_c_kernel(const __grid_constant__ CUtensorMap srcmap, const HT* __restrict__ h,
                   const int8_t* __restrict__ c4, float* __restrict__ y, const float* __restrict__ bias,
                   const __grid_constant__ Geo g, const __grid_constant__ Bits b, const Acc* __restrict__ acc,
-                  const PlanF64* __restrict__ pf, const float* __restrict__ otab, FixList fl) {
+                  const PlanF64* __restrict__ pf, const float* __restrict__ otab, const float4* __restrict__ odq,
+                  FixList fl) {
   using S = StagedOut;
   using ST = std::conditional_t<MODE == 0, HT, int8_t>;  // staged code type
   constexpr int IN_TILE = 36 * S::KB * (int)sizeof(ST);
@@ -373,12 +375,32 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
       }
       float* o = so + lane * S::OK + w * S::OT;
       float dmax = 0.f, kd;
-      sandwich_cols<LOT>(X, [&](int j, const float (&col)[4], float cm) {
-        float dcol = 0.f;
+      // group with a certified arithmetic dequantisation (out_table_kernel): two fp32 ops per output
+      // instead of a table gather
+      float s_hi = 0.f, s_lo = 0.f;
+      bool arith = false;
+      if constexpr (TAB) {
+        const float4 dq = __ldg(&odq[grp]);
+        s_hi = dq.x, s_lo = dq.y, arith = dq.z != 0.f;
+      }
+      if (arith) {
+        sandwich_cols<LOT>(X, [&](int j, const float (&col)[4], float cm) {
+          float dcol = 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[4 * i + j] = deqf(rq_col(col[i], r, kd, dcol)) + bk;
-        dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<LOT>(), dcol));
-      });
+          for (int i = 0; i < 4; ++i) {
+            rq_col(col[i], r, kd, dcol);
+            o[4 * i + j] = __fadd_rn(__fmaf_rn(kd, s_hi, __fmul_rn(kd, s_lo)), bk);
+          }
+          dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<LOT>(), dcol));
+        });
+      } else {
+        sandwich_cols<LOT>(X, [&](int j, const float (&col)[4], float cm) {
+          float dcol = 0.f;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) o[4 * i + j] = deqf(rq_col(col[i], r, kd, dcol)) + bk;
+          dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<LOT>(), dcol));
+        });
+      }
       const bool want = dmax > thr && active;
       if (__any_sync(0xffffffffu, want) && want && !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want))
         fix_out_unit_to<MODE, HT, float>(h, c4, bias, g, b, acc, pf, t, k, (uint32_t)g.Kp,
@@ -500,105 +522,13 @@ __device__ __noinline__ float2 exact_t4_unit(const HT* __restrict__ h, const Geo
   return make_float2(m, tm);
 }
 
-template <int LD, int EB>
-struct StagedT4 {
-  static_assert(LD <= 256, "staged path handles up to 256 padded channels");
-  static constexpr int TPB = 256 / LD;
-  static constexpr int THREADS = TPB * LD;
-  static constexpr int TILE_BYTES = 36 * LD * EB;
-  static constexpr int STAGE_BYTES = TPB * TILE_BYTES;
-  static constexpr int T4_TILE = 16 * LD * 4;
-  static constexpr int E_TILE = LD * 4;
-  static constexpr int OUT_BYTES = TPB * (T4_TILE + E_TILE);
-  static constexpr int SMEM = 2 * STAGE_BYTES + 2 * OUT_BYTES + 16;
-};
-
-// Legendre output_base_change codes (kept in registers) -> T4 / e4 stored, output max recorded.
-template <typename HT, int LD>
-__global__ void __launch_bounds__(StagedT4<LD, sizeof(HT)>::THREADS, WL_MINB)
-    sout_bt_kernel(const HT* __restrict__ h, float* __restrict__ t4, float* __restrict__ e4, Geo g, Bits b,
-                   Acc* __restrict__ acc, const PlanF64* __restrict__ pf, Tables tabs, FixList fl) {
-  using S = StagedT4<LD, sizeof(HT)>;
-  extern __shared__ __align__(128) uint8_t wl_stage_smem[];
-  uint8_t* sm = wl_stage_smem;
-  uint8_t* osm = sm + 2 * S::STAGE_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(osm + 2 * S::OUT_BYTES);
-  const int niter = (g.T + S::TPB - 1) / S::TPB;
-  const int tl = threadIdx.x / LD, k = threadIdx.x % LD;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto issue = [&](int it, int s) {
-    const int t0 = it * S::TPB;
-    const int nt = min(S::TPB, g.T - t0);
-    mbar_arrive_expect_tx(&bar[s], (uint32_t)(nt * S::TILE_BYTES));
-    bulk_g2s(sm + s * S::STAGE_BYTES, reinterpret_cast<const uint8_t*>(h) + (size_t)t0 * S::TILE_BYTES,
-             (uint32_t)(nt * S::TILE_BYTES), &bar[s]);
-  };
-  if (threadIdx.x == 0 && (int)blockIdx.x < niter) issue(blockIdx.x, 0);
-  int kk = 0;
-  for (int it = blockIdx.x; it < niter; it += gridDim.x, ++kk) {
-    const int s = kk & 1;
-    if (threadIdx.x == 0 && it + (int)gridDim.x < niter) issue(it + gridDim.x, s ^ 1);
-    mbar_wait(&bar[s], (uint32_t)((kk >> 1) & 1));
-    const int t = it * S::TPB + tl;
-    const bool active = t < g.T && k < g.K;
-    const int tt = active ? t : 0;
-    const int n = (int)g.fTP.div((unsigned)tt), tile = (int)g.fTP.mod((unsigned)tt), grp = (int)g.fipg.div((unsigned)n);
-    const Acc* ga = acc + (size_t)grp * ST_COUNT;
-    const float r = ga[ST_OBC].r, thr = ga[ST_OBC].thr, ef = ga[ST_OBC].ef;
-    const uint8_t* st = sm + s * S::STAGE_BYTES + tl * S::TILE_BYTES;
-    float* ot = reinterpret_cast<float*>(osm + s * S::OUT_BYTES) + tl * 16 * LD + k;
-    float* oe = reinterpret_cast<float*>(osm + s * S::OUT_BYTES + S::TPB * S::T4_TILE) + tl * LD + k;
-    float K4[6][6];
-    bool deferred = false, inline_fix = false;
-    {
-      float X[6][6];
-      stage_x<LD, HT>(st, k, X);
-      float dmax = 0.f;
-      sandwich_cols<tab::Leg_OBC>(X, [&](int j, const float (&col)[6], float cm) {
-        float dcol = 0.f;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) rq_col(col[i], r, K4[i][j], dcol);
-        dmax = fmaxf(dmax, fmaf(ef * cm, max_row_abs_sum<tab::Leg_OBC>(), dcol));
-      });
-      const bool want = dmax > thr && active;
-      deferred = defer_fix(fl, FIX_OBC, (unsigned)tt * (unsigned)g.K + (unsigned)k, want);
-      inline_fix = want && !deferred;
-    }
-    const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
-    float m, tm, efac;
-    if (inline_fix) {
-      const float2 mm = exact_t4_unit<HT>(h, g, b, ga, pf, tt, k, ty, tx, ot, LD, oe);
-      m = mm.x, tm = mm.y;
-    } else {
-      t4_of_unit(K4, ty, tx, g, ot, LD, efac, m, tm);
-      *oe = efac;
-    }
-    if (deferred) m = tm = 0.f;  // recorded by fixup_obct_kernel from the exact codes
-    record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], tt, k, g.K);
-    fence_proxy_async_smem();
-    if (threadIdx.x == 0) bulk_wait_read<0>();  // the store issued last iteration has read buffer s^1
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int t0 = it * S::TPB, nt = min(S::TPB, g.T - t0);
-      bulk_s2g(t4 + (size_t)t0 * 16 * LD, osm + s * S::OUT_BYTES, (uint32_t)(nt * S::T4_TILE));
-      bulk_s2g(e4 + (size_t)t0 * LD, osm + s * S::OUT_BYTES + S::TPB * S::T4_TILE, (uint32_t)(nt * S::E_TILE));
-      bulk_commit();
-    }
-  }
-  if (threadIdx.x == 0) bulk_wait_all<0>();
-}
-
-// Deferred output_base_change units: exact c4 from h, T4 / e4 rewritten, output max recorded.
+// Deferred output_base_change units: exact c4 from h, the unit's T4E entries (16 T4 values + error
+// factor, layout [Kp/4][T][17][4]) rewritten, output max recorded.
 template <typename HT>
-__global__ void __launch_bounds__(128) fixup_obct_kernel(FixList fl, const HT* __restrict__ h, float* __restrict__ t4,
-                                                         float* __restrict__ e4, const __grid_constant__ Geo g,
-                                                         const __grid_constant__ Bits b, Acc* __restrict__ acc,
-                                                         const PlanF64* __restrict__ pf, Tables tabs) {
+__global__ void __launch_bounds__(128) fixup_obct_kernel(FixList fl, const HT* __restrict__ h, float* __restrict__ t4e,
+                                                         const __grid_constant__ Geo g, const __grid_constant__ Bits b,
+                                                         Acc* __restrict__ acc, const PlanF64* __restrict__ pf,
+                                                         Tables tabs) {
   const unsigned cnt = fix_count(fl, FIX_OBC);
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const unsigned u = fl.items[i];
@@ -612,50 +542,98 @@ __global__ void __launch_bounds__(128) fixup_obct_kernel(FixList fl, const HT* _
     for (int e = 0; e < 36; ++e) K4[e / 6][e % 6] = (float)c4[e / 6][e % 6];
     const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
     float m, tm, efac;
-    t4_of_unit(K4, ty, tx, g, t4 + (size_t)t * 16 * g.Kp + k, g.Kp, efac, m, tm);
-    e4[(size_t)t * g.Kp + k] = efac;
+    float* ot = t4e + ((size_t)(k >> 2) * g.T + t) * 68 + (k & 3);
+    t4_of_unit(K4, ty, tx, g, ot, 4, efac, m, tm);
+    ot[64] = efac;
     record_unit_single(m, tm, grp, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K);
   }
 }
 
-// Final output pass from T4 / e4 (Legendre, fp32 output).  Work item = 8 tiles x 32 channels: TMA
-// boxes {32, 16, 8} of T4 and {32, 1, 8} of e4; warp = tile, lane = channel; outputs staged and
-// stored as in sout_c_kernel.
+// Exact final outputs of one unit written straight to y (dequantised, + bias, cropped): the deferred
+// fix of fixup_outt_kernel and the inline fallback of sout_cw_kernel when the fix list is full.
+template <typename HT>
+__device__ __noinline__ void exact_out_unit_to_y(const HT* __restrict__ h, float* __restrict__ y,
+                                                 const float* __restrict__ bias, const Geo& g, const Bits& b,
+                                                 const Acc* __restrict__ acc, const PlanF64* __restrict__ pf, int t,
+                                                 int k) {
+  const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
+  const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
+  const Acc* ga = acc + (size_t)grp * ST_COUNT;
+  const int qo = b.q[ST_OUT];
+  const double scale = ga[ST_OUT].scale;
+  const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
+  const float bk = bias ? bias[k] : 0.f;
+  exact_out_from_h<HT>(h, g, b, acc, pf, t, k, [&](int ii, int jj, int code) {
+    const int rr = 4 * ty + ii, cc = 4 * tx + jj;
+    if (rr < g.Ho && cc < g.Wo) {
+      const float v = code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
+      y[(((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + cc] = v + bk;
+    }
+  });
+}
+
+// Final output pass from T4E (Legendre, fp32 output).  T4E = [Kp/4 channel groups][T tiles][17][4
+// channels] floats: rows 0..15 the output stage's fp32 values T4 of the unit, row 16 its error factor.
+// Work item = R consecutive tiles x CG channel groups = one TMA box {68, R, CG}; the 8 warps are
+// (pass, channel group) pairs, lane = (tile slot, channel) = (lane >> 2, lane & 3), a pass covers TPP <= 8
+// tiles.  In that mapping
+//   * the staged reads are conflict-free: a unit starts 68 floats (4 banks) after its neighbour tile,
+//   * a warp's store of output row i is, per channel, its tiles' 16-byte pieces side by side, straight
+//     from registers: no shared output staging and no CTA barrier; warps run independently on an
+//     NS-deep full/empty mbarrier ring filled by one thread,
+//   * R is a whole number of tile rows (CwShape), so an item writes, per channel, 4 complete output rows
+//     = one contiguous 16*tw*4-byte range of y.  DRAM efficiency of the y writes depends on exactly that:
+//     tools/probe_ywrite.cu measures 3.7 TB/s for 8-tile (128-byte) runs and 5.5 TB/s for whole tile rows.
+struct CwShape {
+  int R, TPP, CG;  // tiles per item, tiles per pass, channel groups per item; (R / TPP rounded up) * CG = 8 warps
+};
+inline CwShape cw_shape(int tw) {
+  if (tw <= 8) return {(8 / tw) * tw, (8 / tw) * tw, 8};
+  if (tw <= 16) return {tw, (tw + 1) / 2, 4};
+  if (tw <= 32) return {tw, (tw + 3) / 4, 2};
+  return {32, 8, 2};
+}
+struct StagedCw {
+  static constexpr int THREADS = 256;
+  static constexpr int STAGE_BYTES = 64 * 68 * 4;  // R * CG <= 64 units-of-4-channels per item
+  static constexpr int smem(int ns) { return ns * STAGE_BYTES + 2 * ns * 8 + 16; }
+};
+
 template <typename HT, bool TAB, int NS>
-__global__ void __launch_bounds__(StagedOut::THREADS, NS == 2 ? 4 : 3)
-    sout_ct_kernel(const __grid_constant__ CUtensorMap t4map, const __grid_constant__ CUtensorMap e4map,
-                   const HT* __restrict__ h, float* __restrict__ y, const float* __restrict__ bias,
-                   const __grid_constant__ Geo g, const __grid_constant__ Bits b, const Acc* __restrict__ acc,
-                   const PlanF64* __restrict__ pf, const float* __restrict__ otab, FixList fl) {
-  using S = StagedOut;
-  constexpr int T4B = S::TPB * 16 * S::KB * 4, EB = S::TPB * S::KB * 4, IN_BYTES = T4B + EB;
+__global__ void __launch_bounds__(StagedCw::THREADS, 4)
+    sout_cw_kernel(const __grid_constant__ CUtensorMap t4map, const HT* __restrict__ h, float* __restrict__ y,
+                   const float* __restrict__ bias, const __grid_constant__ Geo g, const __grid_constant__ Bits b,
+                   const Acc* __restrict__ acc, const PlanF64* __restrict__ pf, const float* __restrict__ otab,
+                   const float4* __restrict__ odq, FixList fl, const CwShape sh) {
+  using S = StagedCw;
   extern __shared__ __align__(128) uint8_t wl_stage_smem[];
   uint8_t* sm = wl_stage_smem;
-  float* so = reinterpret_cast<float*>(sm + NS * IN_BYTES);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + NS * IN_BYTES + S::OUT_BYTES);
-  __shared__ long long ybase[S::TPB];
-  __shared__ int yrows[S::TPB];
-  const int nkb = (g.K + S::KB - 1) / S::KB;
-  const int niter = ((g.T + S::TPB - 1) / S::TPB) * nkb;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * S::STAGE_BYTES);
+  uint64_t* empty = full + NS;
+  const int ncb = ((g.K + 3) / 4 + sh.CG - 1) / sh.CG;
+  const int niter = ((g.T + sh.R - 1) / sh.R) * ncb;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = lane >> 2, ch = lane & 3;
+  const int pass = w / sh.CG, cgi = w - pass * sh.CG;
+  const int tin = pass * sh.TPP + slot;                 // tile of the item this lane owns
+  const bool lane_on = slot < sh.TPP && tin < sh.R;
+  const uint32_t box_bytes = (uint32_t)(sh.R * sh.CG * 68 * 4);
   const int qo = b.q[ST_OUT];
-  const long long plane = (long long)g.Ho * g.Wo;
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], S::THREADS / 32);
+    }
     fence_mbar_init();
     tma_prefetch_desc(&t4map);
-    tma_prefetch_desc(&e4map);
   }
   __syncthreads();
   auto issue = [&](int it, int s) {
-    const int tg = it / nkb, kb = it - tg * nkb;
-    mbar_arrive_expect_tx(&bar[s], (uint32_t)IN_BYTES);
-    tma_load_3d(sm + s * IN_BYTES, &t4map, &bar[s], kb * S::KB, 0, tg * S::TPB);
-    tma_load_3d(sm + s * IN_BYTES + T4B, &e4map, &bar[s], kb * S::KB, 0, tg * S::TPB);
+    const int tg = it / ncb, cb = it - tg * ncb;
+    mbar_arrive_expect_tx(&full[s], box_bytes);
+    tma_load_3d(sm + s * S::STAGE_BYTES, &t4map, &full[s], 0, tg * sh.R, cb * sh.CG);
   };
-  // NS-deep ring: NS-1 work items in flight while one is computed (buffer (kk-1) % NS is refilled
-  // only after every thread passed iteration kk-1's trailing barrier)
   if (threadIdx.x == 0)
 #pragma unroll
     for (int q = 0; q < NS - 1; ++q)
@@ -663,71 +641,92 @@ __global__ void __launch_bounds__(StagedOut::THREADS, NS == 2 ? 4 : 3)
   int kk = 0;
   for (int it = blockIdx.x; it < niter; it += gridDim.x, ++kk) {
     const int s = kk % NS;
-    if (threadIdx.x == 0 && it + (NS - 1) * (int)gridDim.x < niter) issue(it + (NS - 1) * gridDim.x, (kk + NS - 1) % NS);
-    const int tg = it / nkb, kb = it - tg * nkb;
-    const int t0 = tg * S::TPB, k0 = kb * S::KB;
-    if (threadIdx.x < S::TPB) {
-      const int t = t0 + threadIdx.x;
-      long long base = -1;
-      int rows = 0;
-      if (t < g.T) {
-        const int n = (int)g.fTP.div((unsigned)t), tile = t - n * g.TP;
-        const int ty = (int)g.ftw.div((unsigned)tile), tx = tile - ty * g.tw;
-        base = ((long long)n * g.K + k0) * plane + (long long)(4 * ty) * g.Wo + 4 * tx;
-        rows = min(4, g.Ho - 4 * ty);
-      }
-      ybase[threadIdx.x] = base;
-      yrows[threadIdx.x] = rows;
+    if (threadIdx.x == 0 && it + (NS - 1) * (int)gridDim.x < niter) {
+      // refill the slot of local iteration kk - 1 once all 8 warps released it
+      const int j = kk + NS - 1, f = j / NS;
+      if (f >= 1) mbar_wait(&empty[j % NS], (uint32_t)((f - 1) & 1));
+      issue(it + (NS - 1) * gridDim.x, j % NS);
     }
-    mbar_wait(&bar[s], (uint32_t)((kk / NS) & 1));
-    {
-      const int t = t0 + w, k = k0 + lane;
-      const bool active = t < g.T && k < g.K;
-      const int tt = active ? t : 0;
-      const int grp = (int)g.fipg.div(g.fTP.div((unsigned)tt));
-      const Acc* ga = acc + (size_t)grp * ST_COUNT;
-      const float r = active ? ga[ST_OUT].r : 0.f, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
+    const int tg = it / ncb, cb = it - tg * ncb;
+    const int t = tg * sh.R + tin, k = (cb * sh.CG + cgi) * 4 + ch;
+    const bool active = lane_on && t < g.T && k < g.K;
+    const int tt = active ? t : 0;
+    // per-unit parameters first: their latency overlaps the wait for the box
+    const int n = (int)g.fTP.div((unsigned)tt), tile = tt - n * g.TP;
+    const int grp = (int)g.fipg.div((unsigned)n);
+    const Acc* ga = acc + (size_t)grp * ST_COUNT;
+    const float r = active ? ga[ST_OUT].r : 0.f, thr = ga[ST_OUT].thr, ef = ga[ST_OUT].ef;
+    float4 dq = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (TAB) dq = __ldg(&odq[grp]);
+    const float bk = (bias && active) ? __ldg(&bias[k]) : 0.f;
+    const int ty = (int)g.ftw.div((unsigned)tile), tx = tile - ty * g.tw;
+    mbar_wait(&full[s], (uint32_t)((kk / NS) & 1));
+    const float* p =
+        reinterpret_cast<const float*>(sm + s * S::STAGE_BYTES) + (cgi * sh.R + (lane_on ? tin : 0)) * 68 + ch;
+    f2 v[8];
+    float dmax = 0.f;
+    if (TAB && dq.z != 0.f) {
+      // certified arithmetic dequantisation (out_table_kernel): value = fma(k, s_hi, k * s_lo) + bias.
+      // fma(T, -r, k) is the exact negation of rq_col's fma(T, r, -k), so dmax is the same number.
+      const f2 r2 = bc2(r), nr2 = bc2(-r), shi = bc2(dq.x), slo = bc2(dq.y), bk2 = bc2(bk), mg = bc2(kMagic);
+#pragma unroll
+      for (int e = 0; e < 16; e += 2) {
+        const f2 T = mk2(p[e * 4], p[(e + 1) * 4]);
+        const f2 k2 = sub2(fma2(T, r2, mg), mg);
+        const f2 d = fma2(T, nr2, k2);
+        dmax = fmaxf(dmax, fmaxf(fabsf(lo2(d)), fabsf(hi2(d))));
+        v[e >> 1] = add2(fma2(k2, shi, mul2(k2, slo)), bk2);
+      }
+    } else {
       const float* tabg = TAB ? otab + (size_t)grp * (2 * qo + 1) + qo : nullptr;
       const double scale = ga[ST_OUT].scale;
       const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
-      auto deqf = [=](int code) -> float {
-        if constexpr (TAB)
-          return __ldg(tabg + code);
-        else
-          return code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
-      };
-      const float bk = (bias && active) ? __ldg(&bias[k]) : 0.f;
-      const float* p = reinterpret_cast<const float*>(sm + s * IN_BYTES) + w * 16 * S::KB + lane;
-      const float efac = reinterpret_cast<const float*>(sm + s * IN_BYTES + T4B)[w * S::KB + lane];
-      float* o = so + lane * S::OK + w * S::OT;
-      float dmax = 0.f, kd;
+      float kd;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) o[e] = deqf(rq_col(active ? p[e * S::KB] : 0.f, r, kd, dmax)) + bk;
-      const bool want = fmaf(ef, efac, dmax) > thr && active;
-      if (__any_sync(0xffffffffu, want) && want &&
-          !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want))
-        exact_out_to<HT>(h, g, b, acc, pf, t, k, o, tabg, bk);
-    }
-    __syncthreads();
+      for (int e = 0; e < 16; e += 2) {
+        float o2[2];
 #pragma unroll
-    for (int rep = 0; rep < (S::KB * 4 * S::TPB) / S::THREADS; ++rep) {
-      const int q = rep * S::THREADS + threadIdx.x;
-      const int tq = q & (S::TPB - 1), i = (q / S::TPB) & 3, kq = q / (4 * S::TPB);
-      const long long base = ybase[tq];
-      if (base < 0 || k0 + kq >= g.K || i >= yrows[tq]) continue;
-      const float4 v = *reinterpret_cast<const float4*>(so + kq * S::OK + tq * S::OT + 4 * i);
-      float* row = y + base + kq * plane + (long long)i * g.Wo;
-      if ((g.Wo & 3) == 0) {
-        __stcs(reinterpret_cast<float4*>(row), v);
-      } else {
-        const int cols = g.Wo - (int)((base % g.Wo));
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < cols) row[j] = vv[j];
+        for (int u = 0; u < 2; ++u) {
+          const int code = rq_col(p[(e + u) * 4], r, kd, dmax);
+          if constexpr (TAB)
+            o2[u] = __ldg(tabg + code) + bk;
+          else
+            o2[u] = (code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale))) + bk;
+        }
+        v[e >> 1] = mk2(o2[0], o2[1]);
       }
     }
-    __syncthreads();
+    const float efac = p[64];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // every lane's reads of the slot are done
+    const bool want = fmaf(ef, efac, dmax) > thr && active;
+    bool skip = !active;
+    if (__any_sync(0xffffffffu, want) && want &&
+        !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want)) {
+      exact_out_unit_to_y<HT>(h, y, bias, g, b, acc, pf, t, k);
+      skip = true;
+    }
+    if (!skip) {
+      float* row = y + (((size_t)n * g.K + k) * g.Ho + 4 * ty) * g.Wo + 4 * tx;
+      const int rows = min(4, g.Ho - 4 * ty);
+      if ((g.Wo & 3) == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < rows)
+            __stcs(reinterpret_cast<float4*>(row + (size_t)i * g.Wo),
+                   make_float4(lo2(v[2 * i]), hi2(v[2 * i]), lo2(v[2 * i + 1]), hi2(v[2 * i + 1])));
+      } else {
+        const int cols = min(4, g.Wo - 4 * tx);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < rows) {
+            const float vv[4] = {lo2(v[2 * i]), hi2(v[2 * i]), lo2(v[2 * i + 1]), hi2(v[2 * i + 1])};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < cols) row[(size_t)i * g.Wo + j] = vv[j];
+          }
+      }
+    }
   }
 }
 
@@ -740,21 +739,7 @@ __global__ void __launch_bounds__(128) fixup_outt_kernel(FixList fl, const HT* _
   const unsigned cnt = fix_count(fl, FIX_OUT);
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const unsigned u = fl.items[i];
-    const int t = (int)g.fK.div(u), k = (int)g.fK.mod(u);
-    const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
-    const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
-    const Acc* ga = acc + (size_t)grp * ST_COUNT;
-    const int qo = b.q[ST_OUT];
-    const double scale = ga[ST_OUT].scale;
-    const double maxabs = __longlong_as_double((long long)ga[ST_OUT].F);
-    const float bk = bias ? bias[k] : 0.f;
-    exact_out_from_h<HT>(h, g, b, acc, pf, t, k, [&](int ii, int jj, int code) {
-      const int rr = 4 * ty + ii, cc = 4 * tx + jj;
-      if (rr < g.Ho && cc < g.Wo) {
-        const float v = code == qo ? (float)maxabs : (code == -qo ? (float)-maxabs : (float)((double)code * scale));
-        y[(((size_t)n * g.K + k) * g.Ho + rr) * g.Wo + cc] = v + bk;
-      }
-    });
+    exact_out_unit_to_y<HT>(h, y, bias, g, b, acc, pf, (int)g.fK.div(u), (int)g.fK.mod(u));
   }
 }
 
