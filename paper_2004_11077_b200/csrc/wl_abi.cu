@@ -280,6 +280,7 @@ int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L, bool split) {
   g.Cp = pow2_at_least(g.C, 32);
   g.Kp = pow2_at_least(g.K, 64);
   g.ipg = s->images_per_group;
+  g.lazy = (g.N / g.ipg) < 16 ? 1 : 0;
   g.fTP = make_fastdiv((unsigned)g.TP);
   g.ftw = make_fastdiv((unsigned)g.tw);
   g.fipg = make_fastdiv((unsigned)g.ipg);

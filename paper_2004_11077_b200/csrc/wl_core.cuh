@@ -184,6 +184,19 @@ __device__ __noinline__ double replay_hadamard(const int8_t* __restrict__ u, con
   return acc;
 }
 
+// Group-wide running maxima are written with a read-first atomic: a plain L2 load (ld.global.cg, the
+// coherence point of atomics) filters out every value that cannot raise the maximum, so a slot shared
+// by a whole batch (scale_groups = "batch": one group) sees a handful of atomics per pass instead of
+// one per warp serialised on a single L2 address (16.2 -> ~10 ms on config 4 with batch-wide scales).
+// With many groups (per-image scales) the slots are uncontended and the extra load's latency would
+// only stall the warp, so `lazy` (Geo::lazy: fewer than 16 groups) selects the filter.
+__device__ __forceinline__ void lazy_max(unsigned int* p, unsigned int v, bool lazy) {
+  if (!lazy || v > __ldcg(p)) atomicMax(p, v);
+}
+__device__ __forceinline__ void lazy_max(unsigned long long* p, unsigned long long v, bool lazy) {
+  if (!lazy || v > __ldcg(p)) atomicMax(p, v);
+}
+
 __device__ __forceinline__ unsigned long long dbits(double d) { return (unsigned long long)__double_as_longlong(d); }
 
 // Decide whether this lane must replay its local-argmax elements: only lanes holding the maximum
@@ -210,11 +223,12 @@ __device__ __forceinline__ bool replay_gate(long long m, int g, const Acc* acc, 
   return m >= cur;
 }
 
-__device__ __forceinline__ void publish_max(long long m, int g, Acc* acc, int stride, bool uniform, long long wmax) {
+__device__ __forceinline__ void publish_max(long long m, int g, Acc* acc, int stride, bool uniform, long long wmax,
+                                            bool lazy = false) {
   if (uniform) {
-    if ((threadIdx.x & 31) == 0 && wmax > 0 && g >= 0) atomicMax(&acc[(size_t)g * stride].M, (unsigned long long)wmax);
+    if ((threadIdx.x & 31) == 0 && wmax > 0 && g >= 0) lazy_max(&acc[(size_t)g * stride].M, (unsigned long long)wmax, lazy);
   } else if (m > 0 && g >= 0) {
-    atomicMax(&acc[(size_t)g * stride].M, (unsigned long long)m);
+    lazy_max(&acc[(size_t)g * stride].M, (unsigned long long)m, lazy);
   }
 }
 
@@ -269,12 +283,12 @@ __device__ __forceinline__ void record_max(float m, int g, unsigned* table_entry
   }
 }
 
-__device__ __forceinline__ void publish_mf(float m, int g, Acc* acc_stage, bool uniform, float wmax) {
+__device__ __forceinline__ void publish_mf(float m, int g, Acc* acc_stage, bool uniform, float wmax, bool lazy = false) {
   if (uniform) {
     if ((threadIdx.x & 31) == 0 && wmax > 0.f && g >= 0)
-      atomicMax(&acc_stage[(size_t)g * ST_COUNT].MF, __float_as_uint(wmax));
+      lazy_max(&acc_stage[(size_t)g * ST_COUNT].MF, __float_as_uint(wmax), lazy);
   } else if (m > 0.f && g >= 0) {
-    atomicMax(&acc_stage[(size_t)g * ST_COUNT].MF, __float_as_uint(m));
+    lazy_max(&acc_stage[(size_t)g * ST_COUNT].MF, __float_as_uint(m), lazy);
   }
 }
 

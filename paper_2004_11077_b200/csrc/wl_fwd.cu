@@ -76,10 +76,18 @@ static int input_cast(FwdCtx& c, const XT* x) {
   prof_mark("absmax_input", c.st);
   const bool w64 = sizeof(XT) == 4 && (g.W & 3) == 0 && g.W <= 64 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   if (w64) {
-    const int smem = g.W * (g.Cp + 4);
+#ifndef WL_QI_RH
+#define WL_QI_RH 2
+#endif
+    // band of rh rows per block: per channel one contiguous rh * W float run (at most 256 float4 slots and
+    // ~60 KB of staging per block)
+    int rh = WL_QI_RH;
+    while (rh > 1 && (rh * g.W * (g.Cp + 4) > 60 * 1024 || rh * g.W / 4 > 256)) rh >>= 1;
+    rh = std::min(rh, g.H);
+    const int smem = rh * g.W * (g.Cp + 4);
     WL_CUDA(ensure_smem_attr(reinterpret_cast<const void*>(quant_input_w64_kernel<0>), smem));
-    quant_input_w64_kernel<<<dim3(g.H, g.N), 256, smem, c.st>>>(reinterpret_cast<const float*>(x), c.c0, g, c.b,
-                                                                 c.acc);
+    quant_input_w64_kernel<<<dim3((g.H + rh - 1) / rh, g.N), 256, smem, c.st>>>(reinterpret_cast<const float*>(x),
+                                                                              c.c0, g, c.b, c.acc, rh);
   } else {
     const int qrow = std::max(4, std::min(64, (160000 / (g.Cp + 16)) & ~3));
     const int qsm = qrow * (g.Cp + 16);

@@ -59,7 +59,7 @@ struct EpiHadMax {
     Acc* a = acc + ST_HAD;
     // (replay_gate only computes the warp reduction here; the replay itself runs in finalize)
     replay_gate(m, grp, a, ST_COUNT, uniform, wmax);
-    publish_max(m, grp, a, ST_COUNT, uniform, wmax);
+    publish_max(m, grp, a, ST_COUNT, uniform, wmax, g.lazy != 0);
   }
 };
 

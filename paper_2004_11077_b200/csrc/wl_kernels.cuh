@@ -32,6 +32,7 @@ struct FastDiv {
 
 struct Geo {
   int N, C, K, H, W, pad, Ho, Wo, th, tw, TP, T, Cp, Kp, ipg;
+  int lazy;  // few scale groups: group maxima are written with the read-first atomic (lazy_max)
   FastDiv fTP, ftw, fipg, fC, fK;
 };
 
@@ -173,28 +174,30 @@ __global__ void __launch_bounds__(256) quant_input_kernel(const XT* __restrict__
   }
 }
 
-// fp32 input, W % 4 == 0, W <= 64: block = (row h, image n); thread = (4-pixel chunk w4 = tid & 15,
-// channel group of 4).  Each thread quantises a 4x4 (channel x pixel) block from 4 coalesced float4
-// loads, transposes it in registers into one 32-bit word per pixel (4 channels, PRMT) and stores the
-// words into a [W][Cp + 4] shared row (2-way bank conflicts at worst); the row leaves as coalesced
-// 32-bit words.  ~12 instructions per element (the generic kernel's per-item division and byte
-// stores cost ~30).
+// fp32 input, W % 4 == 0, W <= 64: block = (band of rh image rows, image n).  Per channel the band is one
+// contiguous run of rh * W floats of x (DRAM efficiency follows the length of such runs: row-sized
+// 224-byte pieces read at 5.1 TB/s, 4-row bands faster; tools/probe_ywrite.cu measured the same effect
+// on NCHW writes).  Thread = (float4 i of the band, channel group of 4): it quantises a 4x4 (channel x
+// pixel) block from 4 coalesced float4 loads, transposes it in registers into one 32-bit word per pixel
+// (4 channels, PRMT) and stores the words into a [rh * W][Cp + 4] shared band (2-way bank conflicts at
+// worst); the band leaves as coalesced 32-bit words (one contiguous rh * W * Cp byte range of c0).
+// ~12 instructions per element (the generic kernel's per-item division and byte stores cost ~30).
 #ifndef WL_QI_MINB
-#define WL_QI_MINB 4  // <= 64 registers: 4 row blocks per SM keep more loads in flight (0.89 -> 0.80 ms)
+#define WL_QI_MINB 4
 #endif
-// One image row (h, n) of quant_input_w64.
-__device__ __forceinline__ void quant_row_w64(const float* __restrict__ x, int8_t* __restrict__ c0, const Geo& g,
-                                              const StageQ& q, int h, int n, int8_t* srow) {
+__device__ __forceinline__ void quant_rows_w64(const float* __restrict__ x, int8_t* __restrict__ c0, const Geo& g,
+                                               const StageQ& q, int h0, int rh, int n, int8_t* srow) {
   const float rc = q.maxabs > 0.0 ? (float)((double)q.qmax / q.maxabs) : 0.f;
   const float thr = 0.5f - (float)((q.qmax + 1) * 1.25 * 5.9604644775390625e-8);
   const int ld = g.Cp + 4;
-  const int w4n = g.W >> 2, ncg = g.Cp >> 2;
-  const int w4 = threadIdx.x & 15;
-  if (w4 < w4n) {
+  const int nrow = min(rh, g.H - h0);
+  const int nf4 = (nrow * g.W) >> 2, ncg = g.Cp >> 2;  // float4s per channel band, channel groups
+  const int i = threadIdx.x % nf4, cg0 = threadIdx.x / nf4, cgstep = blockDim.x / nf4;
+  if (cg0 < cgstep) {
     const size_t cstride = (size_t)g.H * g.W;
-    const float* xb = x + ((size_t)n * g.C * g.H + h) * g.W + 4 * w4;
+    const float* xb = x + ((size_t)n * g.C * g.H + h0) * g.W + 4 * i;
 #pragma unroll 2
-    for (int cg = threadIdx.x >> 4; cg < ncg; cg += blockDim.x >> 4) {
+    for (int cg = cg0; cg < ncg; cg += cgstep) {
       // all four loads first (clamped channel, discarded below) so they are in flight together
       float4 v[4];
 #pragma unroll
@@ -220,25 +223,25 @@ __device__ __forceinline__ void quant_row_w64(const float* __restrict__ x, int8_
         }
       }
 #pragma unroll
-      for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(srow + (4 * w4 + p) * ld + 4 * cg) = wd[p];
+      for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(srow + (4 * i + p) * ld + 4 * cg) = wd[p];
     }
   }
   __syncthreads();
-  uint32_t* dst = reinterpret_cast<uint32_t*>(c0 + ((size_t)n * g.H + h) * g.W * g.Cp);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(c0 + ((size_t)n * g.H + h0) * g.W * g.Cp);
   const int wpr = g.Cp >> 2, lw = __ffs(wpr) - 1;  // 32-bit words per pixel (a power of two)
-  for (int i = threadIdx.x; i < g.W * wpr; i += blockDim.x) {
-    const int w = i >> lw, j = i & (wpr - 1);
-    dst[i] = *reinterpret_cast<const uint32_t*>(srow + w * ld + 4 * j);
+  for (int j = threadIdx.x; j < nrow * g.W * wpr; j += blockDim.x) {
+    const int pix = j >> lw, jw = j & (wpr - 1);
+    dst[j] = *reinterpret_cast<const uint32_t*>(srow + pix * ld + 4 * jw);
   }
 }
 
 template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
 __global__ void __launch_bounds__(256, WL_QI_MINB) quant_input_w64_kernel(const float* __restrict__ x, int8_t* __restrict__ c0,
-                                                              Geo g, Bits b, const Acc* __restrict__ acc) {
+                                                              Geo g, Bits b, const Acc* __restrict__ acc, int rh) {
   extern __shared__ __align__(16) int8_t srow[];
-  const int h = blockIdx.x, n = blockIdx.y;
+  const int h0 = blockIdx.x * rh, n = blockIdx.y;
   const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
-  quant_row_w64(x, c0, g, q, h, n, srow);
+  quant_rows_w64(x, c0, g, q, h0, rh, n, srow);
 }
 
 __device__ __forceinline__ void load_input_tile(const int8_t* __restrict__ c0, const Geo& g, int n, int tile, int c,

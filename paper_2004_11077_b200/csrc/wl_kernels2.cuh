@@ -95,22 +95,22 @@ __device__ __forceinline__ void load_planes(const HT* __restrict__ P, uint32_t p
 
 // Max of one (unit row t, channel c) into table entry t*ceil(C/32) + c/32 and the group running max.
 __device__ __forceinline__ void record_unit(float m, float tm, int grp, bool active, Acc* acc, int stage,
-                                            unsigned* table, int t, int c, int C) {
+                                            unsigned* table, int t, int c, int C, bool lazy = false) {
   bool uniform;
   float wmax;
   const int CB = (C + 31) >> 5;
   record_max(active ? m : 0.f, active ? grp : -1, table + (size_t)t * CB + (c >> 5), (C & 31) == 0, acc + stage,
              uniform, wmax);
-  publish_mf(active ? m : 0.f, active ? grp : -1, acc + stage, uniform, wmax);
+  publish_mf(active ? m : 0.f, active ? grp : -1, acc + stage, uniform, wmax, lazy);
   // group max of the first-half magnitudes (for the error bound)
   float tw = active ? tm : 0.f;
   if (uniform) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tw = fmaxf(tw, __shfl_xor_sync(0xffffffffu, tw, o));
     if ((threadIdx.x & 31) == 0 && grp >= 0 && tw > 0.f)
-      atomicMax(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tw));
+      lazy_max(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tw), lazy);
   } else if (active && grp >= 0 && tw > 0.f) {
-    atomicMax(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tw));
+    lazy_max(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tw), lazy);
   }
 }
 
@@ -253,8 +253,8 @@ __device__ __forceinline__ void record_unit_single(float m, float tm, int grp, A
                                                    int t, int c, int C) {
   const int CB = (C + 31) >> 5;
   atomicMax(table + (size_t)t * CB + (c >> 5), __float_as_uint(m));
-  if (m > 0.f) atomicMax(&acc[(size_t)grp * ST_COUNT + stage].MF, __float_as_uint(m));
-  if (tm > 0.f) atomicMax(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tm));
+  if (m > 0.f) lazy_max(&acc[(size_t)grp * ST_COUNT + stage].MF, __float_as_uint(m), true);
+  if (tm > 0.f) lazy_max(&acc[(size_t)grp * ST_COUNT + stage].TM, __float_as_uint(tm), true);
 }
 
 // Exact fix of one input_transform unit (V codes); inline fallback and fixup_it_kernel.
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(256) in_a_kernel(const int8_t* __restrict__ c0
     sandwich_cols<tab::Can_IT>(X, mx, &tm);
   else
     sandwich_cols<tab::Leg_IBC>(X, mx, &tm);
-  record_unit(m, tm, grp, active, acc, st, tabs.t[st], t, c, g.C);
+  record_unit(m, tm, grp, active, acc, st, tabs.t[st], t, c, g.C, g.lazy);
 }
 
 // Legendre: input_base_change codes c1 (stored) and input_transform maximum.
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(256, WL_MINB) in_b_kernel(const int8_t* __rest
     for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
   }, &tm);
   if (deferred) m = tm = 0.f;  // recorded by fixup_ibc_kernel from the exact codes
-  record_unit(m, tm, grp, active, acc, ST_IT, tabs.t[ST_IT], t, c, g.C);
+  record_unit(m, tm, grp, active, acc, ST_IT, tabs.t[ST_IT], t, c, g.C, g.lazy);
 }
 
 // V codes.  Canonical: from c0 through B^T.  Legendre: from the stored c1 through B_P^T.
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(256) out_a_kernel(const HT* __restrict__ h, Ge
       for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
     }, &tm);
   }
-  record_unit(m, tm, grp, active, acc, st, tabs.t[st], t, k, g.K);
+  record_unit(m, tm, grp, active, acc, st, tabs.t[st], t, k, g.K, g.lazy);
 }
 
 // Legendre: output_base_change codes c4 (stored) and cropped output maximum.
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(256, WL_MINB) out_b_kernel(const HT* __restric
       if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[i]));
   }, &tm);
   if (deferred) m = tm = 0.f;  // recorded by fixup_obc_kernel from the exact codes
-  record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K);
+  record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], t, k, g.K, g.lazy);
 }
 
 // Final output: codes of the output stage, dequantised (snap +-qmax to +-max_abs), + bias, NCHW in

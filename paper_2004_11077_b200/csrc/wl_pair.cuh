@@ -229,7 +229,8 @@ __device__ __forceinline__ void staged_loop2(const Geo& g, int nch, const void* 
 // record_unit for a thread holding channels c, c+1 (c even): a 16-lane half-warp covers the 32
 // channels of one table entry (t, c >> 5).
 __device__ __forceinline__ void record_unit2(float m0, float m1, float tm0, float tm1, int grp, bool a0, bool a1,
-                                             Acc* acc, int stage, unsigned* table, int t, int c, int C) {
+                                             Acc* acc, int stage, unsigned* table, int t, int c, int C,
+                                             bool lazy = false) {
   const unsigned full = 0xffffffffu;
   const bool active = a0 || a1;
   const float m = fmaxf(a0 ? m0 : 0.f, a1 ? m1 : 0.f);
@@ -250,13 +251,13 @@ __device__ __forceinline__ void record_unit2(float m0, float m1, float tm0, floa
     w = fmaxf(w, __shfl_xor_sync(full, w, 16));
     tw = fmaxf(tw, __shfl_xor_sync(full, tw, 16));
     if ((threadIdx.x & 31) == 0 && g >= 0) {
-      if (w > 0.f) atomicMax(&acc[(size_t)g * ST_COUNT + stage].MF, __float_as_uint(w));
-      if (tw > 0.f) atomicMax(&acc[(size_t)g * ST_COUNT + stage].TM, __float_as_uint(tw));
+      if (w > 0.f) lazy_max(&acc[(size_t)g * ST_COUNT + stage].MF, __float_as_uint(w), lazy);
+      if (tw > 0.f) lazy_max(&acc[(size_t)g * ST_COUNT + stage].TM, __float_as_uint(tw), lazy);
     }
   } else if (g >= 0) {
     atomicMax(entry, __float_as_uint(m));
-    if (m > 0.f) atomicMax(&acc[(size_t)g * ST_COUNT + stage].MF, __float_as_uint(m));
-    if (tm > 0.f) atomicMax(&acc[(size_t)g * ST_COUNT + stage].TM, __float_as_uint(tm));
+    if (m > 0.f) lazy_max(&acc[(size_t)g * ST_COUNT + stage].MF, __float_as_uint(m), lazy);
+    if (tm > 0.f) lazy_max(&acc[(size_t)g * ST_COUNT + stage].TM, __float_as_uint(tm), lazy);
   }
 }
 
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, WL_MINB)
 #pragma unroll
       for (int i = 0; i < 6; ++i) amax2(m0, m1, col[i]);
     }, &tm0, &tm1);
-    record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, stg, tabs.t[stg], tt, c, g.C);
+    record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, stg, tabs.t[stg], tt, c, g.C, g.lazy);
   });
 }
 
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(Staged2<LD, sizeof(HT)>::THREADS, WL_MINB)
         for (int i = 0; i < 6; ++i) amax2(m0, m1, col[i]);
       }, &tm0, &tm1);
     }
-    record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, stg, tabs.t[stg], tt, k, g.K);
+    record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, stg, tabs.t[stg], tt, k, g.K, g.lazy);
   });
 }
 
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, 2)
     }, &tm0, &tm1);
     if (def0) m0 = tm0 = 0.f;  // recorded by fixup_ibc_kernel from the exact codes
     if (def1) m1 = tm1 = 0.f;
-    record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, ST_IT, tabs.t[ST_IT], tt, c, g.C);
+    record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, ST_IT, tabs.t[ST_IT], tt, c, g.C, g.lazy);
   }, c1);
 }
 
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(StagedT42<LD, sizeof(HT)>::THREADS, 2)
     }
     if (def0) m0 = tm0 = 0.f;  // recorded by fixup_obct_kernel from the exact codes
     if (def1) m1 = tm1 = 0.f;
-    record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, ST_OUT, tabs.t[ST_OUT], tt, k, g.K);
+    record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, ST_OUT, tabs.t[ST_OUT], tt, k, g.K, g.lazy);
     fence_proxy_async_smem();
     if (threadIdx.x == 0) bulk_wait_read<0>();  // the store issued last iteration has read buffer s^1
     __syncthreads();

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(Staged<LD, 1>::THREADS, WL_MINB)
       sandwich_cols<tab::Can_IT>(X, mx, &tm);
     else
       sandwich_cols<tab::Leg_IBC>(X, mx, &tm);
-    record_unit(m, tm, grp, active, acc, stg, tabs.t[stg], active ? t : 0, c, g.C);
+    record_unit(m, tm, grp, active, acc, stg, tabs.t[stg], active ? t : 0, c, g.C, g.lazy);
   });
 }
 
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(Staged<LD, 1>::THREADS, WL_MINB)
       for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
     }, &tm);
     if (deferred) m = tm = 0.f;  // recorded by fixup_ibc_kernel from the exact codes
-    record_unit(m, tm, grp, active, acc, ST_IT, tabs.t[ST_IT], tt, c, g.C);
+    record_unit(m, tm, grp, active, acc, ST_IT, tabs.t[ST_IT], tt, c, g.C, g.lazy);
   }, c1);
 }
 
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(Staged<LD, sizeof(HT)>::THREADS, WL_MINB)
         for (int i = 0; i < 6; ++i) m = fmaxf(m, fabsf(col[i]));
       }, &tm);
     }
-    record_unit(m, tm, grp, active, acc, stg, tabs.t[stg], tt, k, g.K);
+    record_unit(m, tm, grp, active, acc, stg, tabs.t[stg], tt, k, g.K, g.lazy);
   });
 }
 
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(Staged<LD, sizeof(HT)>::THREADS, WL_MINB)
         if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[i]));
     }, &tm);
     if (deferred) m = tm = 0.f;  // recorded by fixup_obc_kernel from the exact codes
-    record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], tt, k, g.K);
+    record_unit(m, tm, grp, active, acc, ST_OUT, tabs.t[ST_OUT], tt, k, g.K, g.lazy);
   }, c4);
 }
 
@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
     sout_cw_kernel(const __grid_constant__ CUtensorMap t4map, const HT* __restrict__ h, float* __restrict__ y,
                    const float* __restrict__ bias, const __grid_constant__ Geo g, const __grid_constant__ Bits b,
                    const Acc* __restrict__ acc, const PlanF64* __restrict__ pf, const float* __restrict__ otab,
-                   const float4* __restrict__ odq, FixList fl, const CwShape sh) {
+                   const float4* __restrict__ odq, FixList fl, const CwShape sh, const float* __restrict__ t4e) {
   using S = StagedCw;
   extern __shared__ __align__(128) uint8_t wl_stage_smem[];
   uint8_t* sm = wl_stage_smem;
@@ -630,9 +630,24 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
   }
   __syncthreads();
   auto issue = [&](int it, int s) {
+#ifdef WL_CW_CBSLOW
+    const int ntg_ = (g.T + sh.R - 1) / sh.R;
+    const int cb = it / ntg_, tg = it - cb * ntg_;
+#else
     const int tg = it / ncb, cb = it - tg * ncb;
+#endif
+#ifndef WL_CW_TMA3D
+    // per channel group the item's tiles are one contiguous range of T4E: CG linear bulk copies
+    const int t0 = tg * sh.R, nt = min(sh.R, g.T - t0);
+    const int ncg = min(sh.CG, g.Kp / 4 - cb * sh.CG);
+    mbar_arrive_expect_tx(&full[s], (uint32_t)(ncg * nt * 272));
+    for (int q = 0; q < ncg; ++q)
+      bulk_g2s(sm + s * S::STAGE_BYTES + q * sh.R * 272, t4e + ((size_t)(cb * sh.CG + q) * g.T + t0) * 68,
+               (uint32_t)(nt * 272), &full[s]);
+#else
     mbar_arrive_expect_tx(&full[s], box_bytes);
     tma_load_3d(sm + s * S::STAGE_BYTES, &t4map, &full[s], 0, tg * sh.R, cb * sh.CG);
+#endif
   };
   if (threadIdx.x == 0)
 #pragma unroll
@@ -647,7 +662,12 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
       if (f >= 1) mbar_wait(&empty[j % NS], (uint32_t)((f - 1) & 1));
       issue(it + (NS - 1) * gridDim.x, j % NS);
     }
+#ifdef WL_CW_CBSLOW
+    const int ntg_ = (g.T + sh.R - 1) / sh.R;
+    const int cb = it / ntg_, tg = it - cb * ntg_;
+#else
     const int tg = it / ncb, cb = it - tg * ncb;
+#endif
     const int t = tg * sh.R + tin, k = (cb * sh.CG + cgi) * 4 + ch;
     const bool active = lane_on && t < g.T && k < g.K;
     const int tt = active ? t : 0;
@@ -671,7 +691,7 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
       const f2 r2 = bc2(r), nr2 = bc2(-r), shi = bc2(dq.x), slo = bc2(dq.y), bk2 = bc2(bk), mg = bc2(kMagic);
 #pragma unroll
       for (int e = 0; e < 16; e += 2) {
-        const f2 T = mk2(p[e * 4], p[(e + 1) * 4]);
+        const f2 T = active ? mk2(p[e * 4], p[(e + 1) * 4]) : bc2(0.f);  // idle lanes: slot not filled
         const f2 k2 = sub2(fma2(T, r2, mg), mg);
         const f2 d = fma2(T, nr2, k2);
         dmax = fmaxf(dmax, fmaxf(fabsf(lo2(d)), fabsf(hi2(d))));
@@ -687,7 +707,7 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
         float o2[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int code = rq_col(p[(e + u) * 4], r, kd, dmax);
+          const int code = rq_col(active ? p[(e + u) * 4] : 0.f, r, kd, dmax);
           if constexpr (TAB)
             o2[u] = __ldg(tabg + code) + bk;
           else
@@ -696,11 +716,14 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
         v[e >> 1] = mk2(o2[0], o2[1]);
       }
     }
-    const float efac = p[64];
+    const float efac = active ? p[64] : 0.f;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // every lane's reads of the slot are done
     const bool want = fmaf(ef, efac, dmax) > thr && active;
     bool skip = !active;
+#ifdef WL_CW_NOSTORE
+    skip = dmax != 12345.f;
+#endif
     if (__any_sync(0xffffffffu, want) && want &&
         !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want)) {
       exact_out_unit_to_y<HT>(h, y, bias, g, b, acc, pf, t, k);
