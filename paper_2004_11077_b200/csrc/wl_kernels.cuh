@@ -18,6 +18,7 @@
 // T = N * TP tiles, TP = ceil(Ho/4)*ceil(Wo/4); element xi = 6*i + j of a 6x6 tile.
 #pragma once
 #include "wl_core.cuh"
+#include "wl_f2.cuh"
 
 namespace wl {
 
@@ -203,24 +204,35 @@ __device__ __forceinline__ void quant_rows_w64(const float* __restrict__ x, int8
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         v[u] = __ldg(reinterpret_cast<const float4*>(xb + (size_t)min(4 * cg + u, g.C - 1) * cstride));
+      // pixel pairs on packed f32x2: y = fma(v, rc, 1.5 * 2^23) holds the signed half-even code in its low
+      // byte (rint is odd-symmetric, so this equals the sign * rint(|v| * rc) of quant_fast); d = fma(v,
+      // -rc, k) is the distance to that integer.  |v| * rc <= qmax * (1 + 2^-24), so no clamp is needed.
       uint32_t wd[4] = {0u, 0u, 0u, 0u};
+      constexpr uint32_t kSel[4] = {0x3214u, 0x3240u, 0x3410u, 0x4210u};  // byte u of word p <- low byte of code
+      const f2 rc2 = bc2(rc), nrc2 = bc2(-rc), mg = bc2(kMagic);
+      float dmax = 0.f;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (4 * cg + u < g.C) {
-          bool bad = false;
-          int k0 = quant_fast(v[u].x, rc, thr, q.qmax, bad), k1 = quant_fast(v[u].y, rc, thr, q.qmax, bad);
-          int k2 = quant_fast(v[u].z, rc, thr, q.qmax, bad), k3 = quant_fast(v[u].w, rc, thr, q.qmax, bad);
-          if (bad) {  // some element within the fp32 band of a half-integer: the exact path decides
-            k0 = quant_code(v[u].x, rc, thr, q.scale, q.qmax), k1 = quant_code(v[u].y, rc, thr, q.scale, q.qmax);
-            k2 = quant_code(v[u].z, rc, thr, q.scale, q.qmax), k3 = quant_code(v[u].w, rc, thr, q.scale, q.qmax);
-          }
-          // byte u of word p <- low byte of code k_p
-          constexpr uint32_t kSel[4] = {0x3214u, 0x3240u, 0x3410u, 0x4210u};
-          wd[0] = __byte_perm(wd[0], (uint32_t)k0, kSel[u]);
-          wd[1] = __byte_perm(wd[1], (uint32_t)k1, kSel[u]);
-          wd[2] = __byte_perm(wd[2], (uint32_t)k2, kSel[u]);
-          wd[3] = __byte_perm(wd[3], (uint32_t)k3, kSel[u]);
+          const f2 va = mk2(v[u].x, v[u].y), vb = mk2(v[u].z, v[u].w);
+          const f2 ya = fma2(va, rc2, mg), yb = fma2(vb, rc2, mg);
+          const f2 da = fma2(va, nrc2, sub2(ya, mg)), db = fma2(vb, nrc2, sub2(yb, mg));
+          dmax = fmaxf(dmax, fmaxf(fmaxf(fabsf(lo2(da)), fabsf(hi2(da))), fmaxf(fabsf(lo2(db)), fabsf(hi2(db)))));
+          wd[0] = __byte_perm(wd[0], __float_as_uint(lo2(ya)), kSel[u]);
+          wd[1] = __byte_perm(wd[1], __float_as_uint(hi2(ya)), kSel[u]);
+          wd[2] = __byte_perm(wd[2], __float_as_uint(lo2(yb)), kSel[u]);
+          wd[3] = __byte_perm(wd[3], __float_as_uint(hi2(yb)), kSel[u]);
         }
+      }
+      if (dmax > thr) {  // some element within the fp32 band of a half-integer: the exact path decides
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (4 * cg + u < g.C) {
+            wd[0] = __byte_perm(wd[0], (uint32_t)quant_code(v[u].x, rc, thr, q.scale, q.qmax), kSel[u]);
+            wd[1] = __byte_perm(wd[1], (uint32_t)quant_code(v[u].y, rc, thr, q.scale, q.qmax), kSel[u]);
+            wd[2] = __byte_perm(wd[2], (uint32_t)quant_code(v[u].z, rc, thr, q.scale, q.qmax), kSel[u]);
+            wd[3] = __byte_perm(wd[3], (uint32_t)quant_code(v[u].w, rc, thr, q.scale, q.qmax), kSel[u]);
+          }
       }
 #pragma unroll
       for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(srow + (4 * i + p) * ld + 4 * cg) = wd[p];
