@@ -79,14 +79,14 @@ SLOT_KERNELS = {
     "gemm_hadamard_codes": ("gemm_i8_persistent<256, 128, 3, EpiHadRq", "gemm_i8_bstat<EpiHadRq", "fixup_had_kernel"),
     "output_base_change_max": ("sout_a2_kernel", "finalize_output_kernel<1, 7", "finalize_output_exec<1, 7"),
     "output_max": ("sout_bt2_kernel", "fixup_obct_kernel", "finalize_output_kernel<1, 8", "finalize_output_exec<1, 8"),
-    "output_write": ("out_table_kernel", "sout_ct_kernel", "fixup_outt_kernel"),
+    "output_write": ("out_table_kernel", "sout_cw_kernel", "fixup_outt_kernel"),
 }
-NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_cfg4.csv")
+NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_cfg4_v2.csv")
 
 
 def ncu_traffic(slot):
     """DRAM bytes (read + write) per launch of a profile slot from the committed `ncu --set full` capture
-    of one config-4 forward (profiles/r02_ncu_full_cfg4.csv, tools/ncu_full_cfg4.sh), or None."""
+    of one config-4 forward (profiles/r02_ncu_full_cfg4_v2.csv, tools/r02_profile.sh), or None."""
     try:
         with open(NCU_FULL) as fh:
             rows = list(csv.reader(fh))
@@ -106,7 +106,9 @@ def ncu_traffic(slot):
 
 
 def kernel_units(name, n, c, k, hw, pad, hbytes=1):
-    """Algorithmic (compulsory) bytes and int8 ops of one launch of each forward slot."""
+    """Algorithmic bytes (what the pass must read and write: its input codes / values and the codes / values it
+    produces, each once; c1 = [T][36][Cp] like V, T4E = 17 floats per unit) and int8 ops of one launch of each
+    forward slot."""
     ho = hw + 2 * pad - 2
     T = n * (-(-ho // 4)) ** 2
     p2 = lambda v, lo: lo if v <= lo else 1 << (v - 1).bit_length()  # noqa: E731  (wl_internal.h pow2_at_least)
@@ -114,9 +116,9 @@ def kernel_units(name, n, c, k, hw, pad, hbytes=1):
     x, c0, V, U, h, y = 4 * n * c * hw * hw, n * hw * hw * cp, 36 * T * cp, 36 * kp * cp, 36 * T * kp * hbytes, 4 * n * k * ho * ho
     table = {
         "absmax_input": (x, 0), "quant_input": (x + c0, 0),
-        "input_base_change_max": (c0, 0), "input_transform_max": (c0, 0), "input_transform_codes": (c0 + V, 0),
+        "input_base_change_max": (c0, 0), "input_transform_max": (c0 + V, 0), "input_transform_codes": (2 * V, 0),
         "gemm_hadamard_max": (V + U, 2 * 36 * T * cp * kp), "gemm_hadamard_codes": (V + U + h, 2 * 36 * T * cp * kp),
-        "output_base_change_max": (h, 0), "output_max": (h, 0), "output_write": (h + y, 0),
+        "output_base_change_max": (h, 0), "output_max": (h + 17 * T * kp * 4, 0), "output_write": (17 * T * kp * 4 + y, 0),
     }
     return table.get(name, (0, 0))
 
@@ -430,10 +432,17 @@ def run_ours(args, rank, world, local_rank):
         roof = {"kernel": dom, "bound": "hbm", "achieved": kb / (dom_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(dom)
-    roof["traffic_source"] = "profiles/r02_ncu_full_cfg4.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
+    roof["traffic_source"] = "profiles/r02_ncu_full_cfg4_v2.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
     roof["algorithmic_bytes_per_launch"] = kb
     roof["ms_per_launch"] = dom_ms
     roof["peak_source"] = peak_kind if roof["bound"] == "hbm" else ("torch._int_mm 8192^3 measured live" if i8_peak else "2x bf16 planning")
+    # every slot against the same two ceilings (the transform passes are FMA-pipe bound: profiles/ ncu rows)
+    slots = {}
+    for name, v in per_kernel.items():
+        sb, sops = kernel_units(name, n, c, k, hw, pad)
+        t_floor = max(sb / (hbm * 1e9), sops / ((i8_peak or 2 * bf16) * 1e12) if sops else 0.0)
+        slots[name] = {"ms": round(v, 4), "algorithmic_gb": round(sb / 1e9, 3),
+                       "roof_frac": round(t_floor / (v * 1e-3), 3) if v > 0 else None}
     value = world * n / (ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
@@ -448,6 +457,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roof,
         "per_rank_ms": per_rank_ms,
         "kernel_ms": {kname: round(v, 4) for kname, v in per_kernel.items()},
+        "kernel_roofline": slots,
         "gpu_launches": launches * args.steps,
         "clocks": clk,
         "e2e": e2e,

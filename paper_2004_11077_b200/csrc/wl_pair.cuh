@@ -421,8 +421,8 @@ __device__ __forceinline__ void t4_of_unit2(const f2 (&K4)[6][6], int ty, int tx
       if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) amax2(m0, m1, col[i]);
     }
   }, &tm0, &tm1);
-  ef0 = cx0 * max_row_abs_sum<tab::Leg_OT>();
-  ef1 = cx1 * max_row_abs_sum<tab::Leg_OT>();
+  ef0 = cx0;  // max |first-half value| of the unit: sout_cw forms the per-row band rowsum_i * ef
+  ef1 = cx1;
 }
 
 template <int LD, int EB>

@@ -502,7 +502,7 @@ __device__ __forceinline__ void t4_of_unit(const float (&K4)[6][6], int ty, int 
       if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) m = fmaxf(m, fabsf(col[i]));
     }
   }, &tm);
-  efac = cmax * max_row_abs_sum<tab::Leg_OT>();
+  efac = cmax;  // max |first-half value| of the unit: sout_cw forms the per-row band rowsum_i * efac
 }
 
 // Rare inline fallback of sout_bt (fix list full): exact c4 from h, then T4 / e4 of the unit written
@@ -573,7 +573,8 @@ __device__ __noinline__ void exact_out_unit_to_y(const HT* __restrict__ h, float
 }
 
 // Final output pass from T4E (Legendre, fp32 output).  T4E = [Kp/4 channel groups][T tiles][17][4
-// channels] floats: rows 0..15 the output stage's fp32 values T4 of the unit, row 16 its error factor.
+// channels] floats: rows 0..15 the output stage's fp32 values T4 of the unit, row 16 the unit's max
+// |first-half value| (the per-row error band is rowsum_i times it).
 // Work item = R consecutive tiles x CG channel groups = one TMA box {68, R, CG}; the 8 warps are
 // (pass, channel group) pairs, lane = (tile slot, channel) = (lane >> 2, lane & 3), a pass covers TPP <= 8
 // tiles.  In that mapping
@@ -684,7 +685,7 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
     const float* p =
         reinterpret_cast<const float*>(sm + s * S::STAGE_BYTES) + (cgi * sh.R + (lane_on ? tin : 0)) * 68 + ch;
     f2 v[8];
-    float dmax = 0.f;
+    float dm[4] = {0.f, 0.f, 0.f, 0.f};  // per output row: max distance of T * r to its rounded code
     if (TAB && dq.z != 0.f) {
       // certified arithmetic dequantisation (out_table_kernel): value = fma(k, s_hi, k * s_lo) + bias.
       // fma(T, -r, k) is the exact negation of rq_col's fma(T, r, -k), so dmax is the same number.
@@ -694,7 +695,7 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
         const f2 T = active ? mk2(p[e * 4], p[(e + 1) * 4]) : bc2(0.f);  // idle lanes: slot not filled
         const f2 k2 = sub2(fma2(T, r2, mg), mg);
         const f2 d = fma2(T, nr2, k2);
-        dmax = fmaxf(dmax, fmaxf(fabsf(lo2(d)), fabsf(hi2(d))));
+        dm[e >> 2] = fmaxf(dm[e >> 2], fmaxf(fabsf(lo2(d)), fabsf(hi2(d))));
         v[e >> 1] = add2(fma2(k2, shi, mul2(k2, slo)), bk2);
       }
     } else {
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
         float o2[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int code = rq_col(active ? p[(e + u) * 4] : 0.f, r, kd, dmax);
+          const int code = rq_col(active ? p[(e + u) * 4] : 0.f, r, kd, dm[e >> 2]);
           if constexpr (TAB)
             o2[u] = __ldg(tabg + code) + bk;
           else
@@ -719,7 +720,12 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
     const float efac = active ? p[64] : 0.f;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // every lane's reads of the slot are done
-    const bool want = fmaf(ef, efac, dmax) > thr && active;
+    // certified band of element (i, j): ef * rowsum(A_P^T row i) * max |first-half value| (>= column j's)
+    const float eb = ef * efac;
+    bool want = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) want |= fmaf(eb, row_abs_sum<tab::Leg_OT>(i), dm[i]) > thr;
+    want = want && active;
     bool skip = !active;
 #ifdef WL_CW_NOSTORE
     skip = dmax != 12345.f;

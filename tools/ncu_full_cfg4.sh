@@ -7,5 +7,5 @@ python tools/prof_forward.py --n 1024 --iters 2 > gpurun_out/plain_cfg4.log 2>&1
 ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k regex:"wl::" -c 60 -o /tmp/prof_cfg4 python tools/prof_forward.py --n 1024 --iters 2 > gpurun_out/ncu_cfg4.log 2>&1
 python tools/ncu_summary.py /tmp/prof_cfg4.ncu-rep gpurun_out/ncu_full_cfg4.csv > /dev/null
-ncu -i /tmp/prof_cfg4.ncu-rep --page source --csv --print-source sass -k regex:sout_ct > gpurun_out/source_sout_ct.csv 2>/dev/null
+ncu -i /tmp/prof_cfg4.ncu-rep --page source --csv --print-source sass -k regex:sout_cw > gpurun_out/source_sout_cw.csv 2>/dev/null
 ls -la gpurun_out/
