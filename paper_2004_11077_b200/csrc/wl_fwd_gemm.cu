@@ -20,7 +20,7 @@ namespace wl {
 struct EpiHadMax {
   static constexpr int kGroups = 4;
   static constexpr int kStageBytes = 0;
-  static constexpr bool kNarrow = false;
+  static constexpr bool kDeferSlow = false;
   Acc* acc;
   unsigned* table;
   Geo g;
@@ -117,7 +117,7 @@ struct EpiHadRq {
   // each epilogue warp stages its 32 rows x 128 columns of codes (swizzled 16-byte slots) and
   // writes them back as whole row segments
   static constexpr int kGroups = WL_RQ_GROUPS;
-  static constexpr bool kNarrow = WL_RQ_GROUPS == 4;
+  static constexpr bool kDeferSlow = true;
   static constexpr int kStageBytes = 32 * (256 / kGroups) * (int)sizeof(HT);
   static constexpr int kRowBytes = (256 / kGroups) * (int)sizeof(HT);
   static constexpr int kSwz = kRowBytes / 16 - 1;  // XOR swizzle of the 16-byte slots within a row
@@ -161,7 +161,10 @@ struct EpiHadRq {
     r_hi = __fmul_ru(a.r, 1.f + 2.384185791015625e-7f);
     small = (long long)g.C * qmax_u * qmax_v < (1LL << 22);
   }
-  __device__ __forceinline__ void apply(int xi, int row, int col, const uint32_t* v, int n) {
+  // Fast path of 16 consecutive columns starting at local column lc of this warp's slice: codes from the
+  // r_lo evaluation are staged unconditionally; returns true if some element's [r_lo, r_hi] bracket
+  // split (then apply_slow redoes the chunk).
+  __device__ __forceinline__ bool apply_fast(const uint32_t* v, int lc) {
     // y[j] = 0x4B400000 + code: its low byte / half-word is the two's-complement code
     uint32_t y[16];
     uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;  // independent chains (ILP)
@@ -186,36 +189,40 @@ struct EpiHadRq {
         if ((j & 3) == 0) d0 |= d; else if ((j & 3) == 1) d1 |= d; else if ((j & 3) == 2) d2 |= d; else d3 |= d;
       }
     }
-    const bool exact = ((d0 | d1) | (d2 | d3)) != 0;  // rare: some element's bracket split
     const int lane = threadIdx.x & 31;
-    const int slot0 = ((col % hc) * (int)sizeof(HT)) >> 4;
+    const int slot0 = (lc * (int)sizeof(HT)) >> 4;
     const uint32_t rbase = smem_u32(stage) + lane * kRowBytes;
-    const HadRqCtx cx{acc, wacc, U, V, g.C, g.Cp, g.Kp, grp, wstage, qmax_u, qmax_v, qmax_h, xi, row, fl};
     if constexpr (sizeof(HT) == 1) {
       uint32_t w[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         w[q] = __byte_perm(__byte_perm(y[4 * q], y[4 * q + 1], 0x0040), __byte_perm(y[4 * q + 2], y[4 * q + 3], 0x0040),
                            0x5410);
-      if (exact) {
-        const uint4 lo = had_rq_slow8<HT>(cx, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]), col, n);
-        const uint4 hi = had_rq_slow8<HT>(cx, make_uint4(v[8], v[9], v[10], v[11]), make_uint4(v[12], v[13], v[14], v[15]),
-                                          col + 8, n - 8);
-        w[0] = lo.x, w[1] = lo.y, w[2] = hi.x, w[3] = hi.y;
-      }
       st_shared_v4(rbase + ((slot0 ^ (lane & kSwz)) << 4), w[0], w[1], w[2], w[3]);
     } else {
       uint32_t w[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) w[q] = __byte_perm(y[2 * q], y[2 * q + 1], 0x5410);
-      if (exact) {
-        const uint4 lo = had_rq_slow8<HT>(cx, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]), col, n);
-        const uint4 hi = had_rq_slow8<HT>(cx, make_uint4(v[8], v[9], v[10], v[11]), make_uint4(v[12], v[13], v[14], v[15]),
-                                          col + 8, n - 8);
-        w[0] = lo.x, w[1] = lo.y, w[2] = lo.z, w[3] = lo.w, w[4] = hi.x, w[5] = hi.y, w[6] = hi.z, w[7] = hi.w;
-      }
       st_shared_v4(rbase + ((slot0 ^ (lane & kSwz)) << 4), w[0], w[1], w[2], w[3]);
       st_shared_v4(rbase + (((slot0 + 1) ^ (lane & kSwz)) << 4), w[4], w[5], w[6], w[7]);
+    }
+    return ((d0 | d1) | (d2 | d3)) != 0;  // rare: some element's bracket split
+  }
+  // Exact redo of a flagged chunk (int64 rounding, ties deferred to fixup_had_kernel): overwrites the
+  // staged codes of the 16 columns at local column lc.
+  __device__ __forceinline__ void apply_slow(int xi, int row, int col, const uint32_t* v, int n, int lc) {
+    const int lane = threadIdx.x & 31;
+    const int slot0 = (lc * (int)sizeof(HT)) >> 4;
+    const uint32_t rbase = smem_u32(stage) + lane * kRowBytes;
+    const HadRqCtx cx{acc, wacc, U, V, g.C, g.Cp, g.Kp, grp, wstage, qmax_u, qmax_v, qmax_h, xi, row, fl};
+    const uint4 lo = had_rq_slow8<HT>(cx, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]), col, n);
+    const uint4 hi = had_rq_slow8<HT>(cx, make_uint4(v[8], v[9], v[10], v[11]), make_uint4(v[12], v[13], v[14], v[15]),
+                                      col + 8, n - 8);
+    if constexpr (sizeof(HT) == 1) {
+      st_shared_v4(rbase + ((slot0 ^ (lane & kSwz)) << 4), lo.x, lo.y, hi.x, hi.y);
+    } else {
+      st_shared_v4(rbase + ((slot0 ^ (lane & kSwz)) << 4), lo.x, lo.y, lo.z, lo.w);
+      st_shared_v4(rbase + (((slot0 + 1) ^ (lane & kSwz)) << 4), hi.x, hi.y, hi.z, hi.w);
     }
   }
   __device__ __forceinline__ void finish_chunk(int, int, bool, int) {}

@@ -575,7 +575,7 @@ __device__ __noinline__ void exact_out_unit_to_y(const HT* __restrict__ h, float
 // Final output pass from T4E (Legendre, fp32 output).  T4E = [Kp/4 channel groups][T tiles][17][4
 // channels] floats: rows 0..15 the output stage's fp32 values T4 of the unit, row 16 the unit's max
 // |first-half value| (the per-row error band is rowsum_i times it).
-// Work item = R consecutive tiles x CG channel groups = one TMA box {68, R, CG}; the 8 warps are
+// Work item = R consecutive tiles x CG channel groups, staged as [CG][R][68] floats; the 8 warps are
 // (pass, channel group) pairs, lane = (tile slot, channel) = (lane >> 2, lane & 3), a pass covers TPP <= 8
 // tiles.  In that mapping
 //   * the staged reads are conflict-free: a unit starts 68 floats (4 banks) after its neighbour tile,
@@ -602,10 +602,10 @@ struct StagedCw {
 
 template <typename HT, bool TAB, int NS>
 __global__ void __launch_bounds__(StagedCw::THREADS, 4)
-    sout_cw_kernel(const __grid_constant__ CUtensorMap t4map, const HT* __restrict__ h, float* __restrict__ y,
+    sout_cw_kernel(const float* __restrict__ t4e, const HT* __restrict__ h, float* __restrict__ y,
                    const float* __restrict__ bias, const __grid_constant__ Geo g, const __grid_constant__ Bits b,
                    const Acc* __restrict__ acc, const PlanF64* __restrict__ pf, const float* __restrict__ otab,
-                   const float4* __restrict__ odq, FixList fl, const CwShape sh, const float* __restrict__ t4e) {
+                   const float4* __restrict__ odq, FixList fl, const CwShape sh) {
   using S = StagedCw;
   extern __shared__ __align__(128) uint8_t wl_stage_smem[];
   uint8_t* sm = wl_stage_smem;
@@ -618,7 +618,6 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
   const int pass = w / sh.CG, cgi = w - pass * sh.CG;
   const int tin = pass * sh.TPP + slot;                 // tile of the item this lane owns
   const bool lane_on = slot < sh.TPP && tin < sh.R;
-  const uint32_t box_bytes = (uint32_t)(sh.R * sh.CG * 68 * 4);
   const int qo = b.q[ST_OUT];
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -627,17 +626,10 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
       mbar_init(&empty[q], S::THREADS / 32);
     }
     fence_mbar_init();
-    tma_prefetch_desc(&t4map);
   }
   __syncthreads();
   auto issue = [&](int it, int s) {
-#ifdef WL_CW_CBSLOW
-    const int ntg_ = (g.T + sh.R - 1) / sh.R;
-    const int cb = it / ntg_, tg = it - cb * ntg_;
-#else
     const int tg = it / ncb, cb = it - tg * ncb;
-#endif
-#ifndef WL_CW_TMA3D
     // per channel group the item's tiles are one contiguous range of T4E: CG linear bulk copies
     const int t0 = tg * sh.R, nt = min(sh.R, g.T - t0);
     const int ncg = min(sh.CG, g.Kp / 4 - cb * sh.CG);
@@ -645,10 +637,6 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
     for (int q = 0; q < ncg; ++q)
       bulk_g2s(sm + s * S::STAGE_BYTES + q * sh.R * 272, t4e + ((size_t)(cb * sh.CG + q) * g.T + t0) * 68,
                (uint32_t)(nt * 272), &full[s]);
-#else
-    mbar_arrive_expect_tx(&full[s], box_bytes);
-    tma_load_3d(sm + s * S::STAGE_BYTES, &t4map, &full[s], 0, tg * sh.R, cb * sh.CG);
-#endif
   };
   if (threadIdx.x == 0)
 #pragma unroll
@@ -663,12 +651,7 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
       if (f >= 1) mbar_wait(&empty[j % NS], (uint32_t)((f - 1) & 1));
       issue(it + (NS - 1) * gridDim.x, j % NS);
     }
-#ifdef WL_CW_CBSLOW
-    const int ntg_ = (g.T + sh.R - 1) / sh.R;
-    const int cb = it / ntg_, tg = it - cb * ntg_;
-#else
     const int tg = it / ncb, cb = it - tg * ncb;
-#endif
     const int t = tg * sh.R + tin, k = (cb * sh.CG + cgi) * 4 + ch;
     const bool active = lane_on && t < g.T && k < g.K;
     const int tt = active ? t : 0;
@@ -727,9 +710,6 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
     for (int i = 0; i < 4; ++i) want |= fmaf(eb, row_abs_sum<tab::Leg_OT>(i), dm[i]) > thr;
     want = want && active;
     bool skip = !active;
-#ifdef WL_CW_NOSTORE
-    skip = dmax != 12345.f;
-#endif
     if (__any_sync(0xffffffffu, want) && want &&
         !defer_fix(fl, FIX_OUT, (unsigned)t * (unsigned)g.K + (unsigned)k, want)) {
       exact_out_unit_to_y<HT>(h, y, bias, g, b, acc, pf, t, k);
