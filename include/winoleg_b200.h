@@ -75,7 +75,9 @@ int wl_weight_transform(const wl_plan* plan, const wl_qcfg* q, const float* w, i
 int wl_weight_transform_f64(const wl_plan* plan, const wl_qcfg* q, const double* w, int c_out, int c_in, void* cache,
                             size_t cache_bytes, void* stream);
 
-/* Forward: y [n][c_out][h+2pad-2][w+2pad-2] fp32 = dequantised output codes (+ bias if non-NULL). */
+/* Forward: y [n][c_out][h+2pad-2][w+2pad-2] fp32 = dequantised output codes (+ bias if non-NULL).
+ * workspace (and the saved buffer of wl_forward_train) must be 256-byte aligned device memory (WL_ERR_ARG
+ * otherwise); x and y may have any alignment (16-byte alignment enables the vectorised paths). */
 int wl_workspace_size(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, size_t* bytes);
 int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,
                const float* bias, float* y, void* workspace, size_t workspace_bytes, void* stream);

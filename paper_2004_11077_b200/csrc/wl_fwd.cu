@@ -114,6 +114,9 @@ int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const
   if (rc) return rc;
   if (workspace_bytes < L.total) return fail(WL_ERR_WORKSPACE, "workspace needs %zu bytes", L.total);
   if (split && saved_bytes < L.saved_total) return fail(WL_ERR_WORKSPACE, "saved buffer needs %zu bytes", L.saved_total);
+  // TMA / bulk copies and 16-byte vector accesses address the workspace blocks at their 256-byte-aligned offsets
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) || (saved && (reinterpret_cast<uintptr_t>(saved) & 255)))
+    return fail(WL_ERR_ARG, "workspace and saved buffers must be 256-byte aligned");
   const Geo& g = L.g;
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);

@@ -587,12 +587,13 @@ __device__ __noinline__ void exact_out_unit_to_y(const HT* __restrict__ h, float
 //     tools/probe_ywrite.cu measures 3.7 TB/s for 8-tile (128-byte) runs and 5.5 TB/s for whole tile rows.
 struct CwShape {
   int R, TPP, CG;  // tiles per item, tiles per pass, channel groups per item; (R / TPP rounded up) * CG = 8 warps
+  int vec4;        // y rows may be stored as float4 (Wo % 4 == 0 and y 16-byte aligned)
 };
 inline CwShape cw_shape(int tw) {
-  if (tw <= 8) return {(8 / tw) * tw, (8 / tw) * tw, 8};
-  if (tw <= 16) return {tw, (tw + 1) / 2, 4};
-  if (tw <= 32) return {tw, (tw + 3) / 4, 2};
-  return {32, 8, 2};
+  if (tw <= 8) return {(8 / tw) * tw, (8 / tw) * tw, 8, 0};
+  if (tw <= 16) return {tw, (tw + 1) / 2, 4, 0};
+  if (tw <= 32) return {tw, (tw + 3) / 4, 2, 0};
+  return {32, 8, 2, 0};
 }
 struct StagedCw {
   static constexpr int THREADS = 256;
@@ -718,7 +719,7 @@ __global__ void __launch_bounds__(StagedCw::THREADS, 4)
     if (!skip) {
       float* row = y + (((size_t)n * g.K + k) * g.Ho + 4 * ty) * g.Wo + 4 * tx;
       const int rows = min(4, g.Ho - 4 * ty);
-      if ((g.Wo & 3) == 0) {
+      if (sh.vec4) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (i < rows)

@@ -137,6 +137,17 @@ def test_ragged_shapes(cin, cout, h, w, pad, mode):
     _compare_with_oracle(x, wt, mode, W.QuantConfig.uniform(8), pad, "batch")
 
 
+@pytest.mark.parametrize("cin,cout,h,w,pad", [(8, 12, 10, 98, 1), (6, 8, 6, 138, 1), (4, 8, 22, 42, 0), (12, 8, 34, 18, 1)])
+def test_wide_images_output_item_shapes(cin, cout, h, w, pad):
+    """Tile rows of 25, 35, 10 and 5 tiles: every branch of the output pass's item shape (tile-row items in 1, 2
+    and 4 passes, 32-tile chunks of rows wider than 32 tiles; csrc/wl_staged.cuh cw_shape), bias included."""
+    rng = np.random.default_rng(cin * 7 + w)
+    x = rng.standard_normal((2, cin, h, w)).astype(np.float32)
+    wt = _kaiming(rng, cout, cin)
+    _compare_with_oracle(x, wt, "legendre", W.QuantConfig.uniform(8), pad, "image")
+    _compare_with_oracle(x, wt, "legendre", W.QuantConfig.uniform(8), pad, "batch")
+
+
 def test_degenerate_inputs_ties_and_equal_maxima():
     rng = np.random.default_rng(5)
     cases = [np.zeros((2, 8, 8, 8)), np.ones((2, 8, 8, 8)), rng.integers(-2, 3, (2, 8, 8, 8)),
