@@ -602,13 +602,60 @@ def run_train(args, rank, world, local_rank):
     e1.record()
     torch.cuda.synchronize()
     _barrier(world)
-    ms = _max_over_ranks(torch, e0.elapsed_time(e1) / args.steps, world, dev)
+    ms_eager = _max_over_ranks(torch, e0.elapsed_time(e1) / args.steps, world, dev)
+    ms, graphed = ms_eager, False
+    if world == 1 and not args.no_graph:
+        # single GPU: the same step as one CUDA graph (the eager step is host-launch-bound at batch 256)
+        step = TR.make_graphed_step(net, opt, x, y, warmup=1)
+        for _ in range(max(args.warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            loss = step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms, graphed = e0.elapsed_time(e1) / args.steps, True
+        TR.invalidate_weight_caches(model)
+    # Phase breakdown on extra steps AFTER the timed region: CUDA events around every Winograd-layer forward
+    # (wl_forward_train) and STE backward (wl_backward); the rest is PyTorch (BN, ReLU, stride-2 / 1x1 convs,
+    # FC, loss, SGD, DDP all-reduce).
+    from paper_2004_11077_b200 import layer as LY
+    marks = []
+
+    def _timed(kind, fn):
+        def wrapper(self, *a, **k):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            out = fn(self, *a, **k)
+            e.record()
+            marks.append((kind, s, e))
+            return out
+        return wrapper
+
+    of, ob = LY.QuantWinogradConv.forward, LY.QuantWinogradConv.backward
+    LY.QuantWinogradConv.forward, LY.QuantWinogradConv.backward = _timed("fwd", of), _timed("bwd", ob)
+    psteps = 3
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for _ in range(psteps):
+        TR.train_step(net, opt, x, y)
+    p1.record()
+    torch.cuda.synchronize()
+    LY.QuantWinogradConv.forward, LY.QuantWinogradConv.backward = of, ob
+    pf = sum(s.elapsed_time(e) for k, s, e in marks if k == "fwd") / psteps
+    pb = sum(s.elapsed_time(e) for k, s, e in marks if k == "bwd") / psteps
+    pt = p0.elapsed_time(p1) / psteps
+    phases = {"winograd_forward_ms": round(pf, 3), "winograd_backward_ms": round(pb, 3),
+              "pytorch_rest_ms": round(pt - pf - pb, 3), "step_ms_with_events": round(pt, 3),
+              "note": "3 extra steps after the timed region, CUDA events around each of the %d Winograd layers" % nwino}
     if rank == 0:
         print(json.dumps({
             "metric": "ResNet-18 (Winograd-aware Legendre 8b) training throughput", "value": world * batch / (ms * 1e-3),
             "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8 fwd / fp32 bwd",
-            "data": "synthetic N(0,1) 3x32x32, uniform labels", "loss": float(loss),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8 fwd (tcgen05 kind::i8) / fp32-accurate split-bf16 bwd (tcgen05 kind::f16)",
+            "data": "synthetic N(0,1) 3x32x32, uniform labels", "loss": float(loss), "phases": phases,
+            "cuda_graph": graphed, "ms_per_step_eager": ms_eager,
             "config": {"workload": "config5: ResNet-18 32x32, %d Winograd layers, batch 256/GPU, SGD m=0.9 lr=0.1"
                        % nwino, "global_batch": world * batch, "parallelism": f"DDP x{world} (NCCL all-reduce)"},
         }), flush=True)
@@ -655,6 +702,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="train workload: time the eager step only")
     ap.add_argument("--scale-groups", default="image", choices=["image", "batch"])
     ap.add_argument("--workload", default="layer", choices=["layer", "train", "bwd", "sweep"],
                     help="layer: config-4 layer throughput (default); train: config-5 ResNet-18 training step; "

@@ -585,6 +585,12 @@ static int direct_impl(const wl_qcfg* q, const wl_shape* s, const T* x, const T*
   return WL_OK;
 }
 
+__global__ void init_weight_header_kernel(WeightHeader* dst, const WeightHeader h) {
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(&h);
+  uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(WeightHeader) / 4); i += blockDim.x) d[i] = src[i];
+}
+
 template <typename XT>
 static int weight_transform_impl(const wl_plan* plan, const wl_qcfg* q, const XT* w, int c_out, int c_in, void* cache,
                                  size_t cache_bytes, void* stream) {
@@ -606,7 +612,9 @@ static int weight_transform_impl(const wl_plan* plan, const wl_qcfg* q, const XT
   hdr.q = *q;
   WeightHeader* dh = reinterpret_cast<WeightHeader*>(cache);
   int8_t* U = reinterpret_cast<int8_t*>(cache) + align256(sizeof(WeightHeader));
-  WL_CUDA(cudaMemcpyAsync(dh, &hdr, sizeof(hdr), cudaMemcpyHostToDevice, st));
+  // the header travels as a kernel argument (copied at launch): a cudaMemcpyAsync from this stack frame
+  // would be recorded by address when the call is captured in a CUDA graph and replayed from dead memory
+  init_weight_header_kernel<<<1, 32, 0, st>>>(dh, hdr);
   WL_CUDA(cudaMemsetAsync(U, 0, (size_t)36 * Kp * Cp, st));
   const Bits b = make_bits(q);
   const long long nw = (long long)c_out * c_in * 9;

@@ -100,6 +100,42 @@ def train_step(model: nn.Module, opt: torch.optim.Optimizer, x: torch.Tensor, y:
     return loss.detach()
 
 
+def invalidate_weight_caches(model: nn.Module) -> None:
+    """Forget every cached weight transform (after graph replays updated the weights without Python seeing it)."""
+    for m in model.modules():
+        if isinstance(m, WinogradAwareConv2d):
+            for r in m._runners.values():
+                r.wcache.key = None
+
+
+def make_graphed_step(model: nn.Module, opt: torch.optim.Optimizer, x: torch.Tensor, y: torch.Tensor,
+                      warmup: int = 3):
+    """The whole training step (forward, STE backward, SGD update) captured once as a CUDA graph: the ~50
+    kernel launches and ctypes calls of each of the 14 Winograd layers are launch-bound at batch 256, and
+    a replay issues them without any host work.  Single-process only (no DDP hooks inside the capture).
+    Returns `step()` -> loss tensor (static: overwritten by every replay).  x and y are the static inputs:
+    copy new batches into them.  Call invalidate_weight_caches(model) before going back to eager calls."""
+    side = torch.cuda.Stream(device=x.device)
+    side.wait_stream(torch.cuda.current_stream(x.device))
+    with torch.cuda.stream(side):  # eager warm-up: allocations, momentum buffers, per-device kernel attributes
+        for _ in range(warmup):
+            train_step(model, opt, x, y)
+    torch.cuda.current_stream(x.device).wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    opt.zero_grad(set_to_none=True)
+    with torch.cuda.graph(graph):
+        loss = F.cross_entropy(model(x), y)
+        loss.backward()
+        opt.step()
+    loss_out = loss.detach()
+
+    def step() -> torch.Tensor:
+        graph.replay()
+        return loss_out
+
+    return step
+
+
 def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous shard [start, stop) of `total` items for `rank` (sizes differ by at most one)."""
     base, extra = divmod(total, world)

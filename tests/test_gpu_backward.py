@@ -72,6 +72,30 @@ def test_module_training_step_runs_and_learns():
     assert all(np.isfinite(losses)) and losses[-1] < losses[0]
 
 
+def test_graphed_training_step_equals_eager_forward_and_updates():
+    """make_graphed_step: the loss of a replay is the eager loss of the same state (the forward is
+    deterministic), and the replay updates the weights."""
+    from paper_2004_11077_b200 import training as TR
+    torch.manual_seed(1)
+    dev = torch.device("cuda")
+    m = TR.ResNet18(TR.winograd_conv_factory("legendre")).to(dev)
+    opt = TR.make_optimizer(m, lr=0.01)
+    x, y = TR.synthetic_batch(32, 0, seed=3, device=dev)
+    step = TR.make_graphed_step(m, opt, x, y, warmup=2)
+    for _ in range(2):
+        ref = TR.ResNet18(TR.winograd_conv_factory("legendre")).to(dev)
+        ref.load_state_dict(m.state_dict())
+        ref.train()
+        with torch.no_grad():
+            l_ref = float(torch.nn.functional.cross_entropy(ref(x), y))
+        w_before = m.stem.weight.detach().clone()
+        l = float(step())
+        torch.cuda.synchronize()
+        assert abs(l - l_ref) <= 1e-6 * max(1.0, abs(l_ref)), (l, l_ref)
+        assert not torch.equal(w_before, m.stem.weight.detach())
+    TR.invalidate_weight_caches(m)
+
+
 def _deq_t(codes, qmax, maxabs, scale):
     """Dequantised value as the reference holds it after fake_quant (quantize.py:120-125)."""
     c = codes.double()
