@@ -887,12 +887,25 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
   const unsigned T = (unsigned)g.T;
   const unsigned long long rows = 36ull * T;
   const unsigned long long nthr = (unsigned long long)gridDim.x * blockDim.x;
+  const bool tmajor = g.TP * g.ipg < 32;
   for (unsigned long long r0 = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; r0 < rows;
        r0 += nthr) {
-    const unsigned long long r = r0 + lane;
-    const bool valid = r < rows;
-    const unsigned xi = valid ? (unsigned)(r / T) : 0u;
-    const unsigned t = valid ? (unsigned)(r - (unsigned long long)xi * T) : 0u;
+    const unsigned long long rr = r0 + lane;
+    const bool valid = rr < rows;
+    // Lane -> table row.  Large groups: consecutive lanes are consecutive tiles of one xi (coalesced table
+    // reads; a warp meets at most two groups).  Groups of fewer than 32 tiles (small images): the argmax of
+    // every group tends to sit at the same xi, so that mapping would hand 32 groups' fp64 replays to one warp
+    // one after the other (measured 0.99 ms on 256 images of 512 x 4 x 4); there lanes run over the 36 xi of
+    // consecutive tiles, i.e. at most two groups per warp again.
+    unsigned xi, t;
+    if (tmajor) {
+      t = valid ? (unsigned)(rr / 36u) : 0u;
+      xi = valid ? (unsigned)(rr - 36ull * t) : 0u;
+    } else {
+      xi = valid ? (unsigned)(rr / T) : 0u;
+      t = valid ? (unsigned)(rr - (unsigned long long)xi * T) : 0u;
+    }
+    const unsigned long long r = (unsigned long long)xi * T + t;  // table row
     const int grp = (int)g.fipg.div(g.fTP.div(t));
     const unsigned long long M = valid ? acc[(size_t)grp * ST_COUNT + ST_HAD].M : 0ull;
     unsigned v[4] = {0u, 0u, 0u, 0u};
