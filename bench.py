@@ -81,12 +81,12 @@ SLOT_KERNELS = {
     "output_max": ("sout_bt2_kernel", "fixup_obct_kernel", "finalize_output_kernel<1, 8", "finalize_output_exec<1, 8"),
     "output_write": ("out_table_kernel", "sout_cw_kernel", "fixup_outt_kernel"),
 }
-NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_cfg4_v2.csv")
+NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_cfg4_v3.csv")
 
 
 def ncu_traffic(slot):
     """DRAM bytes (read + write) per launch of a profile slot from the committed `ncu --set full` capture
-    of one config-4 forward (profiles/r02_ncu_full_cfg4_v2.csv, tools/r02_profile.sh), or None."""
+    of one config-4 forward (profiles/r02_ncu_full_cfg4_v3.csv, tools/r02_profile.sh), or None."""
     try:
         with open(NCU_FULL) as fh:
             rows = list(csv.reader(fh))
@@ -432,17 +432,25 @@ def run_ours(args, rank, world, local_rank):
         roof = {"kernel": dom, "bound": "hbm", "achieved": kb / (dom_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(dom)
-    roof["traffic_source"] = "profiles/r02_ncu_full_cfg4_v2.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
+    roof["traffic_source"] = "profiles/r02_ncu_full_cfg4_v3.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
     roof["algorithmic_bytes_per_launch"] = kb
     roof["ms_per_launch"] = dom_ms
     roof["peak_source"] = peak_kind if roof["bound"] == "hbm" else ("torch._int_mm 8192^3 measured live" if i8_peak else "2x bf16 planning")
-    # every slot against the same two ceilings (the transform passes are FMA-pipe bound: profiles/ ncu rows)
+    # every slot against the same two ceilings; `limiter` is what ncu shows bounds the slot's main kernel
+    # (profiles/r02_ncu_full_cfg4_v3.csv): the five transform passes are CUDA-core FMA/ALU-pipe bound, so their
+    # HBM fraction is low by construction
+    limiter = {"absmax_input": "hbm", "quant_input": "issue + hbm", "input_base_change_max": "fma/alu pipes",
+               "input_transform_max": "fma/alu pipes", "input_transform_codes": "fma/alu pipes",
+               "gemm_hadamard_max": "tmem read (64 B/clk/SM) + hbm", "gemm_hadamard_codes": "epilogue issue + tmem read",
+               "output_base_change_max": "fma/alu pipes", "output_max": "fma/alu pipes",
+               "output_write": "hbm (NCHW write pattern)"}
     slots = {}
     for name, v in per_kernel.items():
         sb, sops = kernel_units(name, n, c, k, hw, pad)
         t_floor = max(sb / (hbm * 1e9), sops / ((i8_peak or 2 * bf16) * 1e12) if sops else 0.0)
         slots[name] = {"ms": round(v, 4), "algorithmic_gb": round(sb / 1e9, 3),
-                       "roof_frac": round(t_floor / (v * 1e-3), 3) if v > 0 else None}
+                       "roof_frac": round(t_floor / (v * 1e-3), 3) if v > 0 else None,
+                       "limiter": limiter.get(name)}
     value = world * n / (ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,

@@ -150,8 +150,10 @@ int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const
   c.fl.count = reinterpret_cast<unsigned*>(ws + L.off_fix);
   c.fl.items = reinterpret_cast<unsigned*>(ws + L.off_fix + 64);
   c.fl.cap = L.fix_cap;
-  c.fix_blocks = 16 * num_sms();  // one wave covers every deferred unit of config-4-sized calls
-  c.fin_blocks = 4 * num_sms();
+  // grid-stride helper kernels: one wave covers every deferred unit / table row of config-4-sized calls;
+  // small calls launch only the blocks their lists and tables can fill (launch-bound shapes)
+  c.fix_blocks = (int)std::min<long long>(16LL * num_sms(), ((long long)L.fix_cap + 127) / 128);
+  c.fin_blocks = (int)std::max<long long>(1, std::min<long long>(4LL * num_sms(), (36LL * g.T + 255) / 256));
   c.pgrid = (L.groups + 127) / 128;
   for (int i = 0; i < ST_COUNT; ++i) c.tabs.t[i] = nullptr;
 
