@@ -148,6 +148,65 @@ def test_wide_images_output_item_shapes(cin, cout, h, w, pad):
     _compare_with_oracle(x, wt, "legendre", W.QuantConfig.uniform(8), pad, "batch")
 
 
+@pytest.mark.parametrize("seed", range(int(os.environ.get("WL_RANDOM_SEEDS", "48"))))
+def test_random_shapes_modes_widths(seed):
+    """Seeded random sweep over shapes, modes, stage widths, padding, scale groups and input statistics
+    (Gaussian, ReLU, heavy-tailed, small-integer inputs full of ties): every draw bit-exact against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    cin, cout = int(rng.choice([1, 3, 7, 16, 31, 40, 64, 96])), int(rng.choice([1, 5, 16, 33, 64, 72, 130]))
+    h, w_ = int(rng.integers(3, 27)), int(rng.integers(3, 27))
+    pad = int(rng.integers(0, 3))
+    if h + 2 * pad < 3 or w_ + 2 * pad < 3:
+        pad = 1
+    n = int(rng.choice([1, 2, 3, 5]))
+    mode = str(rng.choice(["legendre", "canonical"]))
+    kind = seed % 4
+    if kind == 0:
+        x = rng.standard_normal((n, cin, h, w_))
+    elif kind == 1:
+        x = np.maximum(rng.standard_normal((n, cin, h, w_)), 0)
+    elif kind == 2:
+        x = rng.standard_t(2, (n, cin, h, w_))
+    else:
+        x = rng.integers(-3, 4, (n, cin, h, w_)).astype(np.float64)
+    wt = rng.standard_normal((cout, cin, 3, 3)) * (0.3 if kind != 3 else 1.0)
+    if kind == 3:
+        wt = np.rint(wt)
+    bits = dict(input_bits=int(rng.integers(4, 9)), weight_bits=int(rng.integers(4, 9)),
+                weight_transform_bits=int(rng.integers(5, 9)), input_transform_bits=int(rng.integers(5, 9)),
+                hadamard_bits=int(rng.integers(6, 10)), output_transform_bits=int(rng.choice([6, 8, 10, 12, 14, 16])),
+                base_change_bits=int(rng.integers(5, 9)))
+    qc = W.QuantConfig(**bits)
+    groups = "image" if seed % 3 else "batch"
+    _compare_with_oracle(x.astype(np.float32), wt.astype(np.float32), mode, qc, pad, groups)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("WL_RANDOM_SEEDS_WIDE", "12"))))
+def test_random_wide_channels(seed):
+    """Seeded draws with up to 512 channels on tiny images (the LD = 512 kernels, multi-block GEMM tiles, one-tile
+    scale groups), fp32 tensors and the fp64 numpy entry point."""
+    rng = np.random.default_rng(5000 + seed)
+    cin, cout = int(rng.choice([130, 256, 300, 512])), int(rng.choice([65, 200, 257, 512]))
+    h, w_ = int(rng.integers(3, 9)), int(rng.integers(3, 9))
+    pad = int(rng.integers(0, 2))
+    if h + 2 * pad < 3 or w_ + 2 * pad < 3:
+        pad = 1
+    n = int(rng.choice([1, 2, 4]))
+    mode = str(rng.choice(["legendre", "canonical"]))
+    x = rng.standard_normal((n, cin, h, w_)) if seed % 2 else np.rint(2 * rng.standard_normal((n, cin, h, w_)))
+    wt = _kaiming(rng, cout, cin)
+    qc = W.QuantConfig(hadamard_bits=int(rng.choice([8, 9])), output_transform_bits=int(rng.choice([8, 12, 16])))
+    _compare_with_oracle(x.astype(np.float32), wt, mode, qc, pad, "image" if seed % 3 else "batch")
+    if seed % 4 == 0:  # fp64 numpy call on one image: the reference's own signature and dtype
+        xd, wd = x[0].astype(np.float64) * np.pi, wt.astype(np.float64) / 3
+        if pad:
+            xd = np.pad(xd, ((0, 0), (pad, pad), (pad, pad)))
+        y, stats = W.conv2d_winograd_quantized(xd, wd, PLAN, mode, qc)
+        yo, so, _ = O.quant_conv_batch(xd[None], wd, mode, {f: getattr(qc, f) for f in O.BIT_FIELDS}, padding=0)
+        assert np.array_equal(np.asarray(y), yo[0])
+        assert stats_tuples(stats) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[0]]
+
+
 def test_degenerate_inputs_ties_and_equal_maxima():
     rng = np.random.default_rng(5)
     cases = [np.zeros((2, 8, 8, 8)), np.ones((2, 8, 8, 8)), rng.integers(-2, 3, (2, 8, 8, 8)),
