@@ -56,6 +56,31 @@ def test_backward_matches_fp64_closed_form(mode, n, c, k, hw, pad):
         assert rel(db, db_r) <= TOL
 
 
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("WL_RANDOM_SEEDS_BWD", "12"))))
+def test_backward_random_shapes(seed):
+    """Seeded random shapes (ragged, non-square, C / K not multiples of the MMA tiles, padding 0..2, both modes,
+    8b and 8b+9b): dx, dW, db against the fp64 closed form."""
+    rng = np.random.default_rng(7000 + seed)
+    n, c, k = int(rng.choice([1, 2, 5])), int(rng.choice([1, 3, 17, 48, 64, 100])), int(rng.choice([1, 6, 33, 64, 130]))
+    h, w_ = int(rng.integers(3, 21)), int(rng.integers(3, 21))
+    pad = int(rng.integers(0, 3))
+    if h + 2 * pad < 3 or w_ + 2 * pad < 3:
+        pad = 1
+    mode = str(rng.choice(["legendre", "canonical"]))
+    x = rng.standard_normal((n, c, h, w_)).astype(np.float32)
+    w = (rng.standard_normal((k, c, 3, 3)) * np.sqrt(2 / (9 * c))).astype(np.float32)
+    ho, wo = h + 2 * pad - 2, w_ + 2 * pad - 2
+    dy = rng.standard_normal((n, k, ho, wo)).astype(np.float32)
+    qc = W.QuantConfig.from_name("8b+9b" if seed % 2 else "8b")
+    y, dx, dw, db = run(x, w, dy, mode, qc, pad)
+    U, V = BR.quantised_operands(x.astype(np.float64), w.astype(np.float64), mode,
+                                 {f: getattr(qc, f) for f in O.BIT_FIELDS}, pad)
+    dx_r, dw_r, db_r = BR.ste_formula(dy.astype(np.float64), U, V, h, w_, pad)
+    assert rel(dx, dx_r) <= TOL
+    assert rel(dw, dw_r) <= TOL
+    assert rel(db, db_r) <= TOL
+
+
 def test_module_training_step_runs_and_learns():
     torch.manual_seed(0)
     m = W.WinogradAwareConv2d(8, 8, bias=True).cuda()
