@@ -126,6 +126,26 @@ def test_config4_sampled_images():
     _compare_with_oracle(x, w, "legendre", W.QuantConfig.uniform(8), 1, "image", sample=[0, 31, 63])
 
 
+@pytest.mark.parametrize("kind", ["relu", "heavy_tail", "small_integers", "sparse"])
+def test_config4_shape_adverse_statistics(kind):
+    """Config-4 image shape with input statistics that stress the exact paths at scale: ReLU activations,
+    heavy tails (one huge value sets the scale, most codes are tiny), small integers (exact ties in every
+    stage, fix lists far beyond their capacity -> inline fallbacks) and 95 % zeros."""
+    rng = np.random.default_rng(44)
+    n = 6
+    shape = (n, 256, 56, 56)
+    if kind == "relu":
+        x = np.maximum(rng.standard_normal(shape), 0)
+    elif kind == "heavy_tail":
+        x = rng.standard_t(1.5, shape)
+    elif kind == "small_integers":
+        x = rng.integers(-2, 3, shape).astype(np.float64)
+    else:
+        x = rng.standard_normal(shape) * (rng.random(shape) < 0.05)
+    w = _kaiming(rng, 256, 256) if kind != "small_integers" else np.rint(rng.standard_normal((256, 256, 3, 3))).astype(np.float32)
+    _compare_with_oracle(x.astype(np.float32), w, "legendre", W.QuantConfig.uniform(8), 1, "image", sample=[0, n - 1])
+
+
 @pytest.mark.parametrize("cin,cout,h,w,pad", [(3, 64, 32, 32, 1), (5, 10, 13, 14, 0), (33, 70, 9, 7, 1),
                                                (96, 200, 6, 11, 1), (1, 1, 3, 3, 0)])
 @pytest.mark.parametrize("mode", ["legendre", "canonical"])
