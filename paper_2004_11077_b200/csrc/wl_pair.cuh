@@ -163,11 +163,7 @@ struct Staged2 {
 
 // staged_loop with two channels per thread: body(t, c, act0, act1, st, so) with c even; so points
 // at the tile's [36][LD] int8 output block (the body stores 16-bit pairs at so + e * LD + c).
-// kSync = false (passes without a staged output, i.e. the max-only kernels): no CTA barrier at all —
-// every warp waits on the slot's full barrier itself and releases the slot through an empty barrier
-// (count = warps) that only the issuing thread waits on, so warps drift up to one iteration apart
-// (ncu: `barrier` was 1.2 stall cycles per issue in sin_a2 / sout_a2).
-template <int LD, int EB, bool kC0, bool kSync = true, class Body>
+template <int LD, int EB, bool kC0, class Body>
 __device__ __forceinline__ void staged_loop2(const Geo& g, int nch, const void* planes, const CUtensorMap* c0map,
                                              Body&& body, int8_t* out = nullptr) {
   using S = Staged2<LD, EB>;
@@ -176,16 +172,11 @@ __device__ __forceinline__ void staged_loop2(const Geo& g, int nch, const void* 
   const bool kout = out != nullptr;
   uint8_t* osm = sm + 2 * S::STAGE_BYTES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 2 * S::STAGE_BYTES + (kout ? 2 * S::OUT_BYTES : 0));
-  __shared__ uint64_t empty[2];
   const int niter = (g.T + S::TPB - 1) / S::TPB;
   const int tl = threadIdx.x / (LD / 2), c = 2 * (threadIdx.x % (LD / 2));
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
-    if (!kSync) {
-      mbar_init(&empty[0], S::THREADS / 32);
-      mbar_init(&empty[1], S::THREADS / 32);
-    }
     fence_mbar_init();
     if (kC0) tma_prefetch_desc(c0map);
   }
@@ -210,35 +201,26 @@ __device__ __forceinline__ void staged_loop2(const Geo& g, int nch, const void* 
   int k = 0;
   for (int it = blockIdx.x; it < niter; it += gridDim.x, ++k) {
     const int s = k & 1;
-    if (threadIdx.x == 0 && it + (int)gridDim.x < niter) {
-      // slot s ^ 1 was read in iteration k - 1: without the CTA barrier, wait until all warps released it
-      if (!kSync && k >= 1) mbar_wait(&empty[s ^ 1], (uint32_t)(((k - 1) >> 1) & 1));
-      issue(it + gridDim.x, s ^ 1);
-    }
+    if (threadIdx.x == 0 && it + (int)gridDim.x < niter) issue(it + gridDim.x, s ^ 1);
     mbar_wait(&bar[s], (uint32_t)((k >> 1) & 1));
     const int t = it * S::TPB + tl;
     int8_t* so = reinterpret_cast<int8_t*>(osm + s * S::OUT_BYTES + tl * S::OUT_TILE);
     body(t, c, t < g.T && c < nch, t < g.T && c + 1 < nch, sm + s * S::STAGE_BYTES + tl * S::TILE_BYTES, so);
-    if constexpr (!kSync) {
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
-    } else {
-      if (kout) {
-        if (c + 1 >= nch)  // padded channels of the stored block are zero
+    if (kout) {
+      if (c + 1 >= nch)  // padded channels of the stored block are zero
 #pragma unroll
-          for (int e = 0; e < 36; ++e) {
-            if (c >= nch) so[e * LD + c] = 0;
-            so[e * LD + c + 1] = 0;
-          }
-        fence_proxy_async_smem();
-        if (threadIdx.x == 0) bulk_wait_read<0>();  // the store issued last iteration has read buffer s^1
-      }
-      __syncthreads();
-      if (kout && threadIdx.x == 0) {
-        const int t0 = it * S::TPB, nt = min(S::TPB, g.T - t0);
-        bulk_s2g(out + (size_t)t0 * S::OUT_TILE, osm + s * S::OUT_BYTES, (uint32_t)(nt * S::OUT_TILE));
-        bulk_commit();
-      }
+        for (int e = 0; e < 36; ++e) {
+          if (c >= nch) so[e * LD + c] = 0;
+          so[e * LD + c + 1] = 0;
+        }
+      fence_proxy_async_smem();
+      if (threadIdx.x == 0) bulk_wait_read<0>();  // the store issued last iteration has read buffer s^1
+    }
+    __syncthreads();
+    if (kout && threadIdx.x == 0) {
+      const int t0 = it * S::TPB, nt = min(S::TPB, g.T - t0);
+      bulk_s2g(out + (size_t)t0 * S::OUT_TILE, osm + s * S::OUT_BYTES, (uint32_t)(nt * S::OUT_TILE));
+      bulk_commit();
     }
   }
   if (kout && threadIdx.x == 0) bulk_wait_all<0>();
@@ -284,7 +266,7 @@ __device__ __forceinline__ void record_unit2(float m0, float m1, float tm0, floa
 template <int MODE, int LD>
 __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, WL_MINB)
     sin_a2_kernel(const __grid_constant__ CUtensorMap c0map, Geo g, Acc* __restrict__ acc, Tables tabs) {
-  staged_loop2<LD, 1, true, false>(g, g.C, nullptr, &c0map,
+  staged_loop2<LD, 1, true>(g, g.C, nullptr, &c0map,
                             [&](int t, int c, bool a0, bool a1, const uint8_t* st, int8_t*) {
     f2 X[6][6];
     stage_x2<LD, int8_t>(st, c, X);
@@ -304,7 +286,7 @@ __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, WL_MINB)
 template <int MODE, typename HT, int LD>
 __global__ void __launch_bounds__(Staged2<LD, sizeof(HT)>::THREADS, WL_MINB)
     sout_a2_kernel(const HT* __restrict__ h, Geo g, Acc* __restrict__ acc, Tables tabs) {
-  staged_loop2<LD, sizeof(HT), false, false>(g, g.K, h, nullptr,
+  staged_loop2<LD, sizeof(HT), false>(g, g.K, h, nullptr,
                                       [&](int t, int k, bool a0, bool a1, const uint8_t* st, int8_t*) {
     const int tt = (a0 || a1) ? t : 0;
     const int n = (int)g.fTP.div((unsigned)tt), tile = (int)g.fTP.mod((unsigned)tt), grp = (int)g.fipg.div((unsigned)n);
