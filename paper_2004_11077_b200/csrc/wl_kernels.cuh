@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) quant_input_kernel(const XT* __restrict__
   // fast-path error: rc relative 2^-24 on a value <= qmax, plus the fma rounding of the distance
   const float thr = 0.5f - (float)((q.qmax + 1) * 1.25 * 5.9604644775390625e-8);
   const int ld = g.Cp + 16;
-  const bool vec = sizeof(XT) == 4 && (g.W & 3) == 0;
+  const bool vec = sizeof(XT) == 4 && (g.W & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   for (int w0 = 0; w0 < g.W; w0 += kQuantRowW) {
     const int wn = min(kQuantRowW, g.W - w0);
     if (vec) {

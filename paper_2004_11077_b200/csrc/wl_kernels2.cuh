@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(256, WL_MINB) out_c_kernel(const HT* __restric
     load_planes(c4, plane, off, X);
   sandwich_cols<LOT>(X, emit);
   const YT bk = bias ? __ldg(&bias[k]) : (YT)0;
-  const bool vec = sizeof(YT) == 4 && (g.Wo & 3) == 0;
+  const bool vec = sizeof(YT) == 4 && (g.Wo & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int rr = 4 * ty + i;

@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(StagedOut::THREADS, 3)
       if (base < 0 || k0 + kq >= g.K || i >= yrows[tq]) continue;
       const float4 v = *reinterpret_cast<const float4*>(so + kq * S::OK + tq * S::OT + 4 * i);
       float* row = y + base + kq * plane + (long long)i * g.Wo;
-      if ((g.Wo & 3) == 0) {
+      if ((g.Wo & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
         __stcs(reinterpret_cast<float4*>(row), v);
       } else {
         const int cols = g.Wo - (int)((base % g.Wo));

@@ -227,6 +227,27 @@ def test_random_wide_channels(seed):
         assert stats_tuples(stats) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[0]]
 
 
+def test_unaligned_input_and_output_pointers():
+    """x and y at 4-byte (not 16-byte) aligned addresses take the scalar load / store paths and give the same
+    bits as the aligned call."""
+    rng = np.random.default_rng(21)
+    n, c, k, h = 3, 24, 40, 16
+    x = torch.as_tensor(rng.standard_normal((n, c, h, h)).astype(np.float32), device="cuda")
+    w = torch.as_tensor(_kaiming(rng, k, c), device="cuda")
+    for mode in ("legendre", "canonical"):
+        r = W.QuantWinogradConv(PLAN, mode, W.QuantConfig.uniform(8))
+        y0 = r.forward(x, w, padding=1).clone()
+        xb = torch.empty(x.numel() + 1, device="cuda")
+        xu = xb[1:].view_as(x)
+        xu.copy_(x)
+        yb = torch.empty(y0.numel() + 3, device="cuda")
+        yu = yb[3:].view_as(y0)
+        assert xu.data_ptr() % 16 != 0 and yu.data_ptr() % 16 != 0
+        r.forward(xu, w, padding=1, out=yu)
+        torch.cuda.synchronize()
+        assert torch.equal(yu, y0)
+
+
 def test_degenerate_inputs_ties_and_equal_maxima():
     rng = np.random.default_rng(5)
     cases = [np.zeros((2, 8, 8, 8)), np.ones((2, 8, 8, 8)), rng.integers(-2, 3, (2, 8, 8, 8)),
