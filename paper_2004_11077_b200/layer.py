@@ -8,6 +8,7 @@ Drop-in for the reference entry point ``conv2d_winograd_quantized(x, w, plan, mo
 
 * ``x`` [c_in,H,W] (reference shape) or [N,c_in,H,W]; torch CUDA tensor, or a numpy array (copied
   to the current CUDA device; the result is then returned as float64 numpy like the reference).
+* ``scale_groups=k`` (an int dividing N): k consecutive images share one set of stage scales.
 * ``scale_groups="image"``: every image gets its own stage scales, i.e. the batched call equals N
   independent reference calls (bit-exact contract, tests/test_gpu_parity.py).  ``"batch"``: one
   scale per stage over the whole batch (one cast over the [N,...] tensor).
@@ -155,8 +156,10 @@ class QuantWinogradConv:
             ipg = 1
         elif groups == "batch":
             ipg = n
+        elif isinstance(groups, int) and not isinstance(groups, bool) and groups >= 1 and n % groups == 0:
+            ipg = groups  # consecutive images sharing one set of stage scales (the ABI's images_per_group)
         else:
-            raise ValueError(f"scale_groups must be 'image' or 'batch', got {groups!r}")
+            raise ValueError(f"scale_groups must be 'image', 'batch' or a divisor of the batch size, got {groups!r}")
         return _lib.wl_shape(n, cin, int(w.shape[0]), h, wd, int(padding), ipg)
 
     def workspace_bytes(self, shape) -> int:

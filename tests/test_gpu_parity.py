@@ -76,7 +76,7 @@ def _compare_with_oracle(x, w, mode, qc, pad, groups, sample=None):
     r, y = run_gpu(x, w, mode, qc, pad, groups)
     n = x.shape[0]
     idx = np.arange(n) if sample is None else np.asarray(sample)
-    ipg = 1 if groups == "image" else n
+    ipg = 1 if groups == "image" else (n if groups == "batch" else int(groups))
     xs = x[idx] if groups == "image" else x
     yo, so, _ = O.quant_conv_batch(xs.astype(np.float64), w.astype(np.float64), mode,
                                    {f: getattr(qc, f) for f in O.BIT_FIELDS}, padding=pad,
@@ -89,7 +89,8 @@ def _compare_with_oracle(x, w, mode, qc, pad, groups, sample=None):
         for j, i in enumerate(idx):
             assert stats_tuples(st[i]) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[j]]
     else:
-        assert stats_tuples(st[0]) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[0]]
+        for gi in range(n // ipg):
+            assert stats_tuples(st[gi]) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[gi]]
     return r, y
 
 
@@ -178,7 +179,7 @@ def test_random_shapes_modes_widths(seed):
     pad = int(rng.integers(0, 3))
     if h + 2 * pad < 3 or w_ + 2 * pad < 3:
         pad = 1
-    n = int(rng.choice([1, 2, 3, 5]))
+    n = int(rng.choice([1, 2, 3, 5, 6]))
     mode = str(rng.choice(["legendre", "canonical"]))
     kind = seed % 4
     if kind == 0:
@@ -198,6 +199,8 @@ def test_random_shapes_modes_widths(seed):
                 base_change_bits=int(rng.integers(5, 9)))
     qc = W.QuantConfig(**bits)
     groups = "image" if seed % 3 else "batch"
+    if seed % 5 == 0 and n > 1:
+        groups = [d for d in (2, 3, 5) if n % d == 0][0]  # groups of several images
     _compare_with_oracle(x.astype(np.float32), wt.astype(np.float32), mode, qc, pad, groups)
 
 
@@ -225,6 +228,18 @@ def test_random_wide_channels(seed):
         yo, so, _ = O.quant_conv_batch(xd[None], wd, mode, {f: getattr(qc, f) for f in O.BIT_FIELDS}, padding=0)
         assert np.array_equal(np.asarray(y), yo[0])
         assert stats_tuples(stats) == [(s.stage, s.bits, s.max_abs, s.scale) for s in so[0]]
+
+
+@pytest.mark.parametrize("n,ipg,c,k,h,w,pad,mode", [(6, 2, 20, 24, 9, 10, 1, "legendre"), (6, 3, 33, 70, 5, 14, 1, "canonical"),
+                                                    (8, 4, 64, 64, 16, 16, 1, "legendre"), (4, 2, 256, 256, 8, 8, 1, "legendre"),
+                                                    (9, 3, 8, 130, 3, 3, 2, "legendre")])
+def test_groups_of_several_images(n, ipg, c, k, h, w, pad, mode):
+    """Scale groups of 2-4 consecutive images (the ABI's images_per_group): tile rows of one warp / GEMM tile
+    then belong to different groups."""
+    rng = np.random.default_rng(n * 31 + c)
+    x = (rng.standard_normal((n, c, h, w)) * rng.uniform(0.2, 5.0, (n, 1, 1, 1))).astype(np.float32)
+    wt = _kaiming(rng, k, c)
+    _compare_with_oracle(x, wt, mode, W.QuantConfig.from_name("8b+9b"), pad, ipg)
 
 
 def test_unaligned_input_and_output_pointers():
