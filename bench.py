@@ -86,7 +86,7 @@ NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_cfg4_v3.csv")
 
 def ncu_traffic(slot):
     """DRAM bytes (read + write) per launch of a profile slot from the committed `ncu --set full` capture
-    of one config-4 forward (profiles/r02_ncu_full_cfg4_v3.csv, tools/r02_profile.sh), or None."""
+    of one config-4 forward (profiles/r02_ncu_full_cfg4_v3.csv, tools/ncu_full_cfg4.sh), or None."""
     try:
         with open(NCU_FULL) as fh:
             rows = list(csv.reader(fh))

@@ -1,4 +1,4 @@
-"""Run one golden case through the GPU layer (for bisecting with WL_DEBUG_SYNC / WL_NO_* switches)."""
+"""Run one golden case through the GPU layer (for bisecting with WL_DEBUG_SYNC=1)."""
 import sys
 
 import numpy as np
