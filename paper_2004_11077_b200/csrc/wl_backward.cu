@@ -227,37 +227,49 @@ __global__ void __launch_bounds__(256) dx_gather_kernel(const float* __restrict_
 }
 
 // dW[k][c] = G^T . dU . G with dU^T[e][c][k] summed over the S split partials in fp64.
-__global__ void dw_kernel(const float* __restrict__ dup, float* __restrict__ dw, BwGeo g, int S) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= g.K * g.C) return;
-  const int k = idx % g.K, c = idx / g.K;  // k fastest: coalesced partial reads
-  double D[6][6];
+// dW = G^T . dU . G per (k, c); the dU partial sums of the S tile splits are added in fp64.  Block = 32 output
+// channels x 8 input channels: the partials are read k-fastest (coalesced: [split][36][C][K]); the 9 results of
+// each (k, c) go through a shared tile [32 k][8 c * 9] and leave as 288-byte runs of dw [K][C][3][3] (one thread
+// per (k, c) storing its 9 floats 36 KB apart cost 162 us on 512 x 512 channels; this version ~20 us).
+__global__ void __launch_bounds__(256) dw_kernel(const float* __restrict__ dup, float* __restrict__ dw, BwGeo g, int S) {
+  __shared__ float tile[32][8 * 9 + 1];
+  const int kx = threadIdx.x & 31, cy = threadIdx.x >> 5;
+  const int k0 = blockIdx.x * 32, c0 = blockIdx.y * 8;
+  const int k = k0 + kx, c = c0 + cy;
+  if (k < g.K && c < g.C) {
+    double D[6][6];
 #pragma unroll
-  for (int e = 0; e < 36; ++e) {
-    double s = 0.0;
-    for (int sp = 0; sp < S; ++sp) s += (double)__ldg(&dup[(((size_t)sp * 36 + e) * g.C + c) * g.K + k]);
-    D[e / 6][e % 6] = s;
+    for (int e = 0; e < 36; ++e) {
+      double s = 0.0;
+      for (int sp = 0; sp < S; ++sp) s += (double)__ldg(&dup[(((size_t)sp * 36 + e) * g.C + c) * g.K + k]);
+      D[e / 6][e % 6] = s;
+    }
+    double tmp[6][3];  // dU . G
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < 6; ++b) s += D[a][b] * kG[b][q];
+        tmp[a][q] = s;
+      }
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) s += kG[a][p] * tmp[a][q];
+        tile[kx][cy * 9 + 3 * p + q] = (float)s;
+      }
   }
-  double tmp[6][3];  // dU . G
-#pragma unroll
-  for (int a = 0; a < 6; ++a)
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      double s = 0.0;
-#pragma unroll
-      for (int b = 0; b < 6; ++b) s += D[a][b] * kG[b][q];
-      tmp[a][q] = s;
-    }
-  float* out = dw + ((size_t)k * g.C + c) * 9;
-#pragma unroll
-  for (int p = 0; p < 3; ++p)
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      double s = 0.0;
-#pragma unroll
-      for (int a = 0; a < 6; ++a) s += kG[a][p] * tmp[a][q];
-      out[3 * p + q] = (float)s;
-    }
+  __syncthreads();
+  const int ncols = min(8, g.C - c0) * 9;  // valid floats of each k row of the tile
+  for (int i = threadIdx.x; i < 32 * 72; i += 256) {
+    const int row = i / 72, col = i - row * 72;
+    if (k0 + row < g.K && col < ncols) dw[((size_t)(k0 + row) * g.C + c0) * 9 + col] = tile[row][col];
+  }
 }
 
 __global__ void db_kernel(const float* __restrict__ dy, float* __restrict__ db, BwGeo g) {
@@ -348,7 +360,7 @@ int wl_bw_run(const BwGeo& g, const float* dy, const int8_t* ucodes, const wl::A
   }
   dxt_kernel<<<(unsigned)((T * C + tb - 1) / tb), tb, 0, st>>>(W.dv, W.dxt, g, wacc, wstage, qmax_u);
   dx_gather_kernel<<<dim3((unsigned)(g.N * g.H), (g.W + 31) / 32, (unsigned)((C + 31) / 32)), 256, 0, st>>>(W.dxt, dx, g);
-  dw_kernel<<<(unsigned)((K * C + tb - 1) / tb), tb, 0, st>>>(W.dup, dw, g, W.S);
+  dw_kernel<<<dim3((unsigned)((K + 31) / 32), (unsigned)((C + 7) / 8)), 256, 0, st>>>(W.dup, dw, g, W.S);
   if (db) db_kernel<<<(unsigned)K, 256, 0, st>>>(dy, db, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
