@@ -138,7 +138,6 @@ struct EpiHadRq {
   StageF s;
   float r_lo, r_hi;
   int grp;
-  bool small;  // |I| < 2^22: int -> float by the magic-number add instead of I2F
   int pgrp;             // prefetched (next tile) group and its stage parameters
   float pr, pthr;
   static constexpr bool kPrefetch = true;
@@ -159,7 +158,6 @@ struct EpiHadRq {
     // splits the bracket since I != 0 then).
     r_lo = __fmul_rd(a.r, 1.f - 2.384185791015625e-7f);
     r_hi = __fmul_ru(a.r, 1.f + 2.384185791015625e-7f);
-    small = (long long)g.C * qmax_u * qmax_v < (1LL << 22);
   }
   // Fast path of 16 consecutive columns starting at local column lc of this warp's slice: codes from the
   // r_lo evaluation are staged unconditionally; returns true if some element's [r_lo, r_hi] bracket
@@ -168,26 +166,16 @@ struct EpiHadRq {
     // y[j] = 0x4B400000 + code: its low byte / half-word is the two's-complement code
     uint32_t y[16];
     uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;  // independent chains (ILP)
-    if (small) {
-      // column pairs on packed f32x2 (FADD2 / FFMA2: lane-wise identical to the scalar ops)
+    // column pairs on packed f32x2 (FFMA2: lane-wise identical to the scalar ops); the accumulators are
+    // converted with I2FP (exact: |I| < 2^24) — measured faster than the magic-number add + FADD2 (1.07 -> 1.02 ms)
 #pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        const f2 fi = sub2(mk2(__int_as_float((int)v[j] + 0x4B400000), __int_as_float((int)v[j + 1] + 0x4B400000)),
-                           bc2(kMagic));
-        const f2 ya = fma2(fi, bc2(r_lo), bc2(kMagic)), yb = fma2(fi, bc2(r_hi), bc2(kMagic));
-        y[j] = __float_as_uint(lo2(ya));
-        y[j + 1] = __float_as_uint(hi2(ya));
-        const uint32_t da = y[j] ^ __float_as_uint(lo2(yb)), db = y[j + 1] ^ __float_as_uint(hi2(yb));
-        if ((j & 2) == 0) d0 |= da, d1 |= db; else d2 |= da, d3 |= db;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float fi = (float)(int)v[j];
-        y[j] = __float_as_uint(fmaf(fi, r_lo, kMagic));
-        const uint32_t d = y[j] ^ __float_as_uint(fmaf(fi, r_hi, kMagic));
-        if ((j & 3) == 0) d0 |= d; else if ((j & 3) == 1) d1 |= d; else if ((j & 3) == 2) d2 |= d; else d3 |= d;
-      }
+    for (int j = 0; j < 16; j += 2) {
+      const f2 fi = mk2((float)(int)v[j], (float)(int)v[j + 1]);
+      const f2 ya = fma2(fi, bc2(r_lo), bc2(kMagic)), yb = fma2(fi, bc2(r_hi), bc2(kMagic));
+      y[j] = __float_as_uint(lo2(ya));
+      y[j + 1] = __float_as_uint(hi2(ya));
+      const uint32_t da = y[j] ^ __float_as_uint(lo2(yb)), db = y[j + 1] ^ __float_as_uint(hi2(yb));
+      if ((j & 2) == 0) d0 |= da, d1 |= db; else d2 |= da, d3 |= db;
     }
     const int lane = threadIdx.x & 31;
     const int slot0 = (lc * (int)sizeof(HT)) >> 4;
