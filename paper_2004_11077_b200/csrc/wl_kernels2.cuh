@@ -30,10 +30,22 @@ struct StageE {  // max row abs-sum of each stage's integer matrix (error-bound 
   float e[ST_COUNT];
 };
 
-// Certified bound on |T_f - T| for a group: every fma partial sum of the second half is bounded by
-// rowsum(L) * max|tmp| and rounds by at most 2^-24 of itself; <= 6 roundings (+ margin).
-__device__ __forceinline__ float stage_error(const Acc& a, float rowsum) {
-  return 6.5f * 5.9604645e-8f * rowsum * __uint_as_float(a.TM);
+// Certified bound on |T_f - T|: every fma partial sum of the second half is bounded by
+// rowsum(L) * max|tmp| and rounds by at most 2^-24 of itself; <= 6 roundings (+ margin).  max|tmp| is
+// taken at its static bound qmax_in * rowsum(L) (the first half of the sandwich of codes |c| <= qmax_in):
+// the finalize scans use it only to pick the table entries within 2E of the group's fp32 maximum, and a
+// looser E just adds a few candidates — measuring max|tmp| per unit cost 36 FMNMX3 per thread in every max
+// pass (7 % of the ALU-bound max-only passes).
+__device__ __forceinline__ float stage_error(float rowsum, int qmax_in) {
+  return 6.5f * 5.9604645e-8f * rowsum * (rowsum * (float)qmax_in);
+}
+// qmax of the codes a stage transforms
+template <int MODE, int STAGE>
+__device__ __forceinline__ int stage_in_qmax(const Bits& b) {
+  if (STAGE == ST_IBC) return b.q[ST_INPUT];
+  if (STAGE == ST_IT) return MODE == 0 ? b.q[ST_INPUT] : b.q[ST_IBC];
+  if (STAGE == ST_OBC) return b.q[ST_HAD];
+  return MODE == 0 ? b.q[ST_HAD] : b.q[ST_OBC];  // ST_OUT
 }
 
 // Small integer -> float without the (slow) I2F pipe: |v| < 2^22 placed in the mantissa of 1.5*2^23.
@@ -324,11 +336,9 @@ __global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage
   const int gi = blockIdx.x * blockDim.x + threadIdx.x;
   if (gi >= groups) return;
   Acc& a = acc[(size_t)gi * ST_COUNT + stage];
-  const float E = stage_error(a, rowsum);
   const long long M = (long long)a.M;
   const double maxabs = __longlong_as_double((long long)a.F);
   a.r = M ? (float)((double)qmax / (double)M) : 0.f;
-  (void)E;
   // per-element band = ef * rowsum_i * max|tmp col j| (the element's fp32 error E_ij times qmax/M);
   // slack for r = fl(qmax/M) (relative 2^-24 on a value <= qmax) and the fma rounding of d
   a.ef = M ? (float)((double)qmax * ((double)depth + 0.5) * 5.9604644775390625e-8 / (double)M) : 0.f;
@@ -554,7 +564,7 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
     if (valid) {
       const int grp = (int)g.fipg.div(g.fTP.div(t));
       const Acc& a = acc[(size_t)grp * ST_COUNT + STAGE];
-      lim = __uint_as_float(a.MF) - 2.f * stage_error(a, rowsum);
+      lim = __uint_as_float(a.MF) - 2.f * stage_error(rowsum, stage_in_qmax<MODE, STAGE>(b));
     }
     for (int cb = 0; cb < NB; ++cb) {
       const float v = valid ? __uint_as_float(table[(size_t)t * NB + cb]) : 0.f;
@@ -838,7 +848,7 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
     if (valid) {
       const int grp = (int)g.fipg.div(g.fTP.div(t));
       const Acc& a = acc[(size_t)grp * ST_COUNT + STAGE];
-      lim = __uint_as_float(a.MF) - 2.f * stage_error(a, rowsum);
+      lim = __uint_as_float(a.MF) - 2.f * stage_error(rowsum, stage_in_qmax<MODE, STAGE>(b));
     }
     for (int cb = 0; cb < NB; ++cb) {
       const float v = valid ? __uint_as_float(table[(size_t)t * NB + cb]) : 0.f;

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, WL_MINB)
     sandwich_cols2<LT>(X, [&](int, const f2 (&col)[6]) {
 #pragma unroll
       for (int i = 0; i < 6; ++i) amax2(m0, m1, col[i]);
-    }, &tm0, &tm1);
+    });
     record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, stg, tabs.t[stg], tt, c, g.C, g.lazy);
   });
 }
@@ -314,12 +314,12 @@ __global__ void __launch_bounds__(Staged2<LD, sizeof(HT)>::THREADS, WL_MINB)
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) amax2(m0, m1, col[i]);
-      }, &tm0, &tm1);
+      });
     } else {
       sandwich_cols2<tab::Leg_OBC>(X, [&](int, const f2 (&col)[6]) {
 #pragma unroll
         for (int i = 0; i < 6; ++i) amax2(m0, m1, col[i]);
-      }, &tm0, &tm1);
+      });
     }
     record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, stg, tabs.t[stg], tt, k, g.K, g.lazy);
   });
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, 2)
     sandwich_cols2<tab::Leg_IT>(K1, [&](int, const f2 (&col)[6]) {
 #pragma unroll
       for (int i = 0; i < 6; ++i) amax2(m0, m1, col[i]);
-    }, &tm0, &tm1);
+    });
     if (def0) m0 = tm0 = 0.f;  // recorded by fixup_ibc_kernel from the exact codes
     if (def1) m1 = tm1 = 0.f;
     record_unit2(m0, m1, tm0, tm1, grp, a0, a1, acc, ST_IT, tabs.t[ST_IT], tt, c, g.C, g.lazy);
@@ -434,7 +434,7 @@ __device__ __forceinline__ void t4_of_unit2(const f2 (&K4)[6][6], int ty, int tx
       *reinterpret_cast<unsigned long long*>(ot + (4 * i + j) * ostride) = col[i].u;
       if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo) amax2(m0, m1, col[i]);
     }
-  }, &tm0, &tm1);
+  });
   ef0 = cx0;  // max |first-half value| of the unit: sout_cw forms the per-row band rowsum_i * ef
   ef1 = cx1;
 }
