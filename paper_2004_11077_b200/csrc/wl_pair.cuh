@@ -119,13 +119,12 @@ __device__ __forceinline__ unsigned rq_col2(f2 T, f2 r, f2& k, float& d0, float&
 
 // Code pair -> packed floats: bias both codes to unsigned (xor of the sign bits), splice each into
 // the mantissa of 1.5*2^23 with one PRMT, subtract (1.5*2^23 + bias) with one FADD2 (exact).
-// kI2FP: sign-extending PRMT (selector msb = replicate the byte's sign) + I2FP instead of the mantissa
-// splice + FADD2 — no FMA-pipe instruction.  Measured per kernel: faster in the three code passes (sin_b2
-// 1.510 -> 1.479, sin_c2 1.097 -> 1.075, sout_bt2 1.385 -> 1.374 ms: FMA-pipe bound), slower in the two
-// max-only passes (sin_a2 0.588 -> 0.600, sout_a2 0.533 -> 0.553 ms: ALU-pipe bound), so each picks its own.
-template <typename HT, bool kI2FP = false>
+// Code pair -> packed floats: sign-extending PRMT (selector msb = replicate the byte's sign) + I2FP, no
+// FMA-pipe instruction.  (The earlier mantissa splice + FADD2 cost one FMA-pipe op per pair: the transform
+// passes are FMA-pipe bound; measured sin_b2 1.51 -> 1.48, sin_c2 1.10 -> 1.08, sout_bt2 1.385 -> 1.374 ms and,
+// once their max|tmp| tracking was gone, the max-only passes 0.530 -> 0.524 / 0.475 -> 0.468 ms.)
+template <typename HT>
 __device__ __forceinline__ f2 codes2f2(unsigned v) {
-  if constexpr (kI2FP) {
   unsigned lo, hi;
   if constexpr (sizeof(HT) == 1) {
     asm("prmt.b32 %0, %1, 0, 0x8880;" : "=r"(lo) : "r"(v));
@@ -135,30 +134,19 @@ __device__ __forceinline__ f2 codes2f2(unsigned v) {
     asm("prmt.b32 %0, %1, 0, 0xbb32;" : "=r"(hi) : "r"(v));
   }
   return mk2((float)(int)lo, (float)(int)hi);
-  } else if constexpr (sizeof(HT) == 1) {
-    const unsigned u = v ^ 0x8080u;
-    return sub2(mk2(__uint_as_float(__byte_perm(u, 0x4B400000u, 0x7650)),
-                    __uint_as_float(__byte_perm(u, 0x4B400000u, 0x7651))),
-                bc2(kMagic + 128.f));
-  } else {
-    const unsigned u = v ^ 0x80008000u;
-    return sub2(mk2(__uint_as_float(__byte_perm(u, 0x4B400000u, 0x7610)),
-                    __uint_as_float(__byte_perm(u, 0x4B400000u, 0x7632))),
-                bc2(kMagic + 32768.f));
-  }
 }
 
 // X pair of channels (c, c+1) from a staged [36][LD] block of HT codes.
-template <int LD, typename HT, bool kI2FP = false>
+template <int LD, typename HT>
 __device__ __forceinline__ void stage_x2(const uint8_t* st, int c, f2 (&X)[6][6]) {
   if constexpr (sizeof(HT) == 1) {
     const uint16_t* p = reinterpret_cast<const uint16_t*>(st + c);
 #pragma unroll
-    for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = codes2f2<HT, kI2FP>(p[e * LD / 2]);
+    for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = codes2f2<HT>(p[e * LD / 2]);
   } else {
     const unsigned* p = reinterpret_cast<const unsigned*>(reinterpret_cast<const int16_t*>(st) + c);
 #pragma unroll
-    for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = codes2f2<HT, kI2FP>(p[e * LD / 2]);
+    for (int e = 0; e < 36; ++e) X[e / 6][e % 6] = codes2f2<HT>(p[e * LD / 2]);
   }
 }
 
@@ -353,7 +341,7 @@ __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, 2)
     bool def0 = false, def1 = false;
     {
       f2 X[6][6];
-      stage_x2<LD, int8_t, true>(st, c, X);
+      stage_x2<LD, int8_t>(st, c, X);
       float dm0 = 0.f, dm1 = 0.f;
       sandwich_cols2<tab::Leg_IBC>(X, [&](int j, const f2 (&col)[6], float cm0, float cm1) {
         float d0 = 0.f, d1 = 0.f;
@@ -402,7 +390,7 @@ __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, 2)
     const float r = ga[ST_IT].r, thr = ga[ST_IT].thr, ef = ga[ST_IT].ef;
     const f2 r2 = bc2(r);
     f2 X[6][6];
-    stage_x2<LD, int8_t, true>(st, c, X);
+    stage_x2<LD, int8_t>(st, c, X);
     float dm0 = 0.f, dm1 = 0.f;
     f2 kd;
     sandwich_cols2<tab::Leg_IT>(X, [&](int j, const f2 (&col)[6], float cm0, float cm1) {
@@ -500,7 +488,7 @@ __global__ void __launch_bounds__(StagedT42<LD, sizeof(HT)>::THREADS, 2)
     bool def0, def1, f0, f1;
     {
       f2 X[6][6];
-      stage_x2<LD, HT, true>(st, k, X);
+      stage_x2<LD, HT>(st, k, X);
       float dm0 = 0.f, dm1 = 0.f;
       sandwich_cols2<tab::Leg_OBC>(X, [&](int j, const f2 (&col)[6], float cm0, float cm1) {
         float d0 = 0.f, d1 = 0.f;
