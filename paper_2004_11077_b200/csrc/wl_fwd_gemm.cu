@@ -166,6 +166,7 @@ struct EpiHadRq {
     // y[j] = 0x4B400000 + code: its low byte / half-word is the two's-complement code
     uint32_t y[16];
     uint32_t d0 = 0, d1 = 0, d2 = 0, d3 = 0;  // independent chains (ILP)
+    f2 sq0 = bc2(0.f), sq1 = bc2(0.f);
     // column pairs on packed f32x2 (FFMA2: lane-wise identical to the scalar ops); the accumulators are
     // converted with I2FP (exact: |I| < 2^24) — measured faster than the magic-number add + FADD2 (1.07 -> 1.02 ms)
 #pragma unroll
@@ -174,9 +175,22 @@ struct EpiHadRq {
       const f2 ya = fma2(fi, bc2(r_lo), bc2(kMagic)), yb = fma2(fi, bc2(r_hi), bc2(kMagic));
       y[j] = __float_as_uint(lo2(ya));
       y[j + 1] = __float_as_uint(hi2(ya));
+#ifdef WL_RQ_XOR
       const uint32_t da = y[j] ^ __float_as_uint(lo2(yb)), db = y[j + 1] ^ __float_as_uint(hi2(yb));
       if ((j & 2) == 0) d0 |= da, d1 |= db; else d2 |= da, d3 |= db;
+#else
+      // bracket test on the FMA pipe (the epilogue is ALU-pipe bound): ya - yb is the exact code difference,
+      // its squares accumulate to zero iff every code of the chunk agrees (two chains for ILP)
+      const f2 df = sub2(ya, yb);
+      if ((j & 2) == 0) sq0 = fma2(df, df, sq0); else sq1 = fma2(df, df, sq1);
+#endif
     }
+#ifndef WL_RQ_XOR
+    {
+      const f2 sq = add2(sq0, sq1);
+      d0 = __float_as_uint(lo2(sq)) | __float_as_uint(hi2(sq));  // non-negative sums: bits zero iff value zero
+    }
+#endif
     const int lane = threadIdx.x & 31;
     const int slot0 = (lc * (int)sizeof(HT)) >> 4;
     const uint32_t rbase = smem_u32(stage) + lane * kRowBytes;
