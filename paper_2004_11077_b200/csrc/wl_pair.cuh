@@ -117,8 +117,6 @@ __device__ __forceinline__ unsigned rq_col2(f2 T, f2 r, f2& k, float& d0, float&
   return __byte_perm(__float_as_uint(lo2(y)), __float_as_uint(hi2(y)), 0x0040);
 }
 
-// Code pair -> packed floats: bias both codes to unsigned (xor of the sign bits), splice each into
-// the mantissa of 1.5*2^23 with one PRMT, subtract (1.5*2^23 + bias) with one FADD2 (exact).
 // Code pair -> packed floats: sign-extending PRMT (selector msb = replicate the byte's sign) + I2FP, no
 // FMA-pipe instruction.  (The earlier mantissa splice + FADD2 cost one FMA-pipe op per pair: the transform
 // passes are FMA-pipe bound; measured sin_b2 1.51 -> 1.48, sin_c2 1.10 -> 1.08, sout_bt2 1.385 -> 1.374 ms and,
