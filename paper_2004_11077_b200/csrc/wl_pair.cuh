@@ -148,10 +148,20 @@ __device__ __forceinline__ void stage_x2(const uint8_t* st, int c, f2 (&X)[6][6]
   }
 }
 
-template <int LD, int EB>
+// W = padded channels staged per block iteration (threads = W / 2).  Measured on config 4: the c0-fed
+// IBC max pass and the V code pass run 2-5 % faster as 128-thread blocks (W = 256, twice the resident
+// blocks), the other pair kernels are 1-3 % faster as 256-thread blocks.
+#ifndef WL_W_SINA
+#define WL_W_SINA 256
+#endif
+#ifndef WL_W_SINC
+#define WL_W_SINC 256
+#endif
+
+template <int LD, int EB, int W = 512>
 struct Staged2 {
   static_assert(LD <= 256, "staged path handles up to 256 padded channels");
-  static constexpr int TPB = 512 / LD;  // tiles per iteration (two channels per thread)
+  static constexpr int TPB = (W / LD) > 0 ? W / LD : 1;  // tiles per iteration (two channels per thread)
   static constexpr int THREADS = TPB * LD / 2;
   static constexpr int TILE_BYTES = 36 * LD * EB;
   static constexpr int STAGE_BYTES = TPB * TILE_BYTES;
@@ -163,10 +173,10 @@ struct Staged2 {
 
 // staged_loop with two channels per thread: body(t, c, act0, act1, st, so) with c even; so points
 // at the tile's [36][LD] int8 output block (the body stores 16-bit pairs at so + e * LD + c).
-template <int LD, int EB, bool kC0, class Body>
+template <int LD, int EB, bool kC0, int W = 512, class Body>
 __device__ __forceinline__ void staged_loop2(const Geo& g, int nch, const void* planes, const CUtensorMap* c0map,
                                              Body&& body, int8_t* out = nullptr) {
-  using S = Staged2<LD, EB>;
+  using S = Staged2<LD, EB, W>;
   extern __shared__ __align__(128) uint8_t wl_stage_smem[];
   uint8_t* sm = wl_stage_smem;
   const bool kout = out != nullptr;
@@ -264,9 +274,9 @@ __device__ __forceinline__ void record_unit2(float m0, float m1, float tm0, floa
 // ---------------------------------------------------------------------------------- max passes
 
 template <int MODE, int LD>
-__global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, WL_MINB)
+__global__ void __launch_bounds__(Staged2<LD, 1, WL_W_SINA>::THREADS, WL_MINB * 512 / WL_W_SINA)
     sin_a2_kernel(const __grid_constant__ CUtensorMap c0map, Geo g, Acc* __restrict__ acc, Tables tabs) {
-  staged_loop2<LD, 1, true>(g, g.C, nullptr, &c0map,
+  staged_loop2<LD, 1, true, WL_W_SINA>(g, g.C, nullptr, &c0map,
                             [&](int t, int c, bool a0, bool a1, const uint8_t* st, int8_t*) {
     f2 X[6][6];
     stage_x2<LD, int8_t>(st, c, X);
@@ -377,11 +387,12 @@ __global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, 2)
 
 // Legendre V codes from staged c1 (B_P^T), two channels per thread.
 template <int LD>
-__global__ void __launch_bounds__(Staged2<LD, 1>::THREADS, 2)
+__global__ void __launch_bounds__(Staged2<LD, 1, WL_W_SINC>::THREADS, 2 * 512 / WL_W_SINC)
     sin_c2_kernel(const __grid_constant__ CUtensorMap c0map, const int8_t* __restrict__ c0,
                   const int8_t* __restrict__ c1, int8_t* __restrict__ V, const __grid_constant__ Geo g,
                   const __grid_constant__ Bits b, Acc* __restrict__ acc, const PlanF64* __restrict__ pf, FixList fl) {
-  staged_loop2<LD, 1, false>(g, g.C, c1, &c0map, [&](int t, int c, bool a0, bool a1, const uint8_t* st, int8_t* so) {
+  staged_loop2<LD, 1, false, WL_W_SINC>(g, g.C, c1, &c0map,
+                                        [&](int t, int c, bool a0, bool a1, const uint8_t* st, int8_t* so) {
     if (!a0 && !a1) return;
     const int n = (int)g.fTP.div((unsigned)t), grp = (int)g.fipg.div((unsigned)n);
     const Acc* ga = acc + (size_t)grp * ST_COUNT;
