@@ -292,10 +292,12 @@ int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L, bool split) {
                             "independent)");
   L->groups = g.N / g.ipg;
   L->hbytes = q->hadamard_bits > 8 ? 2 : 1;
-  // saved block: [acc][V]
+  // saved block: [acc][cast tickets][V]
   size_t o = 0;
   L->off_acc = o;
   o = align256(o + sizeof(Acc) * ST_COUNT * L->groups);
+  L->off_sync = o;  // fused input cast: block ticket + one arrival counter per group
+  o = align256(o + sizeof(unsigned) * ((size_t)L->groups + 1));
   L->off_v = o;
   o = align256(o + (size_t)36 * g.T * g.Cp);
   L->saved_total = o;

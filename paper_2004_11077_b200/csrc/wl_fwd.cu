@@ -71,20 +71,37 @@ template <typename XT>
 static int input_cast(FwdCtx& c, const XT* x) {
   const Geo& g = c.g;
   const long long per_image = (long long)g.C * g.H * g.W;
-  const int bx = (int)std::min<long long>((per_image / 4 + 255) / 256, 64);
-  absmax_input_kernel<XT><<<dim3(std::max(bx, 1), g.N), 256, 0, c.st>>>(x, per_image, g.ipg, c.acc);
-  prof_mark("absmax_input", c.st);
   const bool w64 = sizeof(XT) == 4 && (g.W & 3) == 0 && g.W <= 64 && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  if (w64) {
 #ifndef WL_QI_RH
 #define WL_QI_RH 2
 #endif
-    // band of rh rows per block: per channel one contiguous rh * W float run (at most 256 float4 slots and
-    // ~60 KB of staging per block)
-    int rh = WL_QI_RH;
-    while (rh > 1 && (rh * g.W * (g.Cp + 4) > 60 * 1024 || rh * g.W / 4 > 256)) rh >>= 1;
-    rh = std::min(rh, g.H);
-    const int smem = rh * g.W * (g.Cp + 4);
+#ifndef WL_CAST_LAG
+#define WL_CAST_LAG 1  // images between a band's max pass and its quantisation (>= images per group)
+#endif
+#ifndef WL_CAST_L2_BYTES
+#define WL_CAST_L2_BYTES (48ll << 20)  // x bytes read between the two reads of a band that L2 is trusted to keep
+#endif
+  // band of rh rows per block: per channel one contiguous rh * W float run (at most 256 float4 slots and
+  // ~60 KB of staging per block)
+  int rh = WL_QI_RH;
+  while (rh > 1 && (rh * g.W * (g.Cp + 4) > 60 * 1024 || rh * g.W / 4 > 256)) rh >>= 1;
+  rh = std::min(rh, g.H);
+  const int smem = rh * g.W * (g.Cp + 4);
+  const int nb = (g.H + rh - 1) / rh;
+  if (w64 && (long long)g.ipg * per_image * 4 <= WL_CAST_L2_BYTES) {
+    // one launch, x read from HBM once (the second read of a band hits L2)
+    const int lag = (int)std::min<long long>(std::max(g.ipg, WL_CAST_LAG),
+                                             std::max<long long>(g.ipg, WL_CAST_L2_BYTES / (per_image * 4)));
+    WL_CUDA(ensure_smem_attr(reinterpret_cast<const void*>(cast_input_w64_kernel<0>), smem));
+    cast_input_w64_kernel<<<(unsigned)nb * (unsigned)(g.N + lag), 256, smem, c.st>>>(
+        reinterpret_cast<const float*>(x), c.c0, g, c.b, c.acc, rh, lag, c.sync);
+    prof_mark("cast_input", c.st);
+    return WL_OK;
+  }
+  const int bx = (int)std::min<long long>((per_image / 4 + 255) / 256, 64);
+  absmax_input_kernel<XT><<<dim3(std::max(bx, 1), g.N), 256, 0, c.st>>>(x, per_image, g.ipg, c.acc);
+  prof_mark("absmax_input", c.st);
+  if (w64) {
     WL_CUDA(ensure_smem_attr(reinterpret_cast<const void*>(quant_input_w64_kernel<0>), smem));
     quant_input_w64_kernel<<<dim3((g.H + rh - 1) / rh, g.N), 256, smem, c.st>>>(reinterpret_cast<const float*>(x),
                                                                               c.c0, g, c.b, c.acc, rh);
@@ -132,6 +149,7 @@ int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const
   c.mode = plan->mode;
   c.leg = plan->mode == WL_LEGENDRE;
   c.acc = reinterpret_cast<Acc*>(sv + L.off_acc);
+  c.sync = reinterpret_cast<unsigned*>(sv + L.off_sync);
   c.V = reinterpret_cast<int8_t*>(sv + L.off_v);
   c.c0 = reinterpret_cast<int8_t*>(ws + L.off_c0);
   c.c1 = reinterpret_cast<int8_t*>(ws + L.off_c1);
@@ -158,7 +176,7 @@ int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const
   for (int i = 0; i < ST_COUNT; ++i) c.tabs.t[i] = nullptr;
 
   prof_begin();
-  WL_CUDA(cudaMemsetAsync(c.acc, 0, sizeof(Acc) * ST_COUNT * L.groups, st));
+  WL_CUDA(cudaMemsetAsync(c.acc, 0, L.off_v - L.off_acc, st));  // group accumulators + cast tickets
   prof_mark("begin", st);
   if ((rc = input_cast<XT>(c, x))) return rc;
 

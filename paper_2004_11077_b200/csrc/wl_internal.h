@@ -43,7 +43,7 @@ extern const int kTableStage[kNumTables];
 // stage slots and the V codes, can keep that prefix alone (wl_forward_train puts it in its own buffer).
 struct Layout {
   Geo g;
-  size_t off_acc, off_v, saved_total;  // offsets inside the saved block
+  size_t off_acc, off_sync, off_v, saved_total;  // offsets inside the saved block
   size_t off_c0, off_h, off_c1, off_c4, off_t4, off_e4, off_tab[kNumTables], tab_bytes[kNumTables], off_otab, off_odq, off_fix,
       total;  // offsets inside the workspace (split: the workspace excludes the saved block)
   unsigned fix_cap;
@@ -104,6 +104,7 @@ struct FwdCtx {
   int mode;
   bool leg;
   Acc* acc;
+  unsigned* sync;  // fused input cast: [0] block ticket, [1 + group] arrivals
   int8_t *c0, *c1, *V, *c4;
   void* h;
   float *t4, *e4, *otab;

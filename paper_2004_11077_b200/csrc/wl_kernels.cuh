@@ -197,13 +197,22 @@ __device__ __forceinline__ void quant_rows_w64(const float* __restrict__ x, int8
   if (cg0 < cgstep) {
     const size_t cstride = (size_t)g.H * g.W;
     const float* xb = x + ((size_t)n * g.C * g.H + h0) * g.W + 4 * i;
+    // the channel-group pointer advances by a constant stride (the clamped tail group recomputes its four)
+    const float* pc = xb + (size_t)(4 * cg0) * cstride;
+    const size_t pstep = (size_t)4 * cgstep * cstride;
+    int8_t* sdst = srow + (4 * i) * ld + 4 * cg0;
 #pragma unroll 2
-    for (int cg = cg0; cg < ncg; cg += cgstep) {
+    for (int cg = cg0; cg < ncg; cg += cgstep, sdst += 4 * cgstep, pc += pstep) {
       // all four loads first (clamped channel, discarded below) so they are in flight together
       float4 v[4];
+      if (4 * cg + 3 < g.C) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        v[u] = __ldg(reinterpret_cast<const float4*>(xb + (size_t)min(4 * cg + u, g.C - 1) * cstride));
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(pc + (size_t)u * cstride));
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = __ldg(reinterpret_cast<const float4*>(xb + (size_t)min(4 * cg + u, g.C - 1) * cstride));
+      }
       // pixel pairs on packed f32x2: y = fma(v, rc, 1.5 * 2^23) holds the signed half-even code in its low
       // byte (rint is odd-symmetric, so this equals the sign * rint(|v| * rc) of quant_fast); d = fma(v,
       // -rc, k) is the distance to that integer.  |v| * rc <= qmax * (1 + 2^-24), so no clamp is needed.
@@ -235,15 +244,28 @@ __device__ __forceinline__ void quant_rows_w64(const float* __restrict__ x, int8
           }
       }
 #pragma unroll
-      for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(srow + (4 * i + p) * ld + 4 * cg) = wd[p];
+      for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(sdst + p * ld) = wd[p];
     }
   }
   __syncthreads();
   uint32_t* dst = reinterpret_cast<uint32_t*>(c0 + ((size_t)n * g.H + h0) * g.W * g.Cp);
   const int wpr = g.Cp >> 2, lw = __ffs(wpr) - 1;  // 32-bit words per pixel (a power of two)
-  for (int j = threadIdx.x; j < nrow * g.W * wpr; j += blockDim.x) {
-    const int pix = j >> lw, jw = j & (wpr - 1);
-    dst[j] = *reinterpret_cast<const uint32_t*>(srow + pix * ld + 4 * jw);
+  const int total = nrow * g.W * wpr;
+  if (wpr <= (int)blockDim.x && (blockDim.x & (wpr - 1)) == 0) {
+    // the block width is a multiple of the words per pixel: a thread keeps its word column, pixels advance
+    // by blockDim / wpr per step
+    const int pstride = (int)blockDim.x >> lw;
+    const int8_t* sp = srow + (threadIdx.x >> lw) * ld + 4 * (threadIdx.x & (wpr - 1));
+    uint32_t* dp = dst + threadIdx.x;
+    const int sstep = pstride * ld;
+    int j = threadIdx.x;
+#pragma unroll 4
+    for (; j < total; j += blockDim.x, sp += sstep, dp += blockDim.x) *dp = *reinterpret_cast<const uint32_t*>(sp);
+  } else {
+    for (int j = threadIdx.x; j < total; j += blockDim.x) {
+      const int pix = j >> lw, jw = j & (wpr - 1);
+      dst[j] = *reinterpret_cast<const uint32_t*>(srow + pix * ld + 4 * jw);
+    }
   }
 }
 
@@ -254,6 +276,104 @@ __global__ void __launch_bounds__(256, WL_QI_MINB) quant_input_w64_kernel(const 
   const int h0 = blockIdx.x * rh, n = blockIdx.y;
   const StageQ q = load_float_stage(acc[(size_t)group_of_image(n, g) * ST_COUNT + ST_INPUT], b.q[ST_INPUT]);
   quant_rows_w64(x, c0, g, q, h0, rh, n, srow);
+}
+
+// Fused cast "input" for fp32 x with W % 4 == 0 and W <= 64: one launch that reads x from HBM once.
+// Block = one band of rh rows, taken from an atomic ticket (tickets start in order, so every block with a
+// smaller ticket is resident or done).  Ticket t reduces max|x| of band t % nb of image n1 = t / nb into the
+// group's Acc::M and arrives on the group's counter; then it quantises the same band of image n2 = n1 - lag
+// exactly as quant_input_w64_kernel does, after checking that n2's group is complete.  lag >= images per
+// group, so a block only ever waits for smaller tickets, whose reductions wait for nothing: no deadlock
+// whatever the number of resident blocks.  The second read of a band follows the first by lag images
+// (lag * C * H * W * 4 bytes of other traffic, a few tens of MB): an L2 hit.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+struct CastShared {
+  double maxabs, scale;
+  float rcp;
+  unsigned ticket;
+  unsigned wmax[8];
+};
+template <int kInTU = 0>
+__global__ void __launch_bounds__(256, WL_QI_MINB) cast_input_w64_kernel(const float* __restrict__ x, int8_t* __restrict__ c0,
+                                                             Geo g, Bits b, Acc* acc, int rh, int lag, unsigned* sync) {
+  extern __shared__ __align__(16) int8_t srow[];
+  __shared__ CastShared cs;
+  if (threadIdx.x == 0) cs.ticket = atomicAdd(&sync[0], 1u);
+  __syncthreads();
+  const int nb = (g.H + rh - 1) / rh;
+  const int n1 = (int)(cs.ticket / (unsigned)nb), h0 = (int)(cs.ticket - (unsigned)n1 * nb) * rh, n2 = n1 - lag;
+  if (n1 < g.N) {
+    const int nrow = min(rh, g.H - h0);
+#ifndef WL_CAST_NOPF
+    // the whole band is requested from DRAM at once (per-line L2 prefetches: the bulk form is a uniform-datapath
+    // instruction that the compiler serialises over the lanes); the loads below
+    // then find their lines in L2 or in flight instead of exposing DRAM latency 8 loads at a time
+    for (int ch = threadIdx.x; ch < g.C; ch += blockDim.x) {
+      const char* run = reinterpret_cast<const char*>(x + (((size_t)n1 * g.C + ch) * g.H + h0) * g.W);
+      const int bytes = nrow * g.W * 4;
+      for (int o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(run + o));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(run + bytes - 4));
+    }
+#endif
+    const int nf4 = (nrow * g.W) >> 2, ncg = g.Cp >> 2;
+    const int i = threadIdx.x % nf4, cg0 = threadIdx.x / nf4, cgstep = blockDim.x / nf4;
+    unsigned m = 0;
+    if (cg0 < cgstep) {
+      // per channel one pointer; max over the sign-cleared bit patterns (monotone for non-negative floats)
+      const size_t cstride = (size_t)g.H * g.W;
+      const float* pch = x + ((size_t)n1 * g.C * g.H + h0) * g.W + 4 * i + (size_t)(4 * cg0) * cstride;
+      const size_t pstep = (size_t)4 * cgstep * cstride;
+      unsigned ma = 0, mb = 0;
+#pragma unroll 2
+      for (int cg = cg0; cg < ncg; cg += cgstep, pch += pstep) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = 4 * cg + u < g.C ? __ldg(reinterpret_cast<const uint4*>(pch + (size_t)u * cstride)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ma = max(ma, max(v[u].x & 0x7fffffffu, v[u].y & 0x7fffffffu));
+          mb = max(mb, max(v[u].z & 0x7fffffffu, v[u].w & 0x7fffffffu));
+        }
+      }
+      m = max(ma, mb);
+    }
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) cs.wmax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int w = 1; w < 8; ++w) m = max(m, cs.wmax[w]);
+      const int grp = group_of_image(n1, g);
+      if (m) atomicMax(&acc[(size_t)grp * ST_COUNT + ST_INPUT].M, max_to_f64_bits<float>(m));
+      __threadfence();
+      atomicAdd(&sync[1 + grp], 1u);
+    }
+  }
+  if (n2 < 0) return;
+  if (threadIdx.x == 0) {
+    const int grp = group_of_image(n2, g);
+    const unsigned target = (unsigned)nb * (unsigned)min(g.ipg, g.N - grp * g.ipg);
+    while (ld_acquire_u32(&sync[1 + grp]) < target) __nanosleep(32);
+    Acc a;
+    a.M = __ldcg(&acc[(size_t)grp * ST_COUNT + ST_INPUT].M);
+    const StageQ q = load_float_stage(a, b.q[ST_INPUT]);
+    cs.maxabs = q.maxabs;
+    cs.scale = q.scale;
+    cs.rcp = q.rcp;
+  }
+  __syncthreads();
+  StageQ q;
+  q.M = 0;
+  q.maxabs = cs.maxabs;
+  q.scale = cs.scale;
+  q.rcp = cs.rcp;
+  q.qmax = b.q[ST_INPUT];
+  quant_rows_w64(x, c0, g, q, h0, rh, n2, srow);
 }
 
 __device__ __forceinline__ void load_input_tile(const int8_t* __restrict__ c0, const Geo& g, int n, int tile, int c,
