@@ -345,17 +345,16 @@ __global__ void __launch_bounds__(256, WL_QI_MINB) cast_input_w64_kernel(const f
     m = __reduce_max_sync(0xffffffffu, m);
     if ((threadIdx.x & 31) == 0) cs.wmax[threadIdx.x >> 5] = m;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // arrive: nobody in this block waits for it (lag >= 1)
 #pragma unroll
       for (int w = 1; w < 8; ++w) m = max(m, cs.wmax[w]);
       const int grp = group_of_image(n1, g);
       if (m) atomicMax(&acc[(size_t)grp * ST_COUNT + ST_INPUT].M, max_to_f64_bits<float>(m));
-      __threadfence();
-      atomicAdd(&sync[1 + grp], 1u);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&sync[1 + grp]) : "memory");
     }
   }
   if (n2 < 0) return;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 32) {  // another warp than the arriving one: the two round trips overlap
     const int grp = group_of_image(n2, g);
     const unsigned target = (unsigned)nb * (unsigned)min(g.ipg, g.N - grp * g.ipg);
     while (ld_acquire_u32(&sync[1 + grp]) < target) __nanosleep(32);
