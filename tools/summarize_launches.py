@@ -19,8 +19,8 @@ def main(path, out):
         key = (name, r[gi], r[bi])
         agg.setdefault(key, []).append(float(r[vi].replace(",", "")) / 1e3)
     ours = {k: v for k, v in agg.items() if k[0].startswith("wl::") or "gemm_i8" in k[0]}
-    # per forward: each wl kernel's launches / number of forwards (quant_input runs once per forward)
-    nfwd = max(len(v) for k, v in ours.items() if "quant_input" in k[0])
+    # per forward: each wl kernel's launches / number of forwards (the input cast runs once per forward)
+    nfwd = max(len(v) for k, v in ours.items() if "quant_input" in k[0] or "cast_input" in k[0])
     step = sum(sum(v) for v in ours.values()) / nfwd
     with open(out, "w") as f:
         f.write("kernel,grid,block,launches,mean_us,per_forward_us,share_of_forward\n")
