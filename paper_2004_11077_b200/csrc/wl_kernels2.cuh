@@ -894,13 +894,13 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
   // max is recomputed by the whole warp (rare): lanes over the entry's output columns.
   const int nchunk = g.Kp / bn;
   const int lane = threadIdx.x & 31;
+  // 36 * T < 2^27 (make_layout rejects larger calls): 32-bit row arithmetic, no 64-bit divisions
   const unsigned T = (unsigned)g.T;
-  const unsigned long long rows = 36ull * T;
-  const unsigned long long nthr = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned rows = 36u * T;
+  const unsigned nthr = gridDim.x * blockDim.x;
   const bool tmajor = g.TP * g.ipg < 32;
-  for (unsigned long long r0 = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; r0 < rows;
-       r0 += nthr) {
-    const unsigned long long rr = r0 + lane;
+  for (unsigned r0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; r0 < rows; r0 += nthr) {
+    const unsigned rr = r0 + lane;
     const bool valid = rr < rows;
     // Lane -> table row.  Large groups: consecutive lanes are consecutive tiles of one xi (coalesced table
     // reads; a warp meets at most two groups).  Groups of fewer than 32 tiles (small images): the argmax of
@@ -909,26 +909,31 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
     // consecutive tiles, i.e. at most two groups per warp again.
     unsigned xi, t;
     if (tmajor) {
-      t = valid ? (unsigned)(rr / 36u) : 0u;
-      xi = valid ? (unsigned)(rr - 36ull * t) : 0u;
+      t = valid ? rr / 36u : 0u;
+      xi = valid ? rr - 36u * t : 0u;
     } else {
-      xi = valid ? (unsigned)(rr / T) : 0u;
-      t = valid ? (unsigned)(rr - (unsigned long long)xi * T) : 0u;
+      xi = valid ? rr / T : 0u;
+      t = valid ? rr - xi * T : 0u;
     }
-    const unsigned long long r = (unsigned long long)xi * T + t;  // table row
+    const unsigned r = xi * T + t;  // table row
     const int grp = (int)g.fipg.div(g.fTP.div(t));
     const unsigned long long M = valid ? acc[(size_t)grp * ST_COUNT + ST_HAD].M : 0ull;
     unsigned v[4] = {0u, 0u, 0u, 0u};
     if (valid) {
       if (nchunk == 4) {
-        const uint4 q = *reinterpret_cast<const uint4*>(table + r * 4);
+        const uint4 q = *reinterpret_cast<const uint4*>(table + (size_t)r * 4);
         v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
       } else {
-        for (int c = 0; c < nchunk && c < 4; ++c) v[c] = table[r * nchunk + c];
+        for (int c = 0; c < nchunk && c < 4; ++c) v[c] = table[(size_t)r * nchunk + c];
       }
     }
+    // entries never exceed the group maximum: one vote on the row maximum skips the chunk loop for almost
+    // every warp (rows with more than 4 chunks always take it)
+    const unsigned vmax = max(max(v[0], v[1]), max(v[2], v[3]));
+    if (nchunk <= 4 && !__any_sync(0xffffffffu, valid && vmax != 0 && (unsigned long long)vmax == M)) continue;
     for (int chunk = 0; chunk < nchunk; ++chunk) {
-      const unsigned vc = chunk < 4 ? v[chunk & 3] : (valid ? table[r * nchunk + chunk] : 0u);
+      const unsigned v4 = chunk == 0 ? v[0] : chunk == 1 ? v[1] : chunk == 2 ? v[2] : v[3];
+      const unsigned vc = chunk < 4 ? v4 : (valid ? table[(size_t)r * nchunk + chunk] : 0u);
       unsigned mask = __ballot_sync(0xffffffffu, valid && vc != 0 && (unsigned long long)vc == M);
       while (mask) {
         const int l = __ffs(mask) - 1;
