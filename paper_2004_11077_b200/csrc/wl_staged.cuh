@@ -590,9 +590,14 @@ struct CwShape {
   int vec4;        // y rows may be stored as float4 (Wo % 4 == 0 and y 16-byte aligned)
 };
 inline CwShape cw_shape(int tw) {
-  if (tw <= 8) return {(8 / tw) * tw, (8 / tw) * tw, 8, 0};
-  if (tw <= 16) return {tw, (tw + 1) / 2, 4, 0};
-  if (tw <= 32) return {tw, (tw + 3) / 4, 2, 0};
+  // Items are deep in tiles and narrow in channels: per channel an item then writes one contiguous range of
+  // 4 * (R / tw) output rows.  Config 4 (tw = 14): 1 / 2 / 4 tile rows per item = 1.38 / 1.33 / 1.31 ms.
+#ifndef WL_CW_SMALL_PASSES
+#define WL_CW_SMALL_PASSES 4
+#endif
+  if (tw <= 8) return {WL_CW_SMALL_PASSES * (8 / tw) * tw, (8 / tw) * tw, 8 / WL_CW_SMALL_PASSES, 0};
+  if (tw <= 16) return {4 * tw, (tw + 1) / 2, 1, 0};
+  if (tw <= 32) return {2 * tw, (tw + 3) / 4, 1, 0};
   return {32, 8, 2, 0};
 }
 struct StagedCw {
