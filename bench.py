@@ -345,26 +345,45 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     launches = r.launches()
 
+    # The step: the public forward of the whole batch.  With per-image scale groups the batch is issued as
+    # `parts` independent calls on forked streams (QuantWinogradConv.forward_split, bit-identical to one call):
+    # one part's kernel tails and helper kernels overlap the other part's passes.  --parts 1 = one stream.
+    parts = args.parts if groups == "image" else 1
+
+    def step():
+        if parts > 1:
+            r.forward_split(x, w, padding=pad, out=y, scale_groups=groups, parts=parts)
+        else:
+            r.forward(x, w, padding=pad, out=y, scale_groups=groups)
+
     for _ in range(args.warmup):
-        r.forward(x, w, padding=pad, out=y, scale_groups=groups)
+        step()
     torch.cuda.synchronize()
     _barrier(world)
     clocks = ClockSampler(local_rank)
     if rank == 0:
         clocks.start()
-    _lib.profile_enable(True)
-    _lib.profile_read()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     _barrier(world)
     e0.record(stream)
     for _ in range(args.steps):
-        r.forward(x, w, padding=pad, out=y, scale_groups=groups)
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
     _barrier(world)
     ms_rank = e0.elapsed_time(e1) / args.steps
+    # Per-slot kernel times: the same K steps as single-stream calls with the library's event marks on (the
+    # marks need one stream), still under the clock sampler.
+    _lib.profile_enable(True)
+    _lib.profile_read()
+    e0.record(stream)
+    for _ in range(args.steps):
+        r.forward(x, w, padding=pad, out=y, scale_groups=groups)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_single = e0.elapsed_time(e1) / args.steps
     kern, calls = _lib.profile_read()
     _lib.profile_enable(False)
     clk = clocks.stop() if rank == 0 else None
@@ -483,6 +502,7 @@ def run_ours(args, rank, world, local_rank):
     roof["traffic_source"] = "profiles/r02_ncu_full_cfg4_v5.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
     roof["algorithmic_bytes_per_launch"] = kb
     roof["ms_per_launch"] = dom_ms
+    roof["timed_in"] = "single-stream pass of the same K steps with the library's CUDA-event marks, right after the timed region"
     roof["peak_source"] = peak_kind if roof["bound"] == "hbm" else ("torch._int_mm 8192^3 measured live" if i8_peak else "2x bf16 planning")
     # every slot against the same two ceilings; `limiter` is what ncu shows bounds the slot's main kernel
     # (profiles/r02_ncu_full_cfg4_v5.csv): the five transform passes are CUDA-core FMA/ALU-pipe bound, so their
@@ -507,6 +527,8 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "int8", "data": "synthetic (torch.randn on device, seeded per rank)",
         "config": {"workload": "config4: N=1024/GPU Cin=Cout=256 56x56 pad1 Legendre F(4,3) 8b fwd",
                    "scale_groups": groups, "l2": "inputs (3.29 GB) larger than L2", "global_batch": world * n,
+                   "call": (f"QuantWinogradConv.forward_split, {parts} parts on forked streams" if parts > 1
+                            else "QuantWinogradConv.forward, one stream"),
                    "parallelism": f"batch-sharded x{world}, no collective"},
         "effective_tops": world * eff / (ms * 1e-3) / 1e12,
         "layer_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms * 1e-3), "hbm_bytes": bytes_,
@@ -515,7 +537,8 @@ def run_ours(args, rank, world, local_rank):
         "per_rank_ms": per_rank_ms,
         "kernel_ms": {kname: round(v, 4) for kname, v in per_kernel.items()},
         "kernel_roofline": slots,
-        "gpu_launches": launches * args.steps,
+        "gpu_launches": launches * parts * args.steps,
+        "streams": parts, "ms_per_step_single_stream": ms_single,
         "graph_replay": graph_replay,
         "clocks": clk,
         "e2e": e2e,
@@ -764,6 +787,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="train workload: time the eager step only")
     ap.add_argument("--scale-groups", default="image", choices=["image", "batch"])
+    ap.add_argument("--parts", type=int, default=2,
+                    help="layer workload: independent calls on forked streams per step (per-image scale groups)")
     ap.add_argument("--workload", default="layer", choices=["layer", "train", "bwd", "sweep"],
                     help="layer: config-4 layer throughput (default); train: config-5 ResNet-18 training step; "
                          "bwd: config-3 forward + STE backward lines; sweep: every forward config + bwd")

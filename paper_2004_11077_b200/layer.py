@@ -149,6 +149,7 @@ class QuantWinogradConv:
         self.wcache = WeightCache()
         self.ws = None
         self._last = None
+        self._parts = None   # (shape, cache, workspace) of every part of the last forward_split call
 
     def _shape(self, x, w, padding, groups):
         n, cin, h, wd = (int(v) for v in x.shape)
@@ -242,6 +243,63 @@ class QuantWinogradConv:
                     ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(x.device)), "wl_forward")
         # stats / debug views read the buffer holding the stage slots (saved block or workspace)
         self._last = (shape, cache, saved if saved is not None else ws, saved is None)
+        self._parts = None
+        return out
+
+    def forward_split(self, x: torch.Tensor, w: torch.Tensor, bias=None, padding: int = 0, scale_groups="image",
+                      out: torch.Tensor | None = None, parts: int = 2) -> torch.Tensor:
+        """forward() of a large batch as `parts` independent calls on `parts` streams.
+
+        Scale groups never straddle a part, so every part is exactly the call the reference would make on
+        those images and the result is bit-identical to forward().  Part 0 runs on the current stream, the
+        others on side streams forked from and joined back into it (capturable in a CUDA graph); each part
+        has its own workspace.  One part's kernel tails and short helper kernels (finalize / fixup passes
+        that occupy a few SMs) overlap the other part's full-width passes: config 4 runs about 3 % faster."""
+        _check_conv_args(x, w)
+        if scale_groups == "batch":
+            raise ValueError("forward_split needs per-image or per-k-images scale groups")
+        n = int(x.shape[0])
+        ipg = self._shape(x, w, padding, scale_groups).images_per_group
+        parts = max(1, min(int(parts), n // ipg))
+        if parts == 1:
+            return self.forward(x, w, bias=bias, padding=padding, scale_groups=scale_groups, out=out)
+        f64 = x.dtype == torch.float64
+        x = x.contiguous() if f64 else x.contiguous().float()
+        w = w.contiguous() if w.dtype == torch.float64 else w.contiguous().float()  # the object forward() caches
+        ho, wo = int(x.shape[2]) + 2 * padding - 2, int(x.shape[3]) + 2 * padding - 2
+        oshape = (n, int(w.shape[0]), ho, wo)
+        if out is None:
+            out = torch.empty(oshape, dtype=x.dtype, device=x.device)
+        elif out.dtype != x.dtype or not out.is_contiguous() or tuple(out.shape) != oshape:
+            raise ValueError(f"out must be a contiguous {x.dtype} tensor of shape {oshape}")
+        dev = x.device
+        bounds = [((n // ipg) * i // parts) * ipg for i in range(parts + 1)]
+        cur = torch.cuda.current_stream(dev)
+        if getattr(self, "_part_streams", None) is None or len(self._part_streams) < parts - 1:
+            self._part_streams = [torch.cuda.Stream(dev) for _ in range(parts - 1)]
+        need = [self.workspace_bytes(self._shape(x[bounds[i]:bounds[i + 1]], w, padding, scale_groups))
+                for i in range(parts)]
+        pws = getattr(self, "_part_ws", None)
+        if pws is None or len(pws) != parts or any(t.numel() < b or t.device != dev for t, b in zip(pws, need)):
+            self._part_ws = pws = [torch.empty(b, dtype=torch.uint8, device=dev) for b in need]
+        self.wcache.get(self.dplan, self.qconfig, w)  # weight transform before the fork
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        done = []
+        for i in range(parts):
+            a, b = bounds[i], bounds[i + 1]
+            s = cur if i == 0 else self._part_streams[i - 1]
+            if i:
+                s.wait_event(fork)
+            with torch.cuda.stream(s):
+                self.forward(x[a:b], w, bias=bias, padding=padding, scale_groups=scale_groups, out=out[a:b],
+                             workspace=pws[i])
+                done.append((self._last[0], self._last[1], pws[i]))
+                if i:
+                    e = torch.cuda.Event()
+                    e.record(s)
+                    cur.wait_event(e)
+        self._parts = done
         return out
 
     def capture(self, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, bias=None, padding: int = 0,
@@ -344,7 +402,12 @@ class QuantWinogradConv:
 
     def stats(self):
         """StageStat rows of the last forward (synchronises the stream)."""
+        if self._parts is not None:  # forward_split: the groups of every part, in batch order
+            return [row for part in self._parts for row in self._stats_of(*part)]
         shape, cache, accbuf, _ = self._last
+        return self._stats_of(shape, cache, accbuf)
+
+    def _stats_of(self, shape, cache, accbuf):
         ns = _lib.lib().wl_num_stages(self.dplan.handle)
         groups = shape.n // shape.images_per_group
         arr = (_lib.wl_stage_stat * (groups * ns))()

@@ -263,6 +263,39 @@ def test_unaligned_input_and_output_pointers():
         assert torch.equal(yu, y0)
 
 
+@pytest.mark.parametrize("n,groups,parts", [(6, "image", 2), (7, "image", 3), (8, 2, 2), (8, 2, 3), (12, 4, 8), (5, "image", 1)])
+def test_forward_split_equals_forward(n, groups, parts):
+    """forward_split (independent parts on forked streams, own workspaces) gives the bits and the StageStats of
+    forward(): scale groups never straddle a part.  Also as a captured CUDA graph (the fork/join is capturable)."""
+    rng = np.random.default_rng(100 + n)
+    c, k, h = 24, 40, 12
+    x = torch.as_tensor((rng.standard_normal((n, c, h, h)) * rng.uniform(0.3, 4.0, (n, 1, 1, 1))).astype(np.float32),
+                        device="cuda")
+    w = torch.as_tensor(_kaiming(rng, k, c), device="cuda")
+    b = torch.as_tensor(rng.standard_normal(k).astype(np.float32), device="cuda")
+    for mode in ("legendre", "canonical"):
+        r = W.QuantWinogradConv(PLAN, mode, W.QuantConfig.from_name("8b+9b"))
+        y0 = r.forward(x, w, bias=b, padding=1, scale_groups=groups).clone()
+        s0 = r.stats()
+        y1 = r.forward_split(x, w, bias=b, padding=1, scale_groups=groups, parts=parts)
+        s1 = r.stats()
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y0)
+        assert s1 == s0
+        y2 = torch.zeros_like(y0)
+        r.forward_split(x, w, bias=b, padding=1, scale_groups=groups, parts=parts, out=y2)  # buffers for the capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            r.forward_split(x, w, bias=b, padding=1, scale_groups=groups, parts=parts, out=y2)
+        y2.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(y2, y0)
+    with pytest.raises(ValueError):
+        r.forward_split(x, w, padding=1, scale_groups="batch")
+
+
 def test_degenerate_inputs_ties_and_equal_maxima():
     rng = np.random.default_rng(5)
     cases = [np.zeros((2, 8, 8, 8)), np.ones((2, 8, 8, 8)), rng.integers(-2, 3, (2, 8, 8, 8)),
