@@ -317,21 +317,28 @@ int make_layout(const wl_shape* s, const wl_qcfg* q, Layout* L, bool split) {
   L->bn = (g.Kp >= 256 ? 256 : g.Kp) / 4;  // table chunk = one max-pass epilogue warp's columns (EpiHadMax::kGroups)
   const size_t CB = (g.C + 31) / 32, KB = (g.K + 31) / 32;
   const size_t ents[kNumTables] = {g.T * CB, g.T * CB, (size_t)36 * g.T * (g.Kp / L->bn), g.T * KB, g.T * KB};
-  for (int i = 0; i < kNumTables; ++i) {
+  // the four transform-stage tables and the fix-list counters are zeroed by one memset per call: they are
+  // laid out back to back ([IBC][IT][OBC][OUT][counters + items]); the Hadamard table (fully written by
+  // the GEMM max epilogue) follows
+  auto place_table = [&](int i) {
     L->off_tab[i] = o;
     L->tab_bytes[i] = ents[i] * sizeof(unsigned);
     o = align256(o + L->tab_bytes[i]);
-  }
+  };
+  for (int i = 0; i < kNumTables; ++i)
+    if (kTableStage[i] != ST_HAD) place_table(i);
+  // deferred-fix list: counters + unit ids (expected ~0.2% of units; overflow falls back inline)
+  L->off_fix = o;
+  const size_t units = (size_t)g.T * std::max(g.C, g.K);
+  L->fix_cap = g_fix_cap_override ? g_fix_cap_override : (unsigned)std::max<size_t>(4096, units / 16);
+  o = align256(o + kFixHeaderBytes + sizeof(unsigned) * (size_t)std::max<size_t>(L->fix_cap, 4096));
+  for (int i = 0; i < kNumTables; ++i)
+    if (kTableStage[i] == ST_HAD) place_table(i);
   // dequantised output table (output widths <= 12 bits; wider widths dequantise in fp64 inline)
   L->off_otab = o;
   if (q->output_transform_bits <= 12) o = align256(o + sizeof(float) * (size_t)L->groups * ((1 << q->output_transform_bits) - 1));
   L->off_odq = o;
   if (q->output_transform_bits <= 12) o = align256(o + sizeof(float4) * (size_t)L->groups);
-  // deferred-fix list: counters + unit ids (expected ~0.2% of units; overflow falls back inline)
-  L->off_fix = o;
-  const size_t units = (size_t)g.T * std::max(g.C, g.K);
-  L->fix_cap = g_fix_cap_override ? g_fix_cap_override : (unsigned)std::max<size_t>(4096, units / 16);
-  o = align256(o + 64 + sizeof(unsigned) * (size_t)std::max<size_t>(L->fix_cap, 4096));
   L->total = o;
   return WL_OK;
 }
@@ -730,12 +737,14 @@ int wl_debug_layout(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q, si
 
 int wl_forward_launches(const wl_plan* plan, const wl_shape* s, const wl_qcfg* q) {
   if (!plan) return WL_ERR_ARG;
-  // absmax, quant, [in_a|in_b(+fixup), finalize, exec, params] x2|1, in_c, fixup, gemm max, finalize,
-  // params, gemm codes, tie fixup, [out_a|out_b(+fixup), finalize, exec, params] x2|1, output table,
+  // input cast (one fused launch, or absmax + quant), [in_a|in_b(+fixup), finalize, exec] x2|1, in_c, fixup,
+  // gemm max, finalize, gemm codes, tie fixup, [out_a|out_b(+fixup), finalize, exec] x2|1, output table,
   // out_c, fixup
+  // (the count assumes the fp32 entry point with a 16-byte aligned x for the fused cast)
   const int otab = (q && q->output_transform_bits <= 12) ? 1 : 0;
-  (void)s;
-  return (plan->mode == WL_LEGENDRE ? 29 : 19) + otab;
+  const int ipg = s ? (s->images_per_group > 0 ? s->images_per_group : s->n) : 1;
+  const int cast = s && cast_fusable_shape(s->c_in, s->h, s->w, ipg) ? 1 : 2;
+  return (plan->mode == WL_LEGENDRE ? 22 : 14) + cast + otab;
 }
 
 int wl_forward(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const float* x, const void* cache,

@@ -14,13 +14,18 @@
 
 namespace wl {
 
+// arguments of stage_params_tail for one stage (the done counter lives in the zeroed fix-list header)
+ParamsTail params_tail(const FwdCtx& c, int stage) {
+  return ParamsTail{c.L->groups, c.b.q[stage], stage == ST_HAD ? 0.f : stage_depth(c.mode, stage),
+                    c.fl.count + kDoneSlot0 + stage};
+}
+
 template <int MODE, int STAGE>
 static void finalize_input_t(FwdCtx& c) {
   finalize_input_kernel<MODE, STAGE><<<c.fin_blocks, 256, 0, c.st>>>(c.c0, c.c1, c.g, c.b, c.acc, c.pf,
                                                                      c.tabs.t[STAGE], c.E.e[STAGE], c.fl);
-  finalize_input_exec<MODE, STAGE><<<c.fin_blocks, 256, 0, c.st>>>(c.c0, c.c1, c.g, c.b, c.acc, c.pf, c.fl);
-  stage_params_kernel<<<c.pgrid, 128, 0, c.st>>>(c.acc, c.L->groups, STAGE, c.b.q[STAGE], c.E.e[STAGE],
-                                                 stage_depth(c.mode, STAGE));
+  finalize_input_exec<MODE, STAGE><<<c.fin_blocks, 256, 0, c.st>>>(c.c0, c.c1, c.g, c.b, c.acc, c.pf, c.fl,
+                                                                   params_tail(c, STAGE));
 }
 
 void finalize_input_stage(FwdCtx& c, int stage) {
@@ -37,9 +42,8 @@ static void finalize_output_t(FwdCtx& c) {
   const HT* hh = reinterpret_cast<const HT*>(c.h);
   finalize_output_kernel<MODE, STAGE, HT, T4><<<c.fin_blocks, 256, 0, c.st>>>(hh, c.c4, c.g, c.b, c.acc, c.pf,
                                                                               c.tabs.t[STAGE], c.E.e[STAGE], c.fl);
-  finalize_output_exec<MODE, STAGE, HT, T4><<<c.fin_blocks, 256, 0, c.st>>>(hh, c.c4, c.g, c.b, c.acc, c.pf, c.fl);
-  stage_params_kernel<<<c.pgrid, 128, 0, c.st>>>(c.acc, c.L->groups, STAGE, c.b.q[STAGE], c.E.e[STAGE],
-                                                 stage_depth(c.mode, STAGE));
+  finalize_output_exec<MODE, STAGE, HT, T4><<<c.fin_blocks, 256, 0, c.st>>>(hh, c.c4, c.g, c.b, c.acc, c.pf, c.fl,
+                                                                            params_tail(c, STAGE));
 }
 
 template <typename HT>
@@ -78,9 +82,6 @@ static int input_cast(FwdCtx& c, const XT* x) {
 #ifndef WL_CAST_LAG
 #define WL_CAST_LAG 1  // images between a band's max pass and its quantisation (>= images per group)
 #endif
-#ifndef WL_CAST_L2_BYTES
-#define WL_CAST_L2_BYTES (48ll << 20)  // x bytes read between the two reads of a band that L2 is trusted to keep
-#endif
   // band of rh rows per block: per channel one contiguous rh * W float run (at most 256 float4 slots and
   // ~60 KB of staging per block)
   int rh = WL_QI_RH;
@@ -88,7 +89,7 @@ static int input_cast(FwdCtx& c, const XT* x) {
   rh = std::min(rh, g.H);
   const int smem = rh * g.W * (g.Cp + 4);
   const int nb = (g.H + rh - 1) / rh;
-  if (w64 && (long long)g.ipg * per_image * 4 <= WL_CAST_L2_BYTES) {
+  if (w64 && cast_fusable_shape(g.C, g.H, g.W, g.ipg)) {
     // one launch, x read from HBM once (the second read of a band hits L2)
     const int lag = (int)std::min<long long>(std::max(g.ipg, WL_CAST_LAG),
                                              std::max<long long>(g.ipg, WL_CAST_L2_BYTES / (per_image * 4)));
@@ -166,7 +167,7 @@ int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const
   c.ybytes = (int)sizeof(YT);
   c.E = stage_rowsums(plan->mode);
   c.fl.count = reinterpret_cast<unsigned*>(ws + L.off_fix);
-  c.fl.items = reinterpret_cast<unsigned*>(ws + L.off_fix + 64);
+  c.fl.items = reinterpret_cast<unsigned*>(ws + L.off_fix + kFixHeaderBytes);
   c.fl.cap = L.fix_cap;
   // grid-stride helper kernels: one wave covers every deferred unit / table row of config-4-sized calls;
   // small calls launch only the blocks their lists and tables can fill (launch-bound shapes)
@@ -180,11 +181,9 @@ int forward_impl(const wl_plan* plan, const wl_qcfg* q, const wl_shape* s, const
   prof_mark("begin", st);
   if ((rc = input_cast<XT>(c, x))) return rc;
 
-  for (int i = 0; i < kNumTables; ++i) {
-    c.tabs.t[kTableStage[i]] = reinterpret_cast<unsigned*>(ws + L.off_tab[i]);
-    if (kTableStage[i] != ST_HAD) WL_CUDA(cudaMemsetAsync(ws + L.off_tab[i], 0, L.tab_bytes[i], st));
-  }
-  WL_CUDA(cudaMemsetAsync(c.fl.count, 0, 64, st));
+  for (int i = 0; i < kNumTables; ++i) c.tabs.t[kTableStage[i]] = reinterpret_cast<unsigned*>(ws + L.off_tab[i]);
+  // one memset: the four transform-stage max tables and the fix-list counters are contiguous (make_layout)
+  WL_CUDA(cudaMemsetAsync(ws + L.off_tab[0], 0, L.off_fix + kFixHeaderBytes - L.off_tab[0], st));
   if (g.Cp <= 256 && !tmap_i8_4d(&c.c0map, c.c0, g.Cp, g.W, g.H, g.N, g.Cp, 6, 6))
     return fail(WL_ERR_CUDA, "cuTensorMapEncodeTiled (input window) failed");
 

@@ -342,8 +342,7 @@ int run_gemm_side(FwdCtx& c, const int8_t* U, const WeightHeader* wh) {
     // the table scan is one 16-byte load per (xi, tile) row: full occupancy (8 blocks of 256 per SM)
     const int fh_blocks = (int)std::max<long long>(1, std::min<long long>(4LL * WL_FH_MULT * num_sms(), (36LL * g.T + 255) / 256));
     finalize_hadamard_kernel<<<fh_blocks, 256, 0, st>>>(U, c.V, g, c.acc, wh->wacc, wstage, qu, c.b.q[ST_IT],
-                                                           c.tabs.t[ST_HAD], c.L->bn);
-    stage_params_kernel<<<c.pgrid, 128, 0, st>>>(c.acc, c.L->groups, ST_HAD, c.b.q[ST_HAD], 0.f, 0.f);
+                                                           c.tabs.t[ST_HAD], c.L->bn, params_tail(c, ST_HAD));
     prof_mark("gemm_hadamard_max", st);
   }
   auto requant = [&](auto ht) -> int {

@@ -37,6 +37,15 @@ inline int pow2_at_least(int v, int lo) {
 
 // ------------------------------------------------------------------ workspace layout
 constexpr int kNumTables = 5;  // IBC, IT, HAD, OBC, OUT
+// Fused input cast (cast_input_w64_kernel): fp32 x, 16-byte aligned, W % 4 == 0, W <= 64, and scale groups small
+// enough that L2 is trusted to keep a group between its max pass and its quantisation.
+#ifndef WL_CAST_L2_BYTES
+#define WL_CAST_L2_BYTES (48ll << 20)
+#endif
+inline bool cast_fusable_shape(int C, int H, int W, int ipg) {
+  return (W & 3) == 0 && W <= 64 && (long long)ipg * C * H * W * 4 <= WL_CAST_L2_BYTES;
+}
+constexpr int kFixHeaderBytes = 128;  // zeroed per call: fix-list / candidate counters [0, 16), stage done counters [16, 32)
 extern const int kTableStage[kNumTables];
 
 // The "saved" block [acc][V] comes first so that the STE backward, which reads only the per-group
@@ -125,6 +134,7 @@ struct FwdCtx {
 void finalize_input_stage(FwdCtx& c, int stage);
 void finalize_output_stage(FwdCtx& c, int stage, bool t4);
 void make_output_table(FwdCtx& c);
+ParamsTail params_tail(const FwdCtx& c, int stage);  // stage_params_tail arguments of one stage (wl_fwd.cu)
 
 template <int LD>
 int run_input_side(FwdCtx& c);  // wl_fwd_in.inc

@@ -10,7 +10,7 @@
 //     ties replayed in fp64 in the reference's operation order;
 //   * maxima: each pass writes the fp32 maximum of every 32-unit entry to a table plus the group's
 //     running fp32 maximum; finalize_* recomputes exactly only the entries within 2E of it
-//     (integer M, fp64 max_abs by replay), and stage_params_kernel derives r, band and scale.
+//     (integer M, fp64 max_abs by replay), and the last block of that kernel (stage_params_tail) derives r, band and scale.
 // Thread mapping: one (tile, channel) unit per thread, channel fastest, so every byte-plane access
 // of a warp is one contiguous 32-byte segment; 32-bit element offsets (host-checked < 2^32).
 #pragma once
@@ -331,19 +331,39 @@ __device__ __forceinline__ void fix_out_unit(const HT* __restrict__ h, const int
 }
 
 // r, threshold and reference scale of one stage for every group, once its M and F are final.
-template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
-__global__ void stage_params_kernel(Acc* __restrict__ acc, int groups, int stage, int qmax, float rowsum, float depth) {
-  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gi >= groups) return;
+// (M and F are read past L1: in the tail below other blocks' atomics produced them during this kernel.)
+__device__ __forceinline__ void stage_params_of(Acc* acc, int gi, int stage, int qmax, float depth) {
   Acc& a = acc[(size_t)gi * ST_COUNT + stage];
-  const long long M = (long long)a.M;
-  const double maxabs = __longlong_as_double((long long)a.F);
+  const long long M = (long long)__ldcg(&a.M);
+  const double maxabs = __longlong_as_double((long long)__ldcg(&a.F));
   a.r = M ? (float)((double)qmax / (double)M) : 0.f;
   // per-element band = ef * rowsum_i * max|tmp col j| (the element's fp32 error E_ij times qmax/M);
   // slack for r = fl(qmax/M) (relative 2^-24 on a value <= qmax) and the fma rounding of d
   a.ef = M ? (float)((double)qmax * ((double)depth + 0.5) * 5.9604644775390625e-8 / (double)M) : 0.f;
   a.thr = M ? 0.5f - (float)((qmax + 1) * 1.25 * 5.9604644775390625e-8) : 1.f;
   a.scale = maxabs > 0.0 ? maxabs / (double)qmax : 1.0;
+}
+
+// Tail of the kernel that makes a stage's M and F final: the last block to finish derives the fast-path
+// parameters of every group (one launch less per stage on the launch-bound small shapes).  `done` is the
+// stage's slot of the zeroed counter block (kDoneSlot0 + stage).  Every thread of the block must call it.
+constexpr int kDoneSlot0 = 16;
+struct ParamsTail {
+  int groups, qmax;
+  float depth;
+  unsigned* done;
+};
+__device__ __forceinline__ void stage_params_tail(Acc* acc, int stage, const ParamsTail& p) {
+  __shared__ int wl_tail_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    wl_tail_last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!wl_tail_last) return;
+  __threadfence();
+  for (int gi = threadIdx.x; gi < p.groups; gi += blockDim.x) stage_params_of(acc, gi, stage, p.qmax, p.depth);
 }
 
 // Dequantised fp32 output of every code of the output stage, per group (quantize.py:120-125:
@@ -587,7 +607,8 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
 template <int MODE, int STAGE>
 __global__ void __launch_bounds__(256) finalize_input_exec(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1,
                                                            Geo g, Bits b, Acc* __restrict__ acc,
-                                                           const PlanF64* __restrict__ pf, FixList fl) {
+                                                           const PlanF64* __restrict__ pf, FixList fl,
+                                                           ParamsTail tail) {
   const unsigned NB = (unsigned)((g.C + 31) >> 5);
   const unsigned cnt = fix_count(fl, kCandSlot0 + STAGE);
   const int lane = threadIdx.x & 31;
@@ -597,6 +618,7 @@ __global__ void __launch_bounds__(256) finalize_input_exec(const int8_t* __restr
     const int ch = (int)cb * 32 + lane;
     if (ch < g.C) exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, (int)t, ch);
   }
+  stage_params_tail(acc, STAGE, tail);
 }
 
 // ---------------------------------------------------------------------------------- output side
@@ -870,7 +892,8 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
 template <int MODE, int STAGE, typename HT, bool FROM_H = false>
 __global__ void __launch_bounds__(256) finalize_output_exec(const HT* __restrict__ h, const int8_t* __restrict__ c4,
                                                             Geo g, Bits b, Acc* __restrict__ acc,
-                                                            const PlanF64* __restrict__ pf, FixList fl) {
+                                                            const PlanF64* __restrict__ pf, FixList fl,
+                                                            ParamsTail tail) {
   const unsigned NB = (unsigned)((g.K + 31) >> 5);
   const unsigned cnt = fix_count(fl, kCandSlot0 + STAGE);
   const int lane = threadIdx.x & 31;
@@ -880,6 +903,7 @@ __global__ void __launch_bounds__(256) finalize_output_exec(const HT* __restrict
     const int ch = (int)cb * 32 + lane;
     if (ch < g.K) exact_output_unit<MODE, STAGE, HT, FROM_H>(h, c4, g, b, acc, pf, (int)t, ch);
   }
+  stage_params_tail(acc, STAGE, tail);
 }
 
 // Hadamard: table[(xi*T + t)*nchunk + chunk] = exact max |I| over the row chunk (written by the GEMM
@@ -888,7 +912,7 @@ __global__ void __launch_bounds__(256) finalize_output_exec(const HT* __restrict
 template <int kInTU = 0>  // header-defined kernel: instantiated only in the TUs that launch it
 __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __restrict__ U, const int8_t* __restrict__ V, Geo g,
                                          Acc* __restrict__ acc, const Acc* __restrict__ wacc, int wstage, int qmax_u,
-                                         int qmax_v, const unsigned* __restrict__ table, int bn) {
+                                         int qmax_v, const unsigned* __restrict__ table, int bn, ParamsTail tail) {
   // Flat, fully parallel scan: thread per (xi, t) table row (nchunk <= 4 entries, one 16-byte load
   // when nchunk == 4); consecutive threads read consecutive rows.  An entry equal to its group's exact
   // max is recomputed by the whole warp (rare): lanes over the entry's output columns.
@@ -968,6 +992,7 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
       }
     }
   }
+  stage_params_tail(acc, ST_HAD, tail);
 }
 
 // ---------------------------------------------------------------------------------- fixup kernels
