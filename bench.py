@@ -349,8 +349,6 @@ def run_ours(args, rank, world, local_rank):
     # `parts` independent calls on forked streams (QuantWinogradConv.forward_split, bit-identical to one call):
     # one part's kernel tails and helper kernels overlap the other part's passes.  --parts 1 = one stream.
     parts = args.parts if groups == "image" else 1
-    if args.grid_div > 1:
-        _lib.lib().wl_debug_set_grid_div(args.grid_div)
 
     def step():
         if parts > 1:
@@ -791,8 +789,6 @@ def main():
     ap.add_argument("--scale-groups", default="image", choices=["image", "batch"])
     ap.add_argument("--parts", type=int, default=2,
                     help="layer workload: independent calls on forked streams per step (per-image scale groups)")
-    ap.add_argument("--grid-div", type=int, default=1,
-                    help="measurement hook: persistent transform kernels at occupancy / div blocks per SM")
     ap.add_argument("--workload", default="layer", choices=["layer", "train", "bwd", "sweep"],
                     help="layer: config-4 layer throughput (default); train: config-5 ResNet-18 training step; "
                          "bwd: config-3 forward + STE backward lines; sweep: every forward config + bwd")

@@ -161,10 +161,6 @@ int wl_debug_gemm_bf16(const void* A, int PA, const void* B, int PB, int batch, 
  * every producer onto its inline fallback; results must not change (tests/test_gpu_parity.py). */
 int wl_debug_set_fix_cap(unsigned cap);
 
-/* Measurement hook: the persistent transform kernels launch occupancy / div blocks per SM (1 = full, the
- * default), so that two calls on two streams can be co-resident on every SM (bench.py --grid-div). */
-int wl_debug_set_grid_div(int div);
-
 const char* wl_last_error(void);
 
 #ifdef __cplusplus

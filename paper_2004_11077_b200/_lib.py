@@ -40,7 +40,7 @@ EXPORTS = ("wl_plan_create", "wl_plan_destroy", "wl_plan_mode", "wl_weight_cache
            "wl_forward_launches", "wl_profile_enable", "wl_profile_read", "wl_backward_workspace_size",
            "wl_backward", "wl_float_workspace_size", "wl_forward_float", "wl_direct_workspace_size",
            "wl_direct_quantized", "wl_direct_quantized_f64", "wl_direct_f64", "wl_train_sizes", "wl_forward_train",
-           "wl_debug_set_fix_cap", "wl_debug_set_grid_div", "wl_debug_gemm_bf16", "wl_last_error")
+           "wl_debug_set_fix_cap", "wl_debug_gemm_bf16", "wl_last_error")
 
 
 def lib():
@@ -66,7 +66,6 @@ def lib():
     L.wl_train_sizes.argtypes = [VP, P(wl_shape), P(wl_qcfg), P(S), P(S)]
     L.wl_forward_train.argtypes = [VP, P(wl_qcfg), P(wl_shape), VP, VP, VP, VP, VP, S, VP, S, VP]
     L.wl_debug_set_fix_cap.argtypes = [ctypes.c_uint]
-    L.wl_debug_set_grid_div.argtypes = [I]
     L.wl_debug_gemm_bf16.argtypes = [VP, I, VP, I, I, I, I, I, I, VP, I, ctypes.c_float, VP]
     L.wl_num_stages.argtypes = [VP]
     L.wl_read_stats.argtypes = [VP, P(wl_shape), P(wl_qcfg), VP, VP, P(wl_stage_stat), VP]

@@ -37,7 +37,6 @@ const char* last_error() { return g_err.c_str(); }
 
 const int kTableStage[kNumTables] = {ST_IBC, ST_IT, ST_HAD, ST_OBC, ST_OUT};
 unsigned g_fix_cap_override = 0;
-int g_grid_div = 1;  // wl_debug_set_grid_div: resident blocks per SM of the persistent transform kernels / this
 
 // ------------------------------------------------------------------ per-device launch helpers
 namespace {
@@ -93,7 +92,6 @@ int staged_grid_impl(const void* kern, int threads, int smem, long long work_ite
       occ[key] = per_sm;
     }
   }
-  per_sm = std::max(1, per_sm / std::max(1, g_grid_div));
   return (int)std::max(1LL, std::min<long long>(work_items, (long long)per_sm * num_sms()));
 }
 
@@ -449,11 +447,6 @@ int wl_debug_gemm_bf16(const void* A, int PA, const void* B, int PB, int batch, 
 
 int wl_debug_set_fix_cap(unsigned cap) {
   g_fix_cap_override = cap;
-  return WL_OK;
-}
-
-int wl_debug_set_grid_div(int div) {
-  g_grid_div = div < 1 ? 1 : div;
   return WL_OK;
 }
 

@@ -63,7 +63,6 @@ FastDiv make_fastdiv(unsigned d);
 
 // Test hook: cap of the deferred-fix lists (0 = automatic). Tiny caps force the inline fallback.
 extern unsigned g_fix_cap_override;
-extern int g_grid_div;
 
 int check_bits(const wl_qcfg* q);
 Bits make_bits(const wl_qcfg* q);
