@@ -129,31 +129,40 @@ __global__ void dm_cols_kernel(const float* __restrict__ dy, __nv_bfloat16* __re
   }
 }
 
-// U codes [Kp][36][Cp] -> bf16 [36][C][Kpad] (exact), zero padded.
-__global__ void ut_kernel(const int8_t* __restrict__ ucodes, __nv_bfloat16* __restrict__ ut, BwGeo g, int Kpad) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= 36LL * g.C * Kpad) return;
-  const int k = (int)(idx % Kpad);
-  const long long r = idx / Kpad;
-  const int c = (int)(r % g.C), e = (int)(r / g.C);
-  ut[idx] = __float2bfloat16_rn(k < g.K ? (float)ucodes[((size_t)k * 36 + e) * g.Cp + c] : 0.f);
-}
-
-// V codes [T][36][Cp] -> bf16 [36][C][Tpad] (exact), a 64 x 64 shared-memory transpose per block.
-__global__ void __launch_bounds__(256) vt_kernel(const int8_t* __restrict__ vcodes, __nv_bfloat16* __restrict__ vt,
-                                                 BwGeo g, int Tpad) {
-  __shared__ int8_t sm[64][65];
-  const int t0 = blockIdx.x * 64, c0 = blockIdx.y * 64, e = blockIdx.z;
-  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
-    const int tt = i >> 6, cc = i & 63;
-    const int t = t0 + tt, c = c0 + cc;
-    sm[cc][tt] = (t < g.T && c < g.C) ? vcodes[((size_t)t * 36 + e) * g.Cp + c] : (int8_t)0;
+// Codes [rows][36][Cp] int8 -> bf16 [36][C][rows_pad] (exact), rows >= `rows` zero: the GEMM operands U^T
+// (rows = K) and V^T (rows = T).  Block = 64 rows x 64 channels of one Winograd element: 32-bit loads along the
+// channels, a word-pitched shared tile, and per thread four consecutive rows of one channel leave as one 8-byte
+// store (a channel's 64 rows are one 128-byte run).  The byte-per-thread version was issue-bound (81 % issue
+// slots, 69 us on 16384 x 64 codes).
+__global__ void __launch_bounds__(256) codes_t_kernel(const int8_t* __restrict__ codes, __nv_bfloat16* __restrict__ out,
+                                                      int rows, int rows_pad, int C, int Cp) {
+  __shared__ uint32_t sm[64][17];
+  const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64, e = blockIdx.z;
+#pragma unroll
+  for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+    const int rr = i >> 4, cw = i & 15;
+    const int r = r0 + rr, c = c0 + 4 * cw;
+    uint32_t v = 0;
+    if (r < rows && c < Cp) v = __ldg(reinterpret_cast<const uint32_t*>(codes + ((size_t)r * 36 + e) * Cp + c));
+    sm[rr][cw] = v;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
-    const int cc = i >> 6, tt = i & 63;
+  const int8_t* smb = reinterpret_cast<const int8_t*>(&sm[0][0]);
+#pragma unroll
+  for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+    const int cc = i >> 4, r4 = i & 15;
     const int c = c0 + cc;
-    if (c < g.C) vt[((size_t)e * g.C + c) * Tpad + t0 + tt] = __float2bfloat16_rn((float)sm[cc][tt]);
+    if (c < C) {
+      __nv_bfloat162 lo, hi;
+      lo.x = __float2bfloat16_rn((float)smb[(4 * r4 + 0) * 68 + cc]);
+      lo.y = __float2bfloat16_rn((float)smb[(4 * r4 + 1) * 68 + cc]);
+      hi.x = __float2bfloat16_rn((float)smb[(4 * r4 + 2) * 68 + cc]);
+      hi.y = __float2bfloat16_rn((float)smb[(4 * r4 + 3) * 68 + cc]);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&lo);
+      w.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(out + ((size_t)e * C + c) * rows_pad + r0 + 4 * r4) = w;
+    }
   }
 }
 
@@ -189,40 +198,44 @@ __global__ void dxt_kernel(const float* __restrict__ dv, float* __restrict__ dxt
 }
 
 // Gather col2im: each input pixel sums the <= 2x2 tile contributions covering it (no atomics).
-// Block = (image n, input row, 32 columns, 32 channels): the sums are formed with channels across
-// lanes (coalesced dxt reads) and leave through shared memory with columns across lanes
-// (coalesced dx rows).
-__global__ void __launch_bounds__(256) dx_gather_kernel(const float* __restrict__ dxt, float* __restrict__ dx, BwGeo g) {
+// Block = (image n, 32 consecutive pixels of its H x W plane, 32 channels): the sums are formed with channels
+// across lanes (coalesced dxt reads) and leave through shared memory with pixels across lanes (128-byte runs
+// of dx whatever the image width).  A padded coordinate p lies in tile p / 4 at offset p % 4 and, when that
+// offset is 0 or 1, also in the tile before it at offset + 4; the (at most four) loads of a pixel are issued
+// before their sum, tile rows then tile columns ascending.
+__global__ void __launch_bounds__(256, 8) dx_gather_kernel(const float* __restrict__ dxt, float* __restrict__ dx,
+                                                           BwGeo g, int pblocks) {
   __shared__ float sm[32][33];
-  const int n = blockIdx.x / g.H, row = blockIdx.x % g.H;
-  const int col0 = blockIdx.y * 32, c0 = blockIdx.z * 32;
+  const int n = blockIdx.x / pblocks, p0 = (blockIdx.x % pblocks) * 32, c0 = blockIdx.z * 32;
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int rp = row + g.pad;
-  {
-    const int c = c0 + lane;
-    for (int cl = grp; cl < 32; cl += 8) {
-      const int col = col0 + cl;
-      float s = 0.f;
-      if (c < g.C && col < g.W) {
-        const int cp = col + g.pad;
-        for (int ty = max(0, (rp - 2) / 4); ty <= min(g.th - 1, rp / 4); ++ty) {
-          const int i = rp - 4 * ty;
-          if (i < 0 || i > 5) continue;
-          for (int tx = max(0, (cp - 2) / 4); tx <= min(g.tw - 1, cp / 4); ++tx) {
-            const int j = cp - 4 * tx;
-            if (j < 0 || j > 5) continue;
-            const int t = n * g.TP + ty * g.tw + tx;
-            s += __ldg(&dxt[((size_t)t * 36 + 6 * i + j) * g.C + c]);
-          }
-        }
-      }
-      sm[cl][lane] = s;
+  const int HW = g.H * g.W;
+  const int c = c0 + lane;
+  const int tstride = 36 * g.C;
+  const float* base = dxt + (size_t)n * g.TP * tstride + c;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int pl = grp + 8 * q, p = p0 + pl;
+    float s = 0.f;
+    if (c < g.C && p < HW) {
+      const int row = p / g.W, col = p - row * g.W;
+      const int rp = row + g.pad, cp = col + g.pad;
+      const int tyA = rp >> 2, iA = rp & 3, txA = cp >> 2, jA = cp & 3;
+      const bool vA = tyA < g.th, vB = iA <= 1 && tyA >= 1 && tyA - 1 < g.th;
+      const bool wA = txA < g.tw, wB = jA <= 1 && txA >= 1 && txA - 1 < g.tw;
+      const float* pa = base + ((size_t)(tyA * g.tw + txA) * tstride + (size_t)((6 * iA + jA) * g.C));  // tile (tyA, txA)
+      const int up = g.tw * tstride - 24 * g.C, left = tstride - 4 * g.C;  // one tile up: i + 4; left: j + 4
+      const float v0 = (vB && wB) ? __ldg(pa - up - left) : 0.f;
+      const float v1 = (vB && wA) ? __ldg(pa - up) : 0.f;
+      const float v2 = (vA && wB) ? __ldg(pa - left) : 0.f;
+      const float v3 = (vA && wA) ? __ldg(pa) : 0.f;
+      s = ((v0 + v1) + v2) + v3;
     }
+    sm[pl][lane] = s;
   }
   __syncthreads();
   for (int cl = grp; cl < 32; cl += 8) {
-    const int c = c0 + cl, col = col0 + lane;
-    if (c < g.C && col < g.W) dx[(((size_t)n * g.C + c) * g.H + row) * g.W + col] = sm[lane][cl];
+    const int cc = c0 + cl, p = p0 + lane;
+    if (cc < g.C && p < HW) dx[((size_t)n * g.C + cc) * HW + p] = sm[lane][cl];
   }
 }
 
@@ -233,16 +246,28 @@ __global__ void __launch_bounds__(256) dx_gather_kernel(const float* __restrict_
 // per (k, c) storing its 9 floats 36 KB apart cost 162 us on 512 x 512 channels; this version ~20 us).
 __global__ void __launch_bounds__(256) dw_kernel(const float* __restrict__ dup, float* __restrict__ dw, BwGeo g, int S) {
   __shared__ float tile[32][8 * 9 + 1];
+  __shared__ float stage[36][256];
   const int kx = threadIdx.x & 31, cy = threadIdx.x >> 5;
   const int k0 = blockIdx.x * 32, c0 = blockIdx.y * 8;
   const int k = k0 + kx, c = c0 + cy;
   if (k < g.K && c < g.C) {
+    // The 36 partials of one split go through per-thread shared slots as asynchronous copies, so all 36 loads are
+    // in flight together: written as plain loads ptxas emits load -> convert -> add a few elements at a time, i.e.
+    // ~36 * S serialised L2 latencies per thread (154 us on 512 x 512 channels, 70 us on 64 x 64 with 16 blocks).
     double D[6][6];
 #pragma unroll
-    for (int e = 0; e < 36; ++e) {
-      double s = 0.0;
-      for (int sp = 0; sp < S; ++sp) s += (double)__ldg(&dup[(((size_t)sp * 36 + e) * g.C + c) * g.K + k]);
-      D[e / 6][e % 6] = s;
+    for (int e = 0; e < 36; ++e) D[e / 6][e % 6] = 0.0;
+    const size_t estride = (size_t)g.C * g.K;
+    const float* src = dup + (size_t)c * g.K + k;
+    const uint32_t slot = (uint32_t)__cvta_generic_to_shared(&stage[0][threadIdx.x]);
+    for (int sp = 0; sp < S; ++sp, src += 36 * estride) {
+#pragma unroll
+      for (int e = 0; e < 36; ++e)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(slot + e * 256 * 4), "l"(src + e * estride) : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+      for (int e = 0; e < 36; ++e) D[e / 6][e % 6] += (double)stage[e][threadIdx.x];
     }
     double tmp[6][3];  // dU . G
 #pragma unroll
@@ -348,8 +373,9 @@ int wl_bw_run(const BwGeo& g, const float* dy, const int8_t* ucodes, const wl::A
   const long long T = g.T, C = g.C, K = g.K;
   dm_rows_kernel<<<(unsigned)((T * W.Kpad + tb - 1) / tb), tb, 0, st>>>(dy, W.dmA, g, W.Kpad);
   dm_cols_kernel<<<(unsigned)(((long long)W.Tpad * K + tb - 1) / tb), tb, 0, st>>>(dy, W.dmB, g, W.Tpad, acc);
-  ut_kernel<<<(unsigned)((36 * C * W.Kpad + tb - 1) / tb), tb, 0, st>>>(ucodes, W.ut, g, W.Kpad);
-  vt_kernel<<<dim3(W.Tpad / 64, (unsigned)((C + 63) / 64), 36), 256, 0, st>>>(vcodes, W.vt, g, W.Tpad);
+  const unsigned cblk = (unsigned)((C + 63) / 64);
+  codes_t_kernel<<<dim3(W.Kpad / 64, cblk, 36), 256, 0, st>>>(ucodes, W.ut, g.K, W.Kpad, g.C, g.Cp);
+  codes_t_kernel<<<dim3(W.Tpad / 64, cblk, 36), 256, 0, st>>>(vcodes, W.vt, g.T, W.Tpad, g.C, g.Cp);
   // dV[e] (T x C) = dM[e] (T x K) . U[e]^T      (s_u applied in dxt_kernel)
   cudaError_t e1 = gemm_bf16_split(W.dmA, 3, W.ut, 1, 36, g.T, g.C, W.Kpad, W.Kpad, W.dv, g.C, 1.f, st);
   // dU^T[e] (C x K) = V[e]^T (C x T) . (s_v dM)[e] (T x K), split over the tiles
@@ -359,7 +385,8 @@ int wl_bw_run(const BwGeo& g, const float* dy, const int8_t* ucodes, const wl::A
     return WL_ERR_CUDA;
   }
   dxt_kernel<<<(unsigned)((T * C + tb - 1) / tb), tb, 0, st>>>(W.dv, W.dxt, g, wacc, wstage, qmax_u);
-  dx_gather_kernel<<<dim3((unsigned)(g.N * g.H), (g.W + 31) / 32, (unsigned)((C + 31) / 32)), 256, 0, st>>>(W.dxt, dx, g);
+  const int pblocks = (g.H * g.W + 31) / 32;
+  dx_gather_kernel<<<dim3((unsigned)(g.N * pblocks), 1, (unsigned)((C + 31) / 32)), 256, 0, st>>>(W.dxt, dx, g, pblocks);
   dw_kernel<<<dim3((unsigned)((K + 31) / 32), (unsigned)((C + 7) / 8)), 256, 0, st>>>(W.dup, dw, g, W.S);
   if (db) db_kernel<<<(unsigned)K, 256, 0, st>>>(dy, db, g);
   cudaError_t e = cudaGetLastError();

@@ -48,6 +48,14 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, GemmSplitArgs a
   a.stages = (kMaxSmem - 1024 - 256) / stage;
   if (a.stages > 4) a.stages = 4;
   if (a.stages < 1) return cudaErrorInvalidValue;
+  // A split of kb K-blocks never uses more than kb ring stages, and when two CTAs per SM still get
+  // min(kb, 2) stages each, the smaller ring wins: one CTA's TMA latency and epilogue run under the other's
+  // MMAs (the config-3 backward GEMMs are one to a few K-blocks deep: a 4-stage 220 KB ring left one
+  // CTA per SM running load -> MMA -> epilogue back to back, 139 us for 377 MB on 64 channels x 32 x 32).
+  const int kb = (a.ks < a.Kd ? a.ks : a.Kd) / 64;
+  if (a.stages > kb) a.stages = kb < 1 ? 1 : kb;
+  const int half = (kMaxSmem / 2 - 1024 - 256) / stage;
+  if (half >= (kb < 2 ? kb : 2) && half >= 1 && a.stages > half) a.stages = half;
   const int smem = 1024 + a.stages * stage + 256;
   auto kern = gemm_bf16_split_kernel<BN>;
   cudaError_t e = set_attr_once(reinterpret_cast<const void*>(kern), smem);
