@@ -506,46 +506,78 @@ __global__ void __launch_bounds__(256, WL_MINB) in_c_kernel(const int8_t* __rest
   if (want && !defer_fix(fl, FIX_IT, idx, want)) fix_it_unit<MODE>(c0, c1, dst, LD, g, b, acc, pf, t, c, LD);
 }
 
+// Argmax replay of a warp whose 32 lanes hold units of ONE scale group (lane = channel of one tile row; every
+// lane calls, inactive lanes with m = 0).  Only the lanes holding the warp's maximum replay, and only while
+// that maximum can still be the group's (the stored maximum only grows, so a lane equal to the final maximum
+// always passes); each lane walks its own set `em` of argmax elements, so a warp's replay calls run together
+// instead of one after the other per distinct element (the fp64 replays were 3/4 of the instructions of the
+// finalize-exec kernels: 32 lanes with 32 different argmax elements).  fp64 magnitudes order like the
+// integers (gap >= 1/M relative, fp64 noise < 1e-13), so the atomicMax over replayed values is the
+// reference's max_abs whichever other lanes also replay.
+template <class R>
+__device__ __forceinline__ void warp_argmax_replay(long long m, unsigned long long em, Acc* a, R&& replay) {
+  long long wmax = m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long other = __shfl_xor_sync(0xffffffffu, wmax, o);
+    wmax = other > wmax ? other : wmax;
+  }
+  if (wmax <= 0 || m != wmax) return;
+  if (m < (long long)(*(volatile const unsigned long long*)&a->M)) return;
+  double f = 0.0;
+  while (em) {
+    const int e = __ffsll((long long)em) - 1;
+    em &= em - 1;
+    f = fmax(f, fabs(replay(e)));
+  }
+  atomicMax(&a->M, (unsigned long long)m);
+  atomicMax(&a->F, dbits(f));
+}
+
 // Exact recomputation of one input-side unit: local exact max and fp64 max_abs of its argmax.
 template <int MODE, int STAGE>
 __device__ void exact_input_unit(const int8_t* __restrict__ c0, const int8_t* __restrict__ c1, const Geo& g,
-                                 const Bits& b, Acc* acc, const PlanF64* pf, int t, int c) {
+                                 const Bits& b, Acc* acc, const PlanF64* pf, int t, int c, bool active) {
+  // called by all 32 lanes of a warp with the same tile t (lane = channel, `active` = channel in range)
   const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
   const int grp = (int)g.fipg.div((unsigned)n);
   Acc* ga = acc + (size_t)grp * ST_COUNT;
-  int Xi[6][6];
-  long long T[6][6];
-  StageQ qin;
-  const double* Lf;
-  if (MODE == 1 && STAGE == ST_IT) {
-    load_planes(c1, (uint32_t)g.Cp, (uint32_t)t * 36u * g.Cp + c, Xi);
-    sandwich<tab::Leg_IT>(Xi, T);
-    qin = load_int_stage(ga[ST_IBC], b.q[ST_IBC]);
-    Lf = pf->it;
-  } else {
-    load_c0(c0, g, n, tile, c, Xi);
-    int Ti[6][6];
-    if (MODE == 0)
-      sandwich<tab::Can_IT>(Xi, Ti);
-    else
-      sandwich<tab::Leg_IBC>(Xi, Ti);
-#pragma unroll
-    for (int e = 0; e < 36; ++e) T[e / 6][e % 6] = Ti[e / 6][e % 6];
-    qin = load_float_stage(ga[ST_INPUT], b.q[ST_INPUT]);
-    Lf = MODE == 0 ? pf->it : pf->ibc;
-  }
-  const long long m = absmax36(T);
-  if (m == 0) return;
   int xc[36];
-  for (int e = 0; e < 36; ++e) xc[e] = Xi[e / 6][e % 6];
-  double f = 0.0;
-  for (int e = 0; e < 36; ++e) {
-    const long long v = T[e / 6][e % 6];
-    if ((v < 0 ? -v : v) == m)
-      f = fmax(f, fabs(replay_sandwich(Lf, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6)));
+  long long m = 0;
+  unsigned long long em = 0;
+  StageQ qin;
+  const double* Lf = nullptr;
+  if (active) {
+    int Xi[6][6];
+    long long T[6][6];
+    if (MODE == 1 && STAGE == ST_IT) {
+      load_planes(c1, (uint32_t)g.Cp, (uint32_t)t * 36u * g.Cp + c, Xi);
+      sandwich<tab::Leg_IT>(Xi, T);
+      qin = load_int_stage(ga[ST_IBC], b.q[ST_IBC]);
+      Lf = pf->it;
+    } else {
+      load_c0(c0, g, n, tile, c, Xi);
+      int Ti[6][6];
+      if (MODE == 0)
+        sandwich<tab::Can_IT>(Xi, Ti);
+      else
+        sandwich<tab::Leg_IBC>(Xi, Ti);
+#pragma unroll
+      for (int e = 0; e < 36; ++e) T[e / 6][e % 6] = Ti[e / 6][e % 6];
+      qin = load_float_stage(ga[ST_INPUT], b.q[ST_INPUT]);
+      Lf = MODE == 0 ? pf->it : pf->ibc;
+    }
+    m = absmax36(T);
+#pragma unroll
+    for (int e = 0; e < 36; ++e) {
+      xc[e] = Xi[e / 6][e % 6];
+      const long long v = T[e / 6][e % 6];
+      if ((v < 0 ? -v : v) == m) em |= 1ull << e;
+    }
   }
-  atomicMax(&ga[STAGE].M, (unsigned long long)m);
-  atomicMax(&ga[STAGE].F, dbits(f));
+  warp_argmax_replay(m, em, ga + STAGE, [&](int e) {
+    return replay_sandwich(Lf, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6);
+  });
 }
 
 // Finalize candidate lists: count slot kCandSlot0 + stage of the FixList counters (the fix lists use
@@ -597,7 +629,7 @@ __global__ void finalize_input_kernel(const int8_t* __restrict__ c0, const int8_
         const int l = __ffs(mask) - 1;
         mask &= mask - 1;
         const int tl = (int)t0 + l, ch = cb * 32 + lane;
-        if (ch < g.C) exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, tl, ch);
+        exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, tl, ch, ch < g.C);
       }
     }
   }
@@ -616,7 +648,7 @@ __global__ void __launch_bounds__(256) finalize_input_exec(const int8_t* __restr
   for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += nw) {
     const unsigned e = fl.items[i], t = e / NB, cb = e - t * NB;
     const int ch = (int)cb * 32 + lane;
-    if (ch < g.C) exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, (int)t, ch);
+    exact_input_unit<MODE, STAGE>(c0, c1, g, b, acc, pf, (int)t, ch, ch < g.C);
   }
   stage_params_tail(acc, STAGE, tail);
 }
@@ -795,61 +827,67 @@ __device__ __forceinline__ void exact_c4_from_h(const HT* __restrict__ h, uint32
 
 template <int MODE, int STAGE, typename HT, bool FROM_H = false>
 __device__ void exact_output_unit(const HT* __restrict__ h, const int8_t* __restrict__ c4, const Geo& g, const Bits& b,
-                                  Acc* acc, const PlanF64* pf, int t, int k) {
+                                  Acc* acc, const PlanF64* pf, int t, int k, bool active) {
+  // called by all 32 lanes of a warp with the same tile t (lane = output channel, `active` = channel in range)
   const int n = (int)g.fTP.div((unsigned)t), tile = (int)g.fTP.mod((unsigned)t);
   const int ty = (int)g.ftw.div((unsigned)tile), tx = (int)g.ftw.mod((unsigned)tile);
   const int grp = (int)g.fipg.div((unsigned)n);
   Acc* ga = acc + (size_t)grp * ST_COUNT;
-  int Xi[6][6];
+  int xc[36];
+  long long m = 0;
+  unsigned long long em = 0;
+  StageQ qin;
   if (MODE == 1 && STAGE == ST_OBC) {
-    load_planes(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
-    int T[6][6];
-    sandwich<tab::Leg_OBC>(Xi, T);
-    const long long m = absmax36(T);
-    if (m == 0) return;
-    const StageQ qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
-    int xc[36];
-    for (int e = 0; e < 36; ++e) xc[e] = Xi[e / 6][e % 6];
-    double f = 0.0;
-    for (int e = 0; e < 36; ++e) {
-      const long long v = T[e / 6][e % 6];
-      if ((v < 0 ? -v : v) == m)
-        f = fmax(f, fabs(replay_sandwich(pf->obc, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6)));
+    if (active) {
+      int Xi[6][6];
+      load_planes(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
+      int T[6][6];
+      sandwich<tab::Leg_OBC>(Xi, T);
+      m = absmax36(T);
+      qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
+#pragma unroll
+      for (int e = 0; e < 36; ++e) {
+        xc[e] = Xi[e / 6][e % 6];
+        const long long v = T[e / 6][e % 6];
+        if ((v < 0 ? -v : v) == m) em |= 1ull << e;
+      }
     }
-    atomicMax(&ga[ST_OBC].M, (unsigned long long)m);
-    atomicMax(&ga[ST_OBC].F, dbits(f));
+    warp_argmax_replay(m, em, ga + ST_OBC, [&](int e) {
+      return replay_sandwich(pf->obc, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6);
+    });
     return;
   }
-  long long Y[4][4];
-  StageQ qin;
-  if (MODE == 0) {
-    load_planes(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
-    int Y32[4][4];
-    sandwich<tab::Can_OT>(Xi, Y32);
-    for (int e = 0; e < 16; ++e) Y[e / 4][e % 4] = Y32[e / 4][e % 4];
-    qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
-  } else {
-    if constexpr (FROM_H)
-      exact_c4_from_h<HT>(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + (uint32_t)k, ga, b, pf, Xi);
-    else
-      load_planes(c4, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
-    sandwich<tab::Leg_OT>(Xi, Y);
-    qin = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
+  if (active) {
+    int Xi[6][6];
+    long long Y[4][4];
+    if (MODE == 0) {
+      load_planes(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
+      int Y32[4][4];
+      sandwich<tab::Can_OT>(Xi, Y32);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) Y[e / 4][e % 4] = Y32[e / 4][e % 4];
+      qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
+    } else {
+      if constexpr (FROM_H)
+        exact_c4_from_h<HT>(h, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + (uint32_t)k, ga, b, pf, Xi);
+      else
+        load_planes(c4, (uint32_t)g.Kp, (uint32_t)t * 36u * g.Kp + k, Xi);
+      sandwich<tab::Leg_OT>(Xi, Y);
+      qin = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
+    }
+    m = absmax_crop(Y, ty, tx, g);
+#pragma unroll
+    for (int e = 0; e < 36; ++e) xc[e] = Xi[e / 6][e % 6];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int i = e / 4, j = e % 4;
+      const long long v = Y[i][j];
+      if (4 * ty + i < g.Ho && 4 * tx + j < g.Wo && (v < 0 ? -v : v) == m) em |= 1ull << e;
+    }
   }
-  const long long m = absmax_crop(Y, ty, tx, g);
-  if (m == 0) return;
-  int xc[36];
-  for (int e = 0; e < 36; ++e) xc[e] = Xi[e / 6][e % 6];
-  double f = 0.0;
-  for (int e = 0; e < 16; ++e) {
-    const int i = e / 4, j = e % 4;
-    if (4 * ty + i >= g.Ho || 4 * tx + j >= g.Wo) continue;
-    const long long v = Y[i][j];
-    if ((v < 0 ? -v : v) == m)
-      f = fmax(f, fabs(replay_sandwich(pf->ot, 4, 6, xc, qin.qmax, qin.maxabs, qin.scale, i, j)));
-  }
-  atomicMax(&ga[ST_OUT].M, (unsigned long long)m);
-  atomicMax(&ga[ST_OUT].F, dbits(f));
+  warp_argmax_replay(m, em, ga + ST_OUT, [&](int e) {
+    return replay_sandwich(pf->ot, 4, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 4, e % 4);
+  });
 }
 
 template <int MODE, int STAGE, typename HT, bool FROM_H = false>
@@ -883,7 +921,7 @@ __global__ void finalize_output_kernel(const HT* __restrict__ h, const int8_t* _
         const int l = __ffs(mask) - 1;
         mask &= mask - 1;
         const int tl = (int)t0 + l, ch = cb * 32 + lane;
-        if (ch < g.K) exact_output_unit<MODE, STAGE, HT, FROM_H>(h, c4, g, b, acc, pf, tl, ch);
+        exact_output_unit<MODE, STAGE, HT, FROM_H>(h, c4, g, b, acc, pf, tl, ch, ch < g.K);
       }
     }
   }
@@ -901,7 +939,7 @@ __global__ void __launch_bounds__(256) finalize_output_exec(const HT* __restrict
   for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += nw) {
     const unsigned e = fl.items[i], t = e / NB, cb = e - t * NB;
     const int ch = (int)cb * 32 + lane;
-    if (ch < g.K) exact_output_unit<MODE, STAGE, HT, FROM_H>(h, c4, g, b, acc, pf, (int)t, ch);
+    exact_output_unit<MODE, STAGE, HT, FROM_H>(h, c4, g, b, acc, pf, (int)t, ch, ch < g.K);
   }
   stage_params_tail(acc, STAGE, tail);
 }
