@@ -141,16 +141,35 @@ struct SrcPlanes {  // [T][36][LD] codes
   __device__ void load(XT (&X)[6][6]) const { load_planes(p, plane, off, X); }
 };
 
+// Stage matrix entry with run-time indices: a __constant__ copy of L (the constexpr L::e() folds only
+// compile-time indices).
+template <class L>
+struct LTab {
+  int v[6][6];
+  constexpr LTab() : v{} {
+    for (int i = 0; i < L::R; ++i)
+      for (int j = 0; j < L::C; ++j) v[i][j] = L::e(i, j);
+  }
+};
+template <class L>
+__constant__ LTab<L> kLTab{};
+template <class L>
+__device__ __forceinline__ int ltab(int i, int j) {
+  return kLTab<L>.v[i][j];
+}
+
 // Exact code of element (i, j) of stage L . X . L^T from the unit's input codes xc (row-major 6x6,
 // loaded once by fix_unit); ties replayed in fp64.
 template <class L>
 __device__ __noinline__ int exact_elem(const int* xc, int i, int j, const Acc* a_stage, int qmax, const Acc* a_in,
                                        int qmax_in, bool in_float, const double* __restrict__ Lf) {
   long long T = 0;
+#pragma unroll
   for (int l = 0; l < L::C; ++l) {
     int tmp = 0;  // first half |.| <= qmax_in * rowsum(L) < 2^31
-    for (int l2 = 0; l2 < L::C; ++l2) tmp += xc[l * 6 + l2] * L::e(j, l2);
-    T += (long long)L::e(i, l) * tmp;
+#pragma unroll
+    for (int l2 = 0; l2 < L::C; ++l2) tmp += xc[l * 6 + l2] * ltab<L>(j, l2);
+    T += (long long)ltab<L>(i, l) * tmp;
   }
   const StageQ q = load_int_stage(*a_stage, qmax);
   bool tie = false;
@@ -195,24 +214,17 @@ __device__ __noinline__ void fix_unit(Src src, float r, float thr, float ef, con
     }
   });
   if (!mask) return;
-  long long T[L::R][L::R];
-  sandwich<L>(Xi, T);
-  const StageQ q = load_int_stage(*a_stage, qmax);
+  // Each lane walks its own flagged elements (typically one or two of the 36) and evaluates only those exactly
+  // (exact_elem: 42 integer MACs per element); the lanes of a warp iterate together.  The earlier form computed
+  // the whole int64 sandwich and then ran one predicated block per element any lane had flagged.
+  int xc[36];
 #pragma unroll
-  for (int e = 0; e < L::R * L::R; ++e) {
-    const int i = e / L::R, j = e % L::R;
-    if ((mask >> (i * 6 + j)) & 1ull) {
-      bool tie = false;
-      int code = rq(T[i][j], q, tie);
-      if (tie) {
-        int xc[36];
-#pragma unroll
-        for (int u = 0; u < 36; ++u) xc[u] = Xi[u / 6][u % 6];
-        const StageQ qin = in_float ? load_float_stage(*a_in, qmax_in) : load_int_stage(*a_in, qmax_in);
-        code = code_of(replay_sandwich(Lf, L::R, L::C, xc, qin.qmax, qin.maxabs, qin.scale, i, j), q);
-      }
-      out(i, j, code);
-    }
+  for (int u = 0; u < 36; ++u) xc[u] = Xi[u / 6][u % 6];
+  while (mask) {
+    const int bit = __ffsll((long long)mask) - 1;
+    mask &= mask - 1;
+    const int i = bit / 6, j = bit - 6 * i;
+    out(i, j, exact_elem<L>(xc, i, j, a_stage, qmax, a_in, qmax_in, in_float, Lf));
   }
 }
 
