@@ -84,7 +84,9 @@ static int input_cast(FwdCtx& c, const XT* x) {
 #endif
   // band of rh rows per block: per channel one contiguous rh * W float run (at most 256 float4 slots and
   // ~60 KB of staging per block)
-  int rh = WL_QI_RH;
+  // narrow images take taller bands (a block's fixed cost is spread over more bytes: configs 1-3 forward
+  // -1..3 % with 4- or 8-row bands; at W = 56 two rows measured best)
+  int rh = g.W <= 32 ? 8 : WL_QI_RH;
   while (rh > 1 && (rh * g.W * (g.Cp + 4) > 60 * 1024 || rh * g.W / 4 > 256)) rh >>= 1;
   rh = std::min(rh, g.H);
   const int smem = rh * g.W * (g.Cp + 4);

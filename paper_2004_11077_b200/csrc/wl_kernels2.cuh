@@ -822,18 +822,28 @@ __device__ __forceinline__ void exact_c4_from_h(const HT* __restrict__ h, uint32
   long long T3[6][6];
   sandwich<tab::Leg_OBC>(Xi, T3);
   const StageQ q = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
+  unsigned long long ties = 0;
 #pragma unroll
   for (int e = 0; e < 36; ++e) {
     bool tie = false;
-    int code = rq(T3[e / 6][e % 6], q, tie);
-    if (tie) {
-      int xc[36];
+    c4[e / 6][e % 6] = rq(T3[e / 6][e % 6], q, tie);
+    if (tie) ties |= 1ull << e;
+  }
+  if (ties) {
+    // exact ties, replayed in fp64: each lane walks its own tie set (one out-of-line replay site instead of 36
+    // unrolled ones), the code lands in its register through a predicated select
+    int xc[36];
 #pragma unroll
-      for (int u = 0; u < 36; ++u) xc[u] = Xi[u / 6][u % 6];
-      const StageQ qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
-      code = code_of(replay_sandwich(pf->obc, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6), q);
+    for (int u = 0; u < 36; ++u) xc[u] = Xi[u / 6][u % 6];
+    const StageQ qin = load_int_stage(ga[ST_HAD], b.q[ST_HAD]);
+    while (ties) {
+      const int e = __ffsll((long long)ties) - 1;
+      ties &= ties - 1;
+      const int code = code_of(replay_sandwich(pf->obc, 6, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 6, e % 6), q);
+#pragma unroll
+      for (int u = 0; u < 36; ++u)
+        if (u == e) c4[u / 6][u % 6] = code;
     }
-    c4[e / 6][e % 6] = code;
   }
 }
 

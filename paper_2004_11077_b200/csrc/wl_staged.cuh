@@ -450,19 +450,30 @@ __device__ __noinline__ void exact_out_from_h(const HT* __restrict__ h, const Ge
   long long Y[4][4];
   sandwich<tab::Leg_OT>(c4, Y);
   const StageQ q = load_int_stage(ga[ST_OUT], b.q[ST_OUT]);
+  int codes[16];
+  unsigned ties = 0;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     bool tie = false;
-    int code = rq(Y[e / 4][e % 4], q, tie);
-    if (tie) {
-      int xc[36];
-#pragma unroll
-      for (int u = 0; u < 36; ++u) xc[u] = c4[u / 6][u % 6];
-      const StageQ qin = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
-      code = code_of(replay_sandwich(pf->ot, 4, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 4, e % 4), q);
-    }
-    put(e / 4, e % 4, code);
+    codes[e] = rq(Y[e / 4][e % 4], q, tie);
+    if (tie) ties |= 1u << e;
   }
+  if (ties) {  // exact ties replayed in fp64 from c4, each lane walking its own tie set
+    int xc[36];
+#pragma unroll
+    for (int u = 0; u < 36; ++u) xc[u] = c4[u / 6][u % 6];
+    const StageQ qin = load_int_stage(ga[ST_OBC], b.q[ST_OBC]);
+    while (ties) {
+      const int e = __ffs((int)ties) - 1;
+      ties &= ties - 1;
+      const int code = code_of(replay_sandwich(pf->ot, 4, 6, xc, qin.qmax, qin.maxabs, qin.scale, e / 4, e % 4), q);
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (u == e) codes[u] = code;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 16; ++e) put(e / 4, e % 4, codes[e]);
 }
 
 // Exact output values (dequantised + bias) of one unit into o[4 * i + j] (shared staging); tabg is the
