@@ -976,6 +976,7 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
   // Flat, fully parallel scan: thread per (xi, t) table row (nchunk <= 4 entries, one 16-byte load
   // when nchunk == 4); consecutive threads read consecutive rows.  An entry equal to its group's exact
   // max is recomputed by the whole warp (rare): lanes over the entry's output columns.
+  __shared__ double prod[8][512];  // per-warp products of one replayed column (C <= 512)
   const int nchunk = g.Kp / bn;
   const int lane = threadIdx.x & 31;
   // 36 * T < 2^27 (make_layout rejects larger calls): 32-bit row arithmetic, no 64-bit divisions
@@ -1029,24 +1030,49 @@ __global__ void __launch_bounds__(256) finalize_hadamard_kernel(const int8_t* __
         const long long Ml = (long long)ga[ST_HAD].M;
         const int8_t* vrow = V + ((size_t)tl * 36 + xl) * g.Cp;
         double f = 0.0;
-        for (int k = chunk * bn + lane; k < min(chunk * bn + bn, g.K); k += 32) {
-          const int8_t* urow = U + ((size_t)k * 36 + xl) * g.Cp;
-          // exact integer dot over the zero-padded Cp channels: 16-byte loads, 4-way byte dot products
-          // (|sum| <= 127 * 255 * 512 < 2^31; channels >= C are zero in U and V)
-          const int4* u4 = reinterpret_cast<const int4*>(urow);
-          const int4* v4 = reinterpret_cast<const int4*>(vrow);
-          int s0 = 0, s1 = 0;
-          for (int c = 0; c < g.Cp / 16; ++c) {
-            const int4 a = __ldg(u4 + c), bb = __ldg(v4 + c);
-            s0 = __dp4a(a.x, bb.x, s0);
-            s1 = __dp4a(a.y, bb.y, s1);
-            s0 = __dp4a(a.z, bb.z, s0);
-            s1 = __dp4a(a.w, bb.w, s1);
+        const int kend = min(chunk * bn + bn, g.K);
+        for (int kb = chunk * bn; kb < kend; kb += 32) {
+          const int k = kb + lane;
+          long long sdot = 0;
+          if (k < kend) {
+            const int8_t* urow = U + ((size_t)k * 36 + xl) * g.Cp;
+            // exact integer dot over the zero-padded Cp channels: 16-byte loads, 4-way byte dot products
+            // (|sum| <= 127 * 255 * 512 < 2^31; channels >= C are zero in U and V)
+            const int4* u4 = reinterpret_cast<const int4*>(urow);
+            const int4* v4 = reinterpret_cast<const int4*>(vrow);
+            int s0 = 0, s1 = 0;
+            for (int c = 0; c < g.Cp / 16; ++c) {
+              const int4 a = __ldg(u4 + c), bb = __ldg(v4 + c);
+              s0 = __dp4a(a.x, bb.x, s0);
+              s1 = __dp4a(a.y, bb.y, s1);
+              s0 = __dp4a(a.z, bb.z, s0);
+              s1 = __dp4a(a.w, bb.w, s1);
+            }
+            sdot = (long long)s0 + s1;
           }
-          const long long sdot = (long long)s0 + s1;
-          if ((sdot < 0 ? -sdot : sdot) == Ml)
-            f = fmax(f, fabs(replay_hadamard<false>(urow, vrow, g.C, load_int_stage(wacc[wstage], qmax_u),
-                                             load_int_stage(ga[ST_IT], qmax_v))));
+          // fp64 replay of an argmax column by the whole warp: the 32 lanes form the products
+          // deq(u_c) * deq(v_c), one lane adds them c ascending from 0.0 (_kernels.py:99-104) — the same
+          // roundings as replay_hadamard, with C dependent adds on the critical path instead of C times
+          // (two byte loads, two dequantisations, a multiply and an add) on a single lane
+          unsigned hit = __ballot_sync(0xffffffffu, k < kend && (sdot < 0 ? -sdot : sdot) == Ml);
+          if (hit) {
+            const StageQ qu = load_int_stage(wacc[wstage], qmax_u), qv = load_int_stage(ga[ST_IT], qmax_v);
+            double* pw = prod[threadIdx.x >> 5];
+            while (hit) {
+              const int src = __ffs(hit) - 1;
+              hit &= hit - 1;
+              const int8_t* us = U + ((size_t)(kb + src) * 36 + xl) * g.Cp;
+              for (int c = lane; c < g.C; c += 32)
+                pw[c] = __dmul_rn(deq(us[c], qu.qmax, qu.maxabs, qu.scale), deq(vrow[c], qv.qmax, qv.maxabs, qv.scale));
+              __syncwarp();
+              if (lane == 0) {
+                double a = 0.0;
+                for (int c = 0; c < g.C; ++c) a = __dadd_rn(a, pw[c]);
+                f = fmax(f, fabs(a));
+              }
+              __syncwarp();
+            }
+          }
         }
         if (f > 0.0) atomicMax(&ga[ST_HAD].F, dbits(f));
       }
