@@ -82,12 +82,12 @@ SLOT_KERNELS = {
     "output_max": ("sout_bt2_kernel", "fixup_obct_kernel", "finalize_output_kernel<1, 8", "finalize_output_exec<1, 8"),
     "output_write": ("out_table_kernel", "sout_cw_kernel", "fixup_outt_kernel"),
 }
-NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_cfg4_v7.csv")
+NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_cfg4_v8.csv")
 
 
 def ncu_traffic(slot):
     """DRAM bytes (read + write) per launch of a profile slot from the committed `ncu --set full` capture
-    of one config-4 forward (profiles/r02_ncu_full_cfg4_v7.csv, tools/ncu_full_cfg4.sh), or None."""
+    of one config-4 forward (profiles/r02_ncu_full_cfg4_v8.csv, tools/ncu_full_cfg4.sh), or None."""
     try:
         with open(NCU_FULL) as fh:
             rows = list(csv.reader(fh))
@@ -499,13 +499,13 @@ def run_ours(args, rank, world, local_rank):
         roof = {"kernel": dom, "bound": "hbm", "achieved": kb / (dom_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(dom)
-    roof["traffic_source"] = "profiles/r02_ncu_full_cfg4_v7.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
+    roof["traffic_source"] = "profiles/r02_ncu_full_cfg4_v8.csv (ncu --set full, dram__bytes_read+write of the slot's kernels)"
     roof["algorithmic_bytes_per_launch"] = kb
     roof["ms_per_launch"] = dom_ms
     roof["timed_in"] = "single-stream pass of the same K steps with the library's CUDA-event marks, right after the timed region"
     roof["peak_source"] = peak_kind if roof["bound"] == "hbm" else ("torch._int_mm 8192^3 measured live" if i8_peak else "2x bf16 planning")
     # every slot against the same two ceilings; `limiter` is what ncu shows bounds the slot's main kernel
-    # (profiles/r02_ncu_full_cfg4_v7.csv): the five transform passes are CUDA-core FMA/ALU-pipe bound, so their
+    # (profiles/r02_ncu_full_cfg4_v8.csv): the five transform passes are CUDA-core FMA/ALU-pipe bound, so their
     # HBM fraction is low by construction
     limiter = {"cast_input": "hbm (x read once; the second read of a band hits L2)", "absmax_input": "hbm",
                "quant_input": "issue + hbm", "input_base_change_max": "fma/alu pipes",
