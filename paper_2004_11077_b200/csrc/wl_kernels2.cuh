@@ -192,10 +192,9 @@ __device__ __forceinline__ int rq_nb(float T, float r, float band, float& k, flo
 }
 
 // Rare path for a unit whose fast path came within the band of a half-integer: redo the fp32
-// sandwich (deterministic, same values) to find the flagged elements (per-row band), then compute
-// the unit's exact integer stage values once (int32 first half, int64 second, compile-time
-// indices: no local-memory tables) and hand every flagged element's exact code to out(i, j, code),
-// which overwrites what the fast path stored; exact ties are replayed in fp64.
+// sandwich (deterministic, same values) to find the flagged elements (per-row band), then hand the
+// exact code of every flagged element (exact_elem: integer evaluation of that one element, exact
+// ties replayed in fp64) to out(i, j, code), which overwrites what the fast path stored.
 template <class L, class Src, class Out>
 __device__ __noinline__ void fix_unit(Src src, float r, float thr, float ef, const Acc* a_stage, int qmax,
                                       const Acc* a_in, int qmax_in, bool in_float, const double* __restrict__ Lf,
