@@ -213,19 +213,22 @@ __global__ void dxt_kernel(const float* __restrict__ dv, float* __restrict__ dxt
 // of dx whatever the image width).  A padded coordinate p lies in tile p / 4 at offset p % 4 and, when that
 // offset is 0 or 1, also in the tile before it at offset + 4; the (at most four) loads of a pixel are issued
 // before their sum, tile rows then tile columns ascending.
-__global__ void __launch_bounds__(256, 8) dx_gather_kernel(const float* __restrict__ dxt, float* __restrict__ dx,
-                                                           BwGeo g, int pblocks) {
-  __shared__ float sm[32][33];
-  const int n = blockIdx.x / pblocks, p0 = (blockIdx.x % pblocks) * 32, c0 = blockIdx.z * 32;
+template <int PQ>  // a block covers 8 * PQ consecutive pixels (PQ per thread) x 32 channels
+__global__ void __launch_bounds__(256) dx_gather_kernel(const float* __restrict__ dxt, float* __restrict__ dx,
+                                                        BwGeo g, int pblocks) {
+  __shared__ float sm[8 * PQ][33];
+  const int n = blockIdx.x / pblocks, p0 = (blockIdx.x % pblocks) * (8 * PQ), c0 = blockIdx.z * 32;
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int HW = g.H * g.W;
   const int c = c0 + lane;
   const int tstride = 36 * g.C;
   const float* base = dxt + (size_t)n * g.TP * tstride + c;
+  const int up = g.tw * tstride - 24 * g.C, left = tstride - 4 * g.C;  // one tile up: i + 4; left: j + 4
+  float v[PQ][4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int pl = grp + 8 * q, p = p0 + pl;
-    float s = 0.f;
+  for (int q = 0; q < PQ; ++q) {
+    const int p = p0 + grp + 8 * q;
+    v[q][0] = v[q][1] = v[q][2] = v[q][3] = 0.f;
     if (c < g.C && p < HW) {
       const int row = p / g.W, col = p - row * g.W;
       const int rp = row + g.pad, cp = col + g.pad;
@@ -233,19 +236,24 @@ __global__ void __launch_bounds__(256, 8) dx_gather_kernel(const float* __restri
       const bool vA = tyA < g.th, vB = iA <= 1 && tyA >= 1 && tyA - 1 < g.th;
       const bool wA = txA < g.tw, wB = jA <= 1 && txA >= 1 && txA - 1 < g.tw;
       const float* pa = base + ((size_t)(tyA * g.tw + txA) * tstride + (size_t)((6 * iA + jA) * g.C));  // tile (tyA, txA)
-      const int up = g.tw * tstride - 24 * g.C, left = tstride - 4 * g.C;  // one tile up: i + 4; left: j + 4
-      const float v0 = (vB && wB) ? __ldg(pa - up - left) : 0.f;
-      const float v1 = (vB && wA) ? __ldg(pa - up) : 0.f;
-      const float v2 = (vA && wB) ? __ldg(pa - left) : 0.f;
-      const float v3 = (vA && wA) ? __ldg(pa) : 0.f;
-      s = ((v0 + v1) + v2) + v3;
+      if (vB && wB) v[q][0] = __ldg(pa - up - left);
+      if (vB && wA) v[q][1] = __ldg(pa - up);
+      if (vA && wB) v[q][2] = __ldg(pa - left);
+      if (vA && wA) v[q][3] = __ldg(pa);
     }
-    sm[pl][lane] = s;
   }
+#pragma unroll
+  for (int q = 0; q < PQ; ++q) sm[grp + 8 * q][lane] = ((v[q][0] + v[q][1]) + v[q][2]) + v[q][3];
   __syncthreads();
   for (int cl = grp; cl < 32; cl += 8) {
-    const int cc = c0 + cl, p = p0 + lane;
-    if (cc < g.C && p < HW) dx[((size_t)n * g.C + cc) * HW + p] = sm[lane][cl];
+    const int cc = c0 + cl;
+    if (cc < g.C) {
+#pragma unroll
+      for (int hh = 0; hh < PQ / 4; ++hh) {
+        const int p = p0 + 32 * hh + lane;
+        if (p < HW) dx[((size_t)n * g.C + cc) * HW + p] = sm[32 * hh + lane][cl];
+      }
+    }
   }
 }
 
@@ -395,8 +403,13 @@ int wl_bw_run(const BwGeo& g, const float* dy, const int8_t* ucodes, const wl::A
     return WL_ERR_CUDA;
   }
   dxt_kernel<<<(unsigned)((T * C + tb - 1) / tb), tb, 0, st>>>(W.dv, W.dxt, g, wacc, wstage, qmax_u);
-  const int pblocks = (g.H * g.W + 31) / 32;
-  dx_gather_kernel<<<dim3((unsigned)(g.N * pblocks), 1, (unsigned)((C + 31) / 32)), 256, 0, st>>>(W.dxt, dx, g, pblocks);
+  if (g.H * g.W >= 256) {  // 64 pixels per block (8 per thread: 32 loads in flight)
+    const int pblocks = (g.H * g.W + 63) / 64;
+    dx_gather_kernel<8><<<dim3((unsigned)(g.N * pblocks), 1, (unsigned)((C + 31) / 32)), 256, 0, st>>>(W.dxt, dx, g, pblocks);
+  } else {
+    const int pblocks = (g.H * g.W + 31) / 32;
+    dx_gather_kernel<4><<<dim3((unsigned)(g.N * pblocks), 1, (unsigned)((C + 31) / 32)), 256, 0, st>>>(W.dxt, dx, g, pblocks);
+  }
   dw_kernel<<<dim3((unsigned)((K + 31) / 32), (unsigned)((C + 7) / 8)), 256, 0, st>>>(W.dup, dw, g, W.S);
   if (db) db_kernel<<<(unsigned)K, 256, 0, st>>>(dy, db, g);
   cudaError_t e = cudaGetLastError();
