@@ -443,7 +443,8 @@ def run_ours(args, rank, world, local_rank):
             graph_replay = {"error": str(exc)[:200]}
 
     # parity sample (checked in the cpu_baseline leg on rank 0 at N=1)
-    ksamp = min(physical_cores()[0], 8)
+    # two images per physical core: every host thread of the CPU leg has work (8 images on 16 cores timed half the box)
+    ksamp = min(n, max(8, 2 * physical_cores()[0]))
     x_s = x[:ksamp].cpu().numpy() if groups == "image" else x.cpu().numpy()
     y_s = y[:ksamp].cpu().numpy() if groups == "image" else y.cpu().numpy()
     w_s = w.cpu().numpy()
