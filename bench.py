@@ -244,6 +244,7 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": val, "unit": "images/s", "cores": cores, "logical_cpus": logical, "kind": "port",
                          "sample": f"{cores} images per step (one per physical core), per-image reference calls"},
         "e2e": {"value": val, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,  # the reference arm is the CPU path by definition
     }
     print(json.dumps(line), flush=True)
 
