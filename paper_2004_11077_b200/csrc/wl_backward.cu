@@ -225,22 +225,27 @@ __global__ void __launch_bounds__(256) dx_gather_kernel(const float* __restrict_
   const float* base = dxt + (size_t)n * g.TP * tstride + c;
   const int up = g.tw * tstride - 24 * g.C, left = tstride - 4 * g.C;  // one tile up: i + 4; left: j + 4
   float v[PQ][4];
+  // (row, col) of this thread's first pixel once, then stepped by 8 pixels: no division per pixel; 32-bit
+  // element offsets inside the image's dxt block (TP * 36 * C floats < 2^31, host-checked); the kernel was
+  // issue-bound at 85 % issue-active
+  int row = (p0 + grp) / g.W, col = (p0 + grp) - row * g.W;
 #pragma unroll
   for (int q = 0; q < PQ; ++q) {
     const int p = p0 + grp + 8 * q;
     v[q][0] = v[q][1] = v[q][2] = v[q][3] = 0.f;
     if (c < g.C && p < HW) {
-      const int row = p / g.W, col = p - row * g.W;
       const int rp = row + g.pad, cp = col + g.pad;
       const int tyA = rp >> 2, iA = rp & 3, txA = cp >> 2, jA = cp & 3;
       const bool vA = tyA < g.th, vB = iA <= 1 && tyA >= 1 && tyA - 1 < g.th;
       const bool wA = txA < g.tw, wB = jA <= 1 && txA >= 1 && txA - 1 < g.tw;
-      const float* pa = base + ((size_t)(tyA * g.tw + txA) * tstride + (size_t)((6 * iA + jA) * g.C));  // tile (tyA, txA)
-      if (vB && wB) v[q][0] = __ldg(pa - up - left);
-      if (vB && wA) v[q][1] = __ldg(pa - up);
-      if (vA && wB) v[q][2] = __ldg(pa - left);
-      if (vA && wA) v[q][3] = __ldg(pa);
+      const int oa = (tyA * g.tw + txA) * tstride + (6 * iA + jA) * g.C;  // tile (tyA, txA)
+      if (vB && wB) v[q][0] = __ldg(base + (oa - up - left));
+      if (vB && wA) v[q][1] = __ldg(base + (oa - up));
+      if (vA && wB) v[q][2] = __ldg(base + (oa - left));
+      if (vA && wA) v[q][3] = __ldg(base + oa);
     }
+    col += 8;
+    while (col >= g.W) col -= g.W, ++row;
   }
 #pragma unroll
   for (int q = 0; q < PQ; ++q) sm[grp + 8 * q][lane] = ((v[q][0] + v[q][1]) + v[q][2]) + v[q][3];
