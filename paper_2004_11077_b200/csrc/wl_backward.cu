@@ -29,9 +29,17 @@ namespace wl {
 namespace bw {
 
 // canonical F(4,3) matrices (the reference's A, B^T, G; construct.py:161-181)
-__constant__ float kAT[4][6] = {{1, 1, 1, 1, 1, 0}, {0, 1, -1, 2, -2, 0}, {0, 1, 1, 4, 4, 0}, {0, 1, -1, 8, -8, 1}};
-__constant__ float kBT[6][6] = {{4, 0, -5, 0, 1, 0},  {0, -4, -4, 1, 1, 0}, {0, 4, -4, -1, 1, 0},
-                                {0, -2, -1, 2, 1, 0}, {0, 2, -1, -2, 1, 0}, {0, 4, 0, -5, 0, 1}};
+// compile-time coefficients: the unrolled sandwiches drop the zero terms (a third of A's and half of B's
+// entries; fma(x, 0, s) cannot be folded by the compiler because of NaN / Inf semantics)
+__host__ __device__ constexpr float kAT(int i, int j) {
+  constexpr float v[4][6] = {{1, 1, 1, 1, 1, 0}, {0, 1, -1, 2, -2, 0}, {0, 1, 1, 4, 4, 0}, {0, 1, -1, 8, -8, 1}};
+  return v[i][j];
+}
+__host__ __device__ constexpr float kBT(int i, int j) {
+  constexpr float v[6][6] = {{4, 0, -5, 0, 1, 0},  {0, -4, -4, 1, 1, 0}, {0, 4, -4, -1, 1, 0},
+                             {0, -2, -1, 2, 1, 0}, {0, 2, -1, -2, 1, 0}, {0, 4, 0, -5, 0, 1}};
+  return v[i][j];
+}
 __constant__ double kG[6][3] = {{0.25, 0, 0},
                                 {-1.0 / 6, -1.0 / 6, -1.0 / 6},
                                 {-1.0 / 6, 1.0 / 6, -1.0 / 6},
@@ -73,7 +81,8 @@ __device__ __forceinline__ void dm_tile(const float* __restrict__ dy, const BwGe
     for (int j = 0; j < 6; ++j) {
       float s = 0.f;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) s = fmaf(Y[a][b], kAT[b][j], s);
+      for (int b = 0; b < 4; ++b)
+        if (kAT(b, j) != 0.f) s = fmaf(Y[a][b], kAT(b, j), s);
       tmp[a][j] = s;
     }
 #pragma unroll
@@ -82,7 +91,8 @@ __device__ __forceinline__ void dm_tile(const float* __restrict__ dy, const BwGe
     for (int j = 0; j < 6; ++j) {
       float s = 0.f;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) s = fmaf(kAT[a][i], tmp[a][j], s);
+      for (int a = 0; a < 4; ++a)
+        if (kAT(a, i) != 0.f) s = fmaf(kAT(a, i), tmp[a][j], s);
       out[6 * i + j] = s;
     }
 }
@@ -193,7 +203,8 @@ __global__ void dxt_kernel(const float* __restrict__ dv, float* __restrict__ dxt
     for (int j = 0; j < 6; ++j) {
       float s = 0.f;
 #pragma unroll
-      for (int b = 0; b < 6; ++b) s = fmaf(D[a][b], kBT[b][j], s);
+      for (int b = 0; b < 6; ++b)
+        if (kBT(b, j) != 0.f) s = fmaf(D[a][b], kBT(b, j), s);
       tmp[a][j] = s;
     }
 #pragma unroll
@@ -202,7 +213,8 @@ __global__ void dxt_kernel(const float* __restrict__ dv, float* __restrict__ dxt
     for (int j = 0; j < 6; ++j) {
       float s = 0.f;
 #pragma unroll
-      for (int a = 0; a < 6; ++a) s = fmaf(kBT[a][i], tmp[a][j], s);
+      for (int a = 0; a < 6; ++a)
+        if (kBT(a, i) != 0.f) s = fmaf(kBT(a, i), tmp[a][j], s);
       dxt[((size_t)t * 36 + 6 * i + j) * g.C + c] = su * s;
     }
 }
