@@ -150,38 +150,44 @@ __global__ void dm_cols_kernel(const float* __restrict__ dy, __nv_bfloat16* __re
 }
 
 // Codes [rows][36][Cp] int8 -> bf16 [36][C][rows_pad] (exact), rows >= `rows` zero: the GEMM operands U^T
-// (rows = K) and V^T (rows = T).  Block = 64 rows x 64 channels of one Winograd element: 32-bit loads along the
-// channels, a word-pitched shared tile, and per thread four consecutive rows of one channel leave as one 8-byte
-// store (a channel's 64 rows are one 128-byte run).  The byte-per-thread version was issue-bound (81 % issue
-// slots, 69 us on 16384 x 64 codes).
+// (rows = K) and V^T (rows = T).  Block = 64 rows x 64 channels of one Winograd element: one 16-byte load per
+// thread along the channels into a word-pitched shared tile; then a thread takes 4 rows x 4 channels (four
+// 32-bit shared reads, conflict-free), converts bytes straight out of the words and stores, per channel, its
+// four rows as one 8-byte piece (8 lanes = 64 bytes of a channel's row run).  3.6 instructions per code; the
+// byte-per-thread version ran at 81 % issue-active (69 us on 16384 x 64 codes).
 __global__ void __launch_bounds__(256) codes_t_kernel(const int8_t* __restrict__ codes, __nv_bfloat16* __restrict__ out,
                                                       int rows, int rows_pad, int C, int Cp) {
   __shared__ uint32_t sm[64][17];
   const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64, e = blockIdx.z;
-#pragma unroll
-  for (int i = threadIdx.x; i < 64 * 16; i += 256) {
-    const int rr = i >> 4, cw = i & 15;
-    const int r = r0 + rr, c = c0 + 4 * cw;
-    uint32_t v = 0;
-    if (r < rows && c < Cp) v = __ldg(reinterpret_cast<const uint32_t*>(codes + ((size_t)r * 36 + e) * Cp + c));
-    sm[rr][cw] = v;
+  {
+    const int rr = threadIdx.x >> 2, ch = threadIdx.x & 3;  // row of the tile, 16-channel chunk
+    const int r = r0 + rr, c = c0 + 16 * ch;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (r < rows && c < Cp) v = __ldg(reinterpret_cast<const uint4*>(codes + ((size_t)r * 36 + e) * Cp + c));
+    sm[rr][4 * ch + 0] = v.x;
+    sm[rr][4 * ch + 1] = v.y;
+    sm[rr][4 * ch + 2] = v.z;
+    sm[rr][4 * ch + 3] = v.w;
   }
   __syncthreads();
-  const int8_t* smb = reinterpret_cast<const int8_t*>(&sm[0][0]);
+  // lane -> (8 row quads, 4 channel words): shared bank = (4 * r4 + cw) mod 32, all distinct
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r4 = (lane & 7) + 8 * (warp & 1), cw = (lane >> 3) + 4 * (warp >> 1);
+  uint32_t w[4];
 #pragma unroll
-  for (int i = threadIdx.x; i < 64 * 16; i += 256) {
-    const int cc = i >> 4, r4 = i & 15;
-    const int c = c0 + cc;
+  for (int i = 0; i < 4; ++i) w[i] = sm[4 * r4 + i][cw];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = c0 + 4 * cw + j;
     if (c < C) {
-      __nv_bfloat162 lo, hi;
-      lo.x = __float2bfloat16_rn((float)smb[(4 * r4 + 0) * 68 + cc]);
-      lo.y = __float2bfloat16_rn((float)smb[(4 * r4 + 1) * 68 + cc]);
-      hi.x = __float2bfloat16_rn((float)smb[(4 * r4 + 2) * 68 + cc]);
-      hi.y = __float2bfloat16_rn((float)smb[(4 * r4 + 3) * 68 + cc]);
-      uint2 w;
-      w.x = *reinterpret_cast<uint32_t*>(&lo);
-      w.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(out + ((size_t)e * C + c) * rows_pad + r0 + 4 * r4) = w;
+      float f[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) f[i] = (float)(int)(int8_t)(w[i] >> (8 * j));
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]), hi = __floats2bfloat162_rn(f[2], f[3]);
+      uint2 o;
+      o.x = *reinterpret_cast<const uint32_t*>(&lo);
+      o.y = *reinterpret_cast<const uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(out + ((size_t)e * C + c) * rows_pad + r0 + 4 * r4) = o;
     }
   }
 }
